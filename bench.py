@@ -1,0 +1,366 @@
+#!/usr/bin/env python
+"""bench.py — seconds per ALS iteration (X half-sweep + Theta half-sweep) on the
+Netflix-shape synthetic workload (480,189 x 17,770, 99M ratings, 10% holdout, f=100,
+lambda=0.05), BASELINE.json's metric.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config netflix]
+
+N>1 runs under torchrun, one rank per GPU: rows of X (then Theta) are model-partitioned
+over the ranks with the other factor replicated, and the solved slices are all-gathered
+over NCCL after each half. Timing: CUDA events on the launching stream
+between barriers + synchronize, max over ranks. Inputs (CSR 713 MB, CSC 713 MB) exceed L2,
+so no explicit flush is needed.
+
+Extra keys: roofline (fused half-sweep kernel vs the measured FP32 FFMA peak), cpu_baseline
+(the UNMODIFIED reference compiled into oracle/_ref, timed on this host's cores on a bounded
+row sample, extrapolated by nonzeros), e2e (the same metric through the host-buffer C ABI:
+alsk_update_x / alsk_update_theta on pinned host buffers, H2D + D2H inside the timed region).
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+CONFIGS = {
+    # name: (m, n, nnz_total, f, lambda)
+    "ml1m": (6040, 3706, 1000209, 10, 0.05),
+    "netflix": (480189, 17770, 99_000_000, 100, 0.05),
+    "yahoo": (1000990, 624961, 252_800_000, 100, 1.4),
+}
+SHAPE_ID = {"ml1m": 0, "netflix": 1, "yahoo": 2}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="netflix", choices=list(CONFIGS))
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+def make_data(cfg_name):
+    """Deterministic synthetic ratings + the reference driver's split (driver.hpp:113)."""
+    from paper_1603_03820_b200 import alskit as A
+    m, n, nnz, f, lam = CONFIGS[cfg_name]
+    R = A.synth_csr(m, n, nnz, A.mix_seed(42, 100 + SHAPE_ID[cfg_name]))
+    sp = A.split_train_test(R, 0.1, A.mix_seed(42, 2))
+    return sp.train, sp.test
+
+
+# ------------------------------------------------------------------ clocks ---------
+class Clocks:
+    def __init__(self, out: Path):
+        self.out = out
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.f = open(self.out, "w")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "--query-gpu=index,clocks.sm,clocks.max.sm,power.draw,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "200"], stdout=self.f, stderr=subprocess.DEVNULL)
+        except (OSError, FileNotFoundError):
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            self.proc.wait(timeout=5)
+            self.f.close()
+
+    def summary(self, device_index=0):
+        try:
+            rows = [l.split(",") for l in self.out.read_text().splitlines() if l.strip()]
+        except OSError:
+            return None
+        rows = [[c.strip() for c in r] for r in rows if len(r) >= 8 and r[0].strip() == str(device_index)]
+        if not rows:
+            return None
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = max(float(r[2]) for r in rows)
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[4 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx, "reasons": reasons,
+                "samples": len(rows)}
+
+
+# ------------------------------------------------------------------ reference arm --
+def cpu_reference_sample(train, test, cfg_name, target_s=12.0):
+    """Time the UNMODIFIED reference (oracle/_ref) update_x on all host threads, on a row
+    sample of each half, extrapolated to a full iteration by nonzero count. Only the
+    cpu_baseline leg / --impl reference may run this."""
+    from oracle import binding
+    from paper_1603_03820_b200 import alskit as A
+    ref = binding.reference()
+    if ref is None:
+        return None
+    m, n, nnz, f, lam = CONFIGS[cfg_name]
+    threads = ref.hardware_threads()
+    csc = A.csr_to_csc(train) if A.device_available() else None
+    if csc is None:
+        st, cp, ri, vv = binding.oracle().csr_to_csc(binding.csr_struct(m, n, train.row_ptr, train.col_idx, train.values))
+        rt = (cp, ri, vv)
+    else:
+        rt = (csc.col_ptr, csc.row_idx, csc.values)
+    x0 = A.random_factor(m, f, 42).entries
+    t0 = A.random_factor(n, f, A.mix_seed(42, 1)).entries
+
+    def sample(row_ptr, col_idx, values, rows, cols, theta, theta_rows, k):
+        rp = (row_ptr[: k + 1]).copy()
+        nz = int(rp[-1])
+        c = binding.csr_struct(k, cols, rp, col_idx[:nz].copy(), values[:nz].copy())
+        t = time.perf_counter()
+        st, _ = ref.update_x(c, theta, theta_rows, f, lam, acc_double=1, batch_rows=4096, threads=0)
+        dt = time.perf_counter() - t
+        assert st == 0, ref.last_error()
+        return dt, nz
+
+    # size the samples from a small probe so each half costs ~target_s/2
+    total_x = int(train.row_ptr[-1])
+    kx = max(64, min(m, 2000))
+    dx, nzx = sample(train.row_ptr, train.col_idx, train.values, m, n, t0, n, kx)
+    kx = int(min(m, max(kx, kx * (target_s / 2) / max(dx, 1e-3))))
+    dx, nzx = sample(train.row_ptr, train.col_idx, train.values, m, n, t0, n, kx)
+    kt = max(4, min(n, 40))
+    dt_, nzt = sample(rt[0], rt[1], rt[2], n, m, x0, m, kt)
+    kt = int(min(n, max(kt, kt * (target_s / 2) / max(dt_, 1e-3))))
+    dt_, nzt = sample(rt[0], rt[1], rt[2], n, m, x0, m, kt)
+    per_iter = dx * total_x / nzx + dt_ * total_x / nzt
+    return {"value": per_iter, "unit": "s/ALS-iter", "cores": threads, "kind": "reference",
+            "sample": f"reference update_x (accumulate_double, threads=0) on the first {kx} rows "
+                      f"({nzx} nnz) of the X-half and {kt} items ({nzt} nnz) of the Theta-half, "
+                      f"{dx:.2f}s + {dt_:.2f}s, extrapolated by nnz to {total_x} train ratings per half"}
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    train, test = make_data(args.config)
+    m, n, nnz, f, lam = CONFIGS[args.config]
+    vals = []
+    base = None
+    for i in range(args.warmup + args.steps):
+        b = cpu_reference_sample(train, test, args.config, target_s=8.0)
+        if b is None:
+            print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built (needs /root/reference at build time)"}))
+            return
+        if i >= args.warmup:
+            vals.append(b["value"])
+        base = b
+    v = float(np.median(vals))
+    base["value"] = v
+    print(json.dumps({
+        "impl": "reference", "metric": "s/ALS-iter (Netflix-shape f=100)", "value": v, "unit": "s/ALS-iter",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": v * 1e3,
+        "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64-accumulate",
+        "data": "synthetic", "config": {"workload": args.config, "m": m, "n": n, "nnz_total": nnz, "f": f,
+                                        "lambda": lam, "holdout": 0.1},
+        "cpu_baseline": base, "e2e": {"value": v, "unit": "s/ALS-iter", "h2d_bytes_per_step": 0,
+                                      "d2h_bytes_per_step": 0}}))
+
+
+# ------------------------------------------------------------------ our arm --------
+def fp32_peak_probe():
+    """Measured FFMA throughput of this device (TFLOP/s), from libalskit_cuda's probe kernel."""
+    from paper_1603_03820_b200 import _native as N
+    fn = getattr(N.LIB, "alsk_fp32_peak_probe", None)
+    if fn is None:
+        return None
+    fn.restype = C.c_double
+    fn.argtypes = []
+    return float(fn())
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+    from paper_1603_03820_b200 import _native as N
+    from paper_1603_03820_b200 import alskit as A
+    from paper_1603_03820_b200.session import DeviceCsr, dev_update, PREC_FP32
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    m, n, nnz, f, lam = CONFIGS[args.config]
+    train, test = make_data(args.config)
+    nz_train = int(train.row_ptr[-1])
+    R = DeviceCsr.from_host(train, dev)
+    RT = R.transpose()
+    # padded, equal-count row slices for the in-place all-gather (NCCL needs equal counts)
+    cx, ct = -(-m // world), -(-n // world)
+    X = torch.zeros(cx * world * f, dtype=torch.float32, device=dev)
+    T = torch.zeros(ct * world * f, dtype=torch.float32, device=dev)
+    X[: m * f].copy_(torch.from_numpy(A.random_factor(m, f, 42).entries))
+    T[: n * f].copy_(torch.from_numpy(A.random_factor(n, f, A.mix_seed(42, 1)).entries))
+    xr = (rank * cx, min(m, (rank + 1) * cx))
+    tr = (rank * ct, min(n, (rank + 1) * ct))
+
+    def half(Rd, theta, theta_rows, out, rows, chunk, rng):
+        if rng[1] > rng[0]:
+            dev_update(Rd, theta, theta_rows, f, lam, PREC_FP32, out[rng[0] * f:], rng[0], rng[1])
+        if world > 1:
+            dist.all_gather_into_tensor(out, out[rank * chunk * f:(rank + 1) * chunk * f])
+
+    def step():
+        half(R, T, n, X, m, cx, xr)
+        half(RT, X, m, T, n, ct, tr)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    launches0 = A.kernel_launch_count()
+    clocks = Clocks(ROOT / "gpurun_out" / f"clocks_rank{rank}.csv") if (ROOT / "gpurun_out").exists() else Clocks(Path(f"/tmp/clocks_rank{rank}.csv"))
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with clocks:
+        N.LIB.alsk_profile_begin()
+        torch.cuda.synchronize()
+        e0.record()
+        for _ in range(args.steps):
+            step()
+        e1.record()
+        torch.cuda.synchronize()
+        kms, kl = C.c_double(), C.c_uint64()
+        N.LIB.alsk_profile_end(C.byref(kms), C.byref(kl))
+    ms = e0.elapsed_time(e1) / args.steps
+    launches = A.kernel_launch_count() - launches0
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        dist.barrier()
+    # objective / RMSE after the run (reported, not timed)
+    rmse = None
+    if rank == 0 and test is not None:
+        out = C.c_double()
+        tt = np.ascontiguousarray(test)
+        rows = torch.from_numpy(tt["row"].copy()).to(dev)
+        cols = torch.from_numpy(tt["col"].copy()).to(dev)
+        vals = torch.from_numpy(tt["value"].copy()).to(dev)
+        A._check(N.LIB.alsk_dev_rmse(rows.data_ptr(), cols.data_ptr(), vals.data_ptr(), len(tt), X.data_ptr(), m,
+                                     T.data_ptr(), n, f, C.byref(out), torch.cuda.current_stream().cuda_stream))
+        rmse = out.value
+
+    result = None
+    if rank == 0:
+        flops_half = nz_train * (f * (f + 1) + 2 * f)  # Nz (f(f+1) + 2f) per half-sweep
+        kernel_ms = kms.value / max(kl.value, 1)
+        peak = fp32_peak_probe()
+        nominal = 148 * 128 * 2 * 1.965e9 / 1e12
+        per_launch_flops = flops_half / world
+        achieved = per_launch_flops / (kernel_ms * 1e-3) / 1e12
+        traffic = None
+        tf = ROOT / "profiles" / "traffic.json"
+        if tf.exists():
+            try:
+                traffic = json.loads(tf.read_text()).get(args.config)
+            except (OSError, ValueError):
+                traffic = None
+        result = {
+            "metric": f"s/ALS-iter ({args.config}-shape f={f})",
+            "value": ms / 1e3, "unit": "s/ALS-iter", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms, "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f32", "data": "synthetic (planted rank-10 + U[-0.5,0.5) noise; SURVEY §8(d) generator)",
+            "config": {"workload": args.config, "m": m, "n": n, "nnz_total": nnz, "nnz_train": nz_train, "f": f,
+                       "lambda": lam, "holdout": 0.1, "parallelism": f"model-parallel rows x{world} + NCCL all-gather"
+                       if world > 1 else "single GPU", "l2": "inputs > L2 (CSR+CSC 1.4 GB), no flush"},
+            "roofline": {"bound": "fp32-fma", "kernel": "fused_update_kernel<13> (hermitian+bias+cholesky+solve)",
+                         "achieved": achieved, "peak": peak if peak else nominal,
+                         "peak_source": "measured FFMA probe (alsk_fp32_peak_probe)" if peak else
+                         "nominal 148 SM x 128 FMA/clk x 2 x 1965 MHz (MEASURED_PEAKS.json has no FP32 entry)",
+                         "peak_nominal": nominal, "unit": "TFLOP/s",
+                         "frac": achieved / (peak if peak else nominal), "traffic": traffic,
+                         "flops_per_launch": per_launch_flops, "kernel_ms_avg": kernel_ms,
+                         "kernel_share_of_step": (kms.value / args.steps) / ms},
+            "gpu_launches": int(launches),
+            "test_rmse_after_run": rmse,
+        }
+        cs = clocks.summary(local)
+        if cs:
+            result["clocks"] = cs
+    if world > 1:
+        dist.barrier()
+    return result, train, test
+
+
+def run_e2e(args, train, test):
+    """Same metric through the host-buffer C ABI (reference-facing call): pinned host CSR, CSC
+    and factors; every step copies the inputs H2D and the solved factors D2H."""
+    import torch
+    from paper_1603_03820_b200 import _native as N
+    from paper_1603_03820_b200 import alskit as A
+    m, n, nnz, f, lam = CONFIGS[args.config]
+    csc = A.csr_to_csc(train)
+    pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()  # noqa: E731
+    rp, ci, vv = pin(train.row_ptr), pin(train.col_idx), pin(train.values)
+    cp, ri, cv = pin(csc.col_ptr), pin(csc.row_idx), pin(csc.values)
+    X = pin(A.random_factor(m, f, 42).entries)
+    T = pin(A.random_factor(n, f, A.mix_seed(42, 1)).entries)
+    nz = int(train.row_ptr[-1])
+    csr = N.CsrT(m, n, 0, nz, rp.data_ptr(), ci.data_ptr(), vv.data_ptr())
+    cfg = N.SolverConfigT(f, lam, 16, 4096, 0, 0, 42)
+
+    def step():
+        A._check(N.LIB.alsk_update_x(C.byref(csr), T.data_ptr(), n, f, C.byref(cfg), X.data_ptr()))
+        A._check(N.LIB.alsk_update_theta(m, n, nz, cp.data_ptr(), ri.data_ptr(), cv.data_ptr(), X.data_ptr(), m, f,
+                                         C.byref(cfg), T.data_ptr()))
+
+    for _ in range(max(1, args.warmup // 2)):
+        step()
+    steps = max(2, args.steps // 2)
+    t = time.perf_counter()
+    for _ in range(steps):
+        step()
+    sec = (time.perf_counter() - t) / steps
+    h2d = (rp.numel() * 8 + ci.numel() * 4 + vv.numel() * 4 + T.numel() * 4) + \
+          (cp.numel() * 8 + ri.numel() * 4 + cv.numel() * 4 + X.numel() * 4)
+    d2h = X.numel() * 4 + T.numel() * 4
+    return {"value": sec, "unit": "s/ALS-iter", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+            "path": "alsk_update_x + alsk_update_theta (host buffers, pinned), wall clock per step", "steps": steps}
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    out = run_ours(args)
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    result, train, test = out
+    if not args.no_e2e and world == 1:
+        result["e2e"] = run_e2e(args, train, test)
+    if not args.no_cpu and world == 1:
+        result["cpu_baseline"] = cpu_reference_sample(train, test, args.config)
+    print(json.dumps(result))
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,250 @@
+/*
+ * alskit_cuda.h — C ABI of the B200-native ALS hot path (libalskit_cuda.so).
+ *
+ * This is the drop-in boundary: plain C types, plain pointers and sizes, no torch and
+ * no C++ types. Every entry point replaces one function of the reference's header-only
+ * C++ API in /root/reference/proj/include/alskit (cited per entry as file:line). The
+ * C++ drop-in headers in include/alskit/*.hpp re-expose these under the reference's own
+ * names and signatures; ctypes/cffi bindings call them directly.
+ *
+ * Conventions
+ *  - Every function returns an alsk_status. On failure a thread-local message is
+ *    available from alsk_last_error(); the message text follows the reference's
+ *    exception text (tests match substrings such as "cholesky breakdown at batch index 1").
+ *  - Functions without the `_dev` suffix take HOST pointers and are synchronous
+ *    (H2D -> kernels -> D2H), exactly like the synchronous reference API.
+ *  - `_dev` functions take DEVICE pointers and a cudaStream_t (passed as void*; NULL =
+ *    legacy default stream). They enqueue work and synchronise only where a status must
+ *    be read back (input validation, Cholesky breakdown).
+ *  - Types follow common.hpp:14-20: index_t = int32_t, offset_t = int64_t, real_t = float.
+ *  - There is no CPU fallback: with no usable CUDA device every compute entry point
+ *    returns ALSK_ERR_CUDA.
+ */
+#ifndef ALSKIT_CUDA_H_
+#define ALSKIT_CUDA_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Error categories mirror alskit::Error::Category (common.hpp:24-64); the CLI exit codes
+ * for input/capacity/numerical/io are 2/3/4/5 (tools/alskit.cpp:23-31). */
+typedef enum alsk_status {
+    ALSK_OK = 0,
+    ALSK_ERR_INPUT = 1,     /* InputError     */
+    ALSK_ERR_CAPACITY = 2,  /* CapacityError  */
+    ALSK_ERR_NUMERICAL = 3, /* NumericalError */
+    ALSK_ERR_IO = 4,        /* IoError        */
+    ALSK_ERR_CUDA = 5       /* device / driver failure (no reference counterpart) */
+} alsk_status;
+
+/* BreakdownPolicy (solver.hpp:72). */
+typedef enum alsk_breakdown { ALSK_BREAKDOWN_FAIL = 0, ALSK_BREAKDOWN_ZERO_ROW = 1 } alsk_breakdown;
+
+/* Arithmetic of the Hermitian assembly + solve.
+ *  FP64_EXACT: reference order, double accumulators, double Cholesky with separately
+ *              rounded multiply/subtract — bit-identical to the reference's default
+ *              accumulate_double=true path (solver.hpp:99-157, 204-262).
+ *  FP32:       register-blocked FP32 accumulation fused with an FP32 in-register
+ *              Cholesky; tolerance-checked (normwise <= 1e-3 per half-sweep). */
+typedef enum alsk_precision { ALSK_PREC_FP64_EXACT = 0, ALSK_PREC_FP32 = 1 } alsk_precision;
+
+/* CsrMatrix (sparse.hpp:38-48). Pointers are host or device per function family. */
+typedef struct alsk_csr {
+    int64_t rows;
+    int64_t cols;
+    int64_t col_offset; /* first global column of a grid block (sparse.hpp:34-37) */
+    int64_t nnz;
+    const int64_t* row_ptr; /* rows+1 */
+    const int32_t* col_idx; /* nnz, GLOBAL column ids */
+    const float* values;    /* nnz */
+} alsk_csr;
+
+/* Triplet (sparse.hpp:17-23): {int64 row, int64 col, float value}, 24 bytes with padding. */
+typedef struct alsk_triplet {
+    int64_t row;
+    int64_t col;
+    float value;
+} alsk_triplet;
+
+/* SolverConfig (solver.hpp:61-69). `bin` and `threads` are accepted for API parity; the
+ * result never depends on them (solver.hpp:88-91). accumulate_double selects
+ * ALSK_PREC_FP64_EXACT (1) or ALSK_PREC_FP32 (0). */
+typedef struct alsk_solver_config {
+    int f;
+    double lambda;
+    int bin;
+    int64_t batch_rows;
+    int accumulate_double;
+    int threads;
+    uint64_t seed;
+} alsk_solver_config;
+
+/* ---- diagnostics ------------------------------------------------------------------- */
+const char* alsk_last_error(void);
+/* Batch index of the last Cholesky breakdown reported as ALSK_ERR_NUMERICAL (-1 if none). */
+int64_t alsk_last_breakdown_index(void);
+/* 1 when a CUDA device is usable in this process, else 0. */
+int alsk_device_available(void);
+/* Number of kernels this library has launched in this process (bench evidence). */
+uint64_t alsk_kernel_launch_count(void);
+const char* alsk_build_info(void);
+/* Kernel-only timing of the fused half-sweep kernel: between begin and end, every fused
+ * launch is bracketed by CUDA events on its stream; end returns the summed milliseconds
+ * and the number of launches timed. */
+void alsk_profile_begin(void);
+void alsk_profile_end(double* total_ms, uint64_t* launches);
+/* Measured FP32 FFMA throughput of the current device in TFLOP/s (roofline denominator). */
+double alsk_fp32_peak_probe(void);
+
+/* ---- host-buffer drop-in entry points (synchronous) ------------------------------- */
+
+/* get_hermitian_mo_into (solver.hpp:292-304): rows [row_begin,row_end) of r against
+ * theta (theta_rows x f) into a_out[(row_end-row_begin)*f*f], b_out[(..)*f].
+ * Also serves local_hermitian (parallel.hpp:412-421) when r->col_offset != 0. */
+alsk_status alsk_get_hermitian_mo_into(const alsk_csr* r, const float* theta, int64_t theta_rows,
+                                       int f, const alsk_solver_config* cfg, int64_t row_begin,
+                                       int64_t row_end, float* a_out, float* b_out);
+
+/* get_hermitian_base (solver.hpp:277-287): full batch, untiled reference entry point. */
+alsk_status alsk_get_hermitian_base(const alsk_csr* r, const float* theta, int64_t theta_rows,
+                                    int f, double lambda, int accumulate_double, float* a_out,
+                                    float* b_out);
+
+/* local_hermitian (parallel.hpp:412-421): no full-shape check, column range from
+ * r->col_offset .. col_offset+theta_rows. */
+alsk_status alsk_local_hermitian(const alsk_csr* block, const float* theta_part,
+                                 int64_t theta_rows, int f, const alsk_solver_config* cfg,
+                                 float* a_out, float* b_out);
+
+/* batch_solve (solver.hpp:320-325 -> batch_solve_into 204-262): double Cholesky in the
+ * reference's operation order (bit-identical). x_out[count*f]. */
+alsk_status alsk_batch_solve(const float* a, const float* b, int64_t count, int f,
+                             alsk_breakdown policy, float* x_out);
+
+/* update_x (solver.hpp:330-345). precision from cfg->accumulate_double. x_out[rows*f]. */
+alsk_status alsk_update_x(const alsk_csr* r, const float* theta, int64_t theta_rows, int f,
+                          const alsk_solver_config* cfg, float* x_out);
+
+/* update_theta (solver.hpp:349-352): CSC arrays (col_ptr, row_idx, values) of R
+ * (rows x cols) reinterpreted as the CSR of R^T without the copy transpose_of makes. */
+alsk_status alsk_update_theta(int64_t rows, int64_t cols, int64_t nnz, const int64_t* col_ptr,
+                              const int32_t* row_idx, const float* values, const float* x,
+                              int64_t x_rows, int f, const alsk_solver_config* cfg,
+                              float* theta_out);
+
+/* loss (solver.hpp:358-390) and rmse (solver.hpp:393-406); double accumulation. */
+alsk_status alsk_loss(const alsk_csr* r, const float* x, int64_t x_rows, const float* theta,
+                      int64_t theta_rows, int f, double lambda, double* out);
+alsk_status alsk_rmse(const alsk_triplet* test, int64_t count, const float* x, int64_t x_rows,
+                      const float* theta, int64_t theta_rows, int f, double* out);
+
+/* csr_to_csc (sparse.hpp:185-207) / csc_to_csr (209-231): stable transposes, bit-exact.
+ * Outputs are caller-allocated: col_ptr_out[cols+1], row_idx_out[nnz], values_out[nnz]. */
+alsk_status alsk_csr_to_csc(const alsk_csr* a, int64_t* col_ptr_out, int32_t* row_idx_out,
+                            float* values_out);
+alsk_status alsk_csc_to_csr(int64_t rows, int64_t cols, int64_t nnz, const int64_t* col_ptr,
+                            const int32_t* row_idx, const float* values, int64_t* row_ptr_out,
+                            int32_t* col_idx_out, float* values_out);
+
+/* csr_from_triplets (sparse.hpp:132-170): range check, (row,col) sort, duplicate check.
+ * row_ptr_out[m+1], col_idx_out[count], values_out[count]. */
+alsk_status alsk_csr_from_triplets(int64_t m, int64_t n, const alsk_triplet* t, int64_t count,
+                                   int64_t* row_ptr_out, int32_t* col_idx_out, float* values_out);
+
+/* grid_partition (sparse.hpp:250-314), two calls:
+ *  1) alsk_grid_partition_counts: row_cuts_out[q+1], col_cuts_out[p+1], block_nnz_out[p*q]
+ *     (block (i,j) at j*p+i) so the caller can size the blocks;
+ *  2) alsk_grid_partition_fill: block_row_ptr[b] (local_rows_j+1), block_col_idx[b],
+ *     block_values[b] — arrays of p*q caller-allocated host pointers. */
+alsk_status alsk_grid_partition_counts(const alsk_csr* r, int p, int q, int64_t* row_cuts_out,
+                                       int64_t* col_cuts_out, int64_t* block_nnz_out);
+alsk_status alsk_grid_partition_fill(const alsk_csr* r, int p, int q, int64_t* const* block_row_ptr,
+                                     int32_t* const* block_col_idx, float* const* block_values);
+
+/* parallel_reduce (parallel.hpp:474-477 -> reduce_batches 206-280) for the one-phase and
+ * two-phase schedules: slice i of the elementwise double sum of p partial batches
+ * (each count*(f*f) A + count*f B floats). parts_a/parts_b: p host pointers; the result
+ * for slice i goes to out_a[i]/out_b[i] sized per slice_cuts(count,p) (parallel.hpp:160-168).
+ * Summation order: own partial first, then sources ascending — the reference's order for
+ * the one-phase schedule; the two-phase schedule sums within groups first (same values up
+ * to double reassociation, rounded once to float). */
+alsk_status alsk_parallel_reduce(const float* const* parts_a, const float* const* parts_b, int p,
+                                 int64_t count, int f, const int32_t* group_of, int two_phase,
+                                 float* const* out_a, float* const* out_b);
+
+/* su_als_update_x (parallel.hpp:487-583): grid of p x q blocks (block (i,j) at j*p+i,
+ * host CSR with col_offset), theta partitions (partition i has col_cuts[i+1]-col_cuts[i]
+ * rows), reduce schedule from group_of/two_phase as in alsk_parallel_reduce. The capacity
+ * check (parallel.hpp:512-519) is the host planner's job. With accumulate_double the
+ * partial Hermitians stay double until the reduction and are rounded to float once.
+ * x_out[row_cuts[q]*f]. */
+alsk_status alsk_su_als_update_x(const alsk_csr* blocks, int p, int q, const int64_t* row_cuts,
+                                 const int64_t* col_cuts, const float* const* theta_parts, int f,
+                                 const alsk_solver_config* cfg, const int32_t* group_of,
+                                 int two_phase, float* x_out);
+
+/* ---- device-resident entry points (session / multi-GPU path) ---------------------- */
+
+/* Fused update of rows [row_begin,row_end) of r (device CSR) against theta (device),
+ * writing x rows into x_out + (row_begin-x_row_base)*f. The half-sweep of update_x.
+ * Returns ALSK_ERR_NUMERICAL on breakdown (after a stream sync of one 16-byte status). */
+alsk_status alsk_dev_update(const alsk_csr* r, const float* theta, int64_t theta_rows, int f,
+                            double lambda, alsk_precision precision, int64_t batch_rows,
+                            int64_t row_begin, int64_t row_end, float* x_out, void* stream);
+
+/* Partial Hermitian of rows [row_begin,row_end) in packed-lower double form for the
+ * data-parallel split: out[(row-row_begin)*(f*(f+1)/2 + f)] with lambda*n_local on the
+ * diagonal (parallel.hpp:408-411). */
+alsk_status alsk_dev_partial_hermitian(const alsk_csr* r, const float* theta, int64_t theta_rows,
+                                       int f, double lambda, int64_t row_begin, int64_t row_end,
+                                       double* out_packed, void* stream);
+/* Solve packed double systems (count of them) into x_out[count*f]. */
+alsk_status alsk_dev_solve_packed(const double* packed, int64_t count, int f, float* x_out,
+                                  void* stream);
+
+/* Device loss/rmse; result written to *out (host) after a stream sync. */
+alsk_status alsk_dev_loss(const alsk_csr* r, const int64_t* col_nnz, const float* x,
+                          const float* theta, int64_t theta_rows, int f, double lambda,
+                          double* out, void* stream);
+alsk_status alsk_dev_rmse(const int64_t* rows, const int64_t* cols, const float* values,
+                          int64_t count, const float* x, int64_t x_rows, const float* theta,
+                          int64_t theta_rows, int f, double* out, void* stream);
+
+/* Device stable transpose: CSR (device) -> CSC (device, caller-allocated). */
+alsk_status alsk_dev_csr_to_csc(const alsk_csr* a, int64_t* col_ptr_out, int32_t* row_idx_out,
+                                float* values_out, void* stream);
+
+/* Hermitian FP32 kernel alone (materialised A/B, device) — used to time the assembly
+ * against the FP32 roofline separately from the solve. */
+alsk_status alsk_dev_hermitian(const alsk_csr* r, const float* theta, int64_t theta_rows, int f,
+                               double lambda, alsk_precision precision, int64_t row_begin,
+                               int64_t row_end, float* a_out, float* b_out, void* stream);
+
+/* ---- host data helpers (dataio/factor restatements used by the drivers) ------------ */
+
+/* random_factor (factor.hpp:49-54) and mix_seed (common.hpp:70-75), bit-exact. */
+void alsk_random_factor(int64_t rows, int f, uint64_t seed, float* out);
+uint64_t alsk_mix_seed(uint64_t seed, uint64_t salt);
+
+/* split_train_test (dataio.hpp:251-290), bit-exact: two calls — the first returns the
+ * held-out count k and train nnz; the second fills caller buffers. */
+alsk_status alsk_split_train_test(const alsk_csr* r, double holdout, uint64_t seed,
+                                  int64_t* k_out, int64_t* train_row_ptr, int32_t* train_col_idx,
+                                  float* train_values, alsk_triplet* test_out);
+
+/* Deterministic synthetic generator: row degree
+ * floor(nnz(u+1)/m)-floor(nnz u/m), columns by Floyd sampling from mt19937_64(mix_seed(seed,u)),
+ * values from a planted rank-10 model + U[-0.5,0.5) noise. Row-parallel on host threads.
+ * Fills a CSR with exactly nnz entries. */
+alsk_status alsk_synth_csr(int64_t m, int64_t n, int64_t nnz, uint64_t seed, int threads,
+                           int64_t* row_ptr, int32_t* col_idx, float* values);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* ALSKIT_CUDA_H_ */

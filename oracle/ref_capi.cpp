@@ -1,0 +1,267 @@
+// ORACLE — TEST INFRASTRUCTURE ONLY (checker and CPU baseline, never the product).
+//
+// Compiles the UNMODIFIED reference headers from /root/reference/proj/include (path via
+// -I, namespace renamed with -Dalskit=alskit_ref) into oracle/_ref/libalskit_ref.so and
+// exposes them through plain-C entry points with the same buffer conventions as
+// include/alskit_cuda.h. No reference source is copied into this repository; the build
+// recipe is oracle/Makefile, outputs land only in oracle/_ref/ (git-ignored).
+#include <chrono>
+#include <cstdint>
+#include <cstring>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "alskit/alskit.hpp"  // from /root/reference/proj/include, namespace alskit_ref
+#include "alskit_cuda.h"
+
+namespace R = alskit_ref;
+
+namespace {
+
+thread_local std::string g_err;
+
+R::CsrMatrix to_csr(const alsk_csr* a) {
+    R::CsrMatrix m;
+    m.rows = a->rows;
+    m.cols = a->cols;
+    m.col_offset = a->col_offset;
+    m.row_ptr.assign(a->row_ptr, a->row_ptr + a->rows + 1);
+    m.col_idx.assign(a->col_idx, a->col_idx + a->nnz);
+    m.values.assign(a->values, a->values + a->nnz);
+    return m;
+}
+
+R::FactorMatrix to_factor(const float* p, int64_t rows, int f) {
+    R::FactorMatrix m(rows, f);
+    std::memcpy(m.entries.data(), p, sizeof(float) * rows * f);
+    return m;
+}
+
+R::SolverConfig to_cfg(double lambda, int acc_double, int64_t batch_rows, int threads) {
+    R::SolverConfig c;
+    c.lambda = lambda;
+    c.accumulate_double = acc_double != 0;
+    c.batch_rows = batch_rows;
+    c.threads = threads;
+    return c;
+}
+
+template <class Fn>
+alsk_status guarded(Fn&& fn) {
+    try {
+        fn();
+        return ALSK_OK;
+    } catch (const R::Error& e) {
+        g_err = e.what();
+        switch (e.category()) {
+            case R::Error::Category::input: return ALSK_ERR_INPUT;
+            case R::Error::Category::capacity: return ALSK_ERR_CAPACITY;
+            case R::Error::Category::numerical: return ALSK_ERR_NUMERICAL;
+            case R::Error::Category::io: return ALSK_ERR_IO;
+        }
+        return ALSK_ERR_INPUT;
+    }
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ref_last_error(void) { return g_err.c_str(); }
+int ref_hardware_threads(void) { return R::resolve_threads(0); }
+
+alsk_status ref_hermitian_mo(const alsk_csr* r, const float* theta, int64_t theta_rows, int f,
+                             double lambda, int acc_double, int bin, int64_t rb, int64_t re,
+                             float* A, float* B) {
+    return guarded([&] {
+        R::SolverConfig cfg = to_cfg(lambda, acc_double, 4096, 1);
+        cfg.bin = bin;
+        R::HermitianBatch out;
+        R::get_hermitian_mo_into(to_csr(r), to_factor(theta, theta_rows, f), cfg, rb, re, out);
+        std::memcpy(A, out.a.data(), sizeof(float) * out.a.size());
+        std::memcpy(B, out.b.data(), sizeof(float) * out.b.size());
+    });
+}
+
+alsk_status ref_local_hermitian(const alsk_csr* r, const float* theta, int64_t theta_rows, int f,
+                                double lambda, int acc_double, float* A, float* B) {
+    return guarded([&] {
+        const R::HermitianBatch out = R::local_hermitian(to_csr(r), to_factor(theta, theta_rows, f),
+                                                         to_cfg(lambda, acc_double, 4096, 1));
+        std::memcpy(A, out.a.data(), sizeof(float) * out.a.size());
+        std::memcpy(B, out.b.data(), sizeof(float) * out.b.size());
+    });
+}
+
+alsk_status ref_batch_solve(const float* A, const float* B, int64_t count, int f, int zero_row,
+                            float* X) {
+    return guarded([&] {
+        R::HermitianBatch batch;
+        batch.resize(count, f);
+        std::memcpy(batch.a.data(), A, sizeof(float) * batch.a.size());
+        std::memcpy(batch.b.data(), B, sizeof(float) * batch.b.size());
+        const R::FactorMatrix x =
+            R::batch_solve(batch, zero_row ? R::BreakdownPolicy::zero_row : R::BreakdownPolicy::fail, 1);
+        std::memcpy(X, x.entries.data(), sizeof(float) * x.entries.size());
+    });
+}
+
+// update_x with the reference's own threading: threads=0 means hardware_concurrency
+// (thread_pool.hpp:20-24). This is also the CPU baseline arm of bench.py.
+alsk_status ref_update_x(const alsk_csr* r, const float* theta, int64_t theta_rows, int f,
+                         double lambda, int acc_double, int64_t batch_rows, int threads, float* X) {
+    return guarded([&] {
+        const R::FactorMatrix x = R::update_x(to_csr(r), to_factor(theta, theta_rows, f),
+                                              to_cfg(lambda, acc_double, batch_rows, threads));
+        std::memcpy(X, x.entries.data(), sizeof(float) * x.entries.size());
+    });
+}
+
+alsk_status ref_loss(const alsk_csr* r, const float* x, int64_t x_rows, const float* theta,
+                     int64_t theta_rows, int f, double lambda, double* out) {
+    return guarded([&] {
+        *out = R::loss(to_csr(r), to_factor(x, x_rows, f), to_factor(theta, theta_rows, f), lambda);
+    });
+}
+
+alsk_status ref_rmse(const alsk_triplet* t, int64_t count, const float* x, int64_t x_rows,
+                     const float* theta, int64_t theta_rows, int f, double* out) {
+    return guarded([&] {
+        std::vector<R::Triplet> test(static_cast<size_t>(count));
+        for (int64_t i = 0; i < count; ++i) test[i] = R::Triplet{t[i].row, t[i].col, t[i].value};
+        *out = R::rmse(test, to_factor(x, x_rows, f), to_factor(theta, theta_rows, f));
+    });
+}
+
+alsk_status ref_csr_to_csc(const alsk_csr* a, int64_t* col_ptr, int32_t* row_idx, float* vals) {
+    return guarded([&] {
+        const R::CscMatrix c = R::csr_to_csc(to_csr(a));
+        std::memcpy(col_ptr, c.col_ptr.data(), sizeof(int64_t) * c.col_ptr.size());
+        std::memcpy(row_idx, c.row_idx.data(), sizeof(int32_t) * c.row_idx.size());
+        std::memcpy(vals, c.values.data(), sizeof(float) * c.values.size());
+    });
+}
+
+alsk_status ref_csr_from_triplets(int64_t m, int64_t n, const alsk_triplet* t, int64_t count,
+                                  int64_t* row_ptr, int32_t* col_idx, float* vals) {
+    return guarded([&] {
+        std::vector<R::Triplet> tr(static_cast<size_t>(count));
+        for (int64_t i = 0; i < count; ++i) tr[i] = R::Triplet{t[i].row, t[i].col, t[i].value};
+        const R::CsrMatrix a = R::csr_from_triplets(m, n, tr);
+        std::memcpy(row_ptr, a.row_ptr.data(), sizeof(int64_t) * a.row_ptr.size());
+        std::memcpy(col_idx, a.col_idx.data(), sizeof(int32_t) * a.col_idx.size());
+        std::memcpy(vals, a.values.data(), sizeof(float) * a.values.size());
+    });
+}
+
+void ref_random_factor(int64_t rows, int f, uint64_t seed, float* out) {
+    const R::FactorMatrix x = R::random_factor(rows, f, seed);
+    std::memcpy(out, x.entries.data(), sizeof(float) * x.entries.size());
+}
+
+uint64_t ref_mix_seed(uint64_t seed, uint64_t salt) { return R::detail::mix_seed(seed, salt); }
+
+alsk_status ref_split_train_test(const alsk_csr* r, double holdout, uint64_t seed, int64_t* k_out,
+                                 int64_t* trp, int32_t* tci, float* tv, alsk_triplet* test) {
+    return guarded([&] {
+        const R::SplitResult s = R::split_train_test(to_csr(r), holdout, seed);
+        *k_out = static_cast<int64_t>(s.test.size());
+        if (!trp) return;
+        std::memcpy(trp, s.train.row_ptr.data(), sizeof(int64_t) * s.train.row_ptr.size());
+        std::memcpy(tci, s.train.col_idx.data(), sizeof(int32_t) * s.train.col_idx.size());
+        std::memcpy(tv, s.train.values.data(), sizeof(float) * s.train.values.size());
+        for (size_t i = 0; i < s.test.size(); ++i)
+            test[i] = alsk_triplet{s.test[i].row, s.test[i].col, s.test[i].value};
+    });
+}
+
+alsk_status ref_grid_partition_counts(const alsk_csr* r, int p, int q, int64_t* row_cuts,
+                                      int64_t* col_cuts, int64_t* block_nnz) {
+    return guarded([&] {
+        const R::GridPartition g = R::grid_partition(to_csr(r), p, q);
+        std::memcpy(row_cuts, g.row_cuts.data(), sizeof(int64_t) * g.row_cuts.size());
+        std::memcpy(col_cuts, g.col_cuts.data(), sizeof(int64_t) * g.col_cuts.size());
+        for (size_t b = 0; b < g.blocks.size(); ++b) block_nnz[b] = g.blocks[b].nnz();
+    });
+}
+
+alsk_status ref_grid_partition_fill(const alsk_csr* r, int p, int q, int64_t* const* brp,
+                                    int32_t* const* bci, float* const* bv) {
+    return guarded([&] {
+        const R::GridPartition g = R::grid_partition(to_csr(r), p, q);
+        for (size_t b = 0; b < g.blocks.size(); ++b) {
+            const R::CsrMatrix& blk = g.blocks[b];
+            std::memcpy(brp[b], blk.row_ptr.data(), sizeof(int64_t) * blk.row_ptr.size());
+            std::memcpy(bci[b], blk.col_idx.data(), sizeof(int32_t) * blk.col_idx.size());
+            std::memcpy(bv[b], blk.values.data(), sizeof(float) * blk.values.size());
+        }
+    });
+}
+
+// parallel_reduce over the reference's one-phase or two-phase schedule.
+alsk_status ref_parallel_reduce(const float* const* pa, const float* const* pb, int p,
+                                int64_t count, int f, const int32_t* group_of, int two_phase,
+                                float* const* oa, float* const* ob) {
+    return guarded([&] {
+        std::vector<R::HermitianBatch> parts(p);
+        for (int i = 0; i < p; ++i) {
+            parts[i].resize(count, f);
+            std::memcpy(parts[i].a.data(), pa[i], sizeof(float) * parts[i].a.size());
+            std::memcpy(parts[i].b.data(), pb[i], sizeof(float) * parts[i].b.size());
+        }
+        R::Topology topo;
+        topo.workers = p;
+        if (group_of) {
+            int ng = 0;
+            for (int i = 0; i < p; ++i) ng = std::max(ng, group_of[i] + 1);
+            topo.groups.assign(ng, {});
+            for (int i = 0; i < p; ++i) topo.groups[group_of[i]].push_back(i);
+        }
+        const R::ReduceSchedule sched = R::build_reduce_schedule(
+            topo, two_phase ? R::ReduceScheme::two_phase : R::ReduceScheme::one_phase);
+        const auto out = R::parallel_reduce(parts, sched, 1);
+        for (int i = 0; i < p; ++i) {
+            std::memcpy(oa[i], out[i].a.data(), sizeof(float) * out[i].a.size());
+            std::memcpy(ob[i], out[i].b.data(), sizeof(float) * out[i].b.size());
+        }
+    });
+}
+
+// su_als_update_x over a grid built by the reference itself from `r`.
+alsk_status ref_su_als_update_x(const alsk_csr* r, const float* theta, int64_t theta_rows, int f,
+                                int p, int q, double lambda, int acc_double, int two_phase,
+                                float* X) {
+    return guarded([&] {
+        const R::CsrMatrix rr = to_csr(r);
+        const R::GridPartition g = R::grid_partition(rr, p, q);
+        const auto parts = R::split_factor(to_factor(theta, theta_rows, f), g.col_cuts);
+        R::Topology topo;
+        topo.workers = p;
+        if (two_phase) {
+            topo.groups.assign(2, {});
+            for (int i = 0; i < p; ++i) topo.groups[i < p / 2 ? 0 : 1].push_back(i);
+        }
+        const R::FactorMatrix x = R::su_als_update_x(
+            g, parts, topo, two_phase ? R::ReduceScheme::two_phase : R::ReduceScheme::one_phase,
+            to_cfg(lambda, acc_double, 4096, 1));
+        std::memcpy(X, x.entries.data(), sizeof(float) * x.entries.size());
+    });
+}
+
+// Planner KAT (parallel.hpp:287-386)
+alsk_status ref_plan_partition(int64_t m, int64_t n, int64_t nnz, int f, int workers,
+                               int64_t capacity, int64_t headroom, int* p_out, int* q_out,
+                               int64_t* footprint_out) {
+    return guarded([&] {
+        R::Topology topo;
+        topo.workers = workers;
+        topo.capacity = capacity;
+        const R::PartitionPlan plan = R::plan_partition(m, n, nnz, f, topo, headroom);
+        *p_out = plan.p;
+        *q_out = plan.q;
+        *footprint_out = plan.per_worker_footprint;
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,656 @@
+// C ABI of libalskit_cuda.so (include/alskit_cuda.h). Host-buffer entry points stage
+// inputs to the device, run the kernels and copy results back, mirroring the synchronous
+// reference API; `_dev` entry points work on device pointers and a caller stream.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "alskit_cuda.h"
+#include "kernels.cuh"
+
+namespace alsk {
+
+std::atomic<uint64_t> g_launches{0};
+
+namespace {
+
+thread_local std::string t_error;
+thread_local int64_t t_breakdown = -1;
+
+// Kernel-only timing of the fused half-sweep kernel (CUDA events on the launching stream),
+// enabled by alsk_profile_begin; read by bench.py for the roofline figure.
+struct Profile {
+    bool on = false;
+    double ms = 0.0;
+    uint64_t launches = 0;
+} g_prof;
+
+template <class Fn>
+alsk_status guard(Fn&& fn) {
+    t_error.clear();
+    t_breakdown = -1;
+    try {
+        fn();
+        return ALSK_OK;
+    } catch (const Failure& e) {
+        t_error = e.what();
+        return e.status;
+    } catch (const std::bad_alloc&) {
+        t_error = "host allocation failed";
+        return ALSK_ERR_CAPACITY;
+    } catch (const std::exception& e) {
+        t_error = e.what();
+        return ALSK_ERR_CUDA;
+    }
+}
+
+// check_update_shapes (solver.hpp:76-81)
+void check_update_shapes(const alsk_csr* r, int64_t theta_rows, int f) {
+    if (r->col_offset == 0 && theta_rows != r->cols)
+        fail_input("factor rows " + std::to_string(theta_rows) + " do not match matrix columns " +
+                   std::to_string(r->cols));
+    if (f < 1) fail_input("rank must be >= 1");
+}
+
+// Device copy of a host CSR.
+struct StagedCsr {
+    DevBuf row_ptr, col_idx, values;
+    DevCsr view;
+    StagedCsr(const alsk_csr* h, cudaStream_t s) {
+        row_ptr.alloc(sizeof(int64_t) * (h->rows + 1), s);
+        col_idx.alloc(sizeof(int32_t) * std::max<int64_t>(h->nnz, 1), s);
+        values.alloc(sizeof(float) * std::max<int64_t>(h->nnz, 1), s);
+        h2d(row_ptr.as<int64_t>(), h->row_ptr, h->rows + 1, s);
+        h2d(col_idx.as<int32_t>(), h->col_idx, h->nnz, s);
+        h2d(values.as<float>(), h->values, h->nnz, s);
+        view.rows = h->rows;
+        view.cols = h->cols;
+        view.col_offset = h->col_offset;
+        view.nnz = h->nnz;
+        view.row_ptr = row_ptr.as<int64_t>();
+        view.col_idx = col_idx.as<int32_t>();
+        view.values = values.as<float>();
+    }
+};
+
+DevCsr dev_view(const alsk_csr* r) {
+    DevCsr v;
+    v.rows = r->rows;
+    v.cols = r->cols;
+    v.col_offset = r->col_offset;
+    v.nnz = r->nnz;
+    v.row_ptr = r->row_ptr;
+    v.col_idx = r->col_idx;
+    v.values = r->values;
+    return v;
+}
+
+struct StatusBufs {
+    DevBuf min_row, column, pivot;
+    SolveStatus st{};
+    StatusBufs(int64_t count, cudaStream_t s) {
+        min_row.alloc(sizeof(unsigned long long), s);
+        column.alloc(sizeof(int32_t) * std::max<int64_t>(count, 1), s);
+        pivot.alloc(sizeof(double) * std::max<int64_t>(count, 1), s);
+        ALSK_CUDA(cudaMemsetAsync(min_row.as<void>(), 0xff, sizeof(unsigned long long), s));
+        st.min_row = min_row.as<unsigned long long>();
+        st.column = column.as<int32_t>();
+        st.pivot = pivot.as<double>();
+    }
+    // Raise the reference's NumericalError (solver.hpp:232-235) if any row broke down.
+    // `index_base` is subtracted from the failing launch-relative row to get the batch
+    // index; batch_rows > 0 folds a global row into update_x's batch numbering.
+    void raise_if_broken(cudaStream_t s, int64_t batch_rows) {
+        unsigned long long bad = 0;
+        d2h(&bad, st.min_row, 1, s);
+        ALSK_CUDA(cudaStreamSynchronize(s));
+        if (bad == ~0ull) return;
+        int32_t col = 0;
+        double piv = 0.0;
+        d2h(&col, st.column + bad, 1, s);
+        d2h(&piv, st.pivot + bad, 1, s);
+        ALSK_CUDA(cudaStreamSynchronize(s));
+        const int64_t k = batch_rows > 0 ? static_cast<int64_t>(bad) % batch_rows : static_cast<int64_t>(bad);
+        t_breakdown = k;
+        fail_numerical("cholesky breakdown at batch index " + std::to_string(k) + " (pivot " +
+                       std::to_string(piv) + " at column " + std::to_string(col - 1) + ")");
+    }
+};
+
+// Rows per materialised batch so A stays within ~2 GiB of device memory.
+int64_t device_batch_rows(int f, int64_t rows) {
+    const int64_t per = static_cast<int64_t>(f) * f * 4 + static_cast<int64_t>(f) * 4 + 16;
+    return std::max<int64_t>(1, std::min<int64_t>(rows, (int64_t(2) << 30) / per));
+}
+
+// Core of update_x on device data: rows [rb,re) -> x_out (rows-local).
+void update_rows_device(const DevCsr& r, const float* theta, int64_t theta_rows, int f,
+                        double lambda, bool exact, int64_t batch_rows, int64_t rb, int64_t re,
+                        float* x_out, cudaStream_t s) {
+    if (re <= rb) return;
+    check_columns(r, rb, re, r.col_offset, r.col_offset + theta_rows, s);
+    StatusBufs sb(re - rb, s);
+    const int64_t br = batch_rows < 1 ? 1 : batch_rows;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (g_prof.on) {
+        ALSK_CUDA(cudaEventCreate(&e0));
+        ALSK_CUDA(cudaEventCreate(&e1));
+        ALSK_CUDA(cudaEventRecord(e0, s));
+    }
+    if (!exact && update_fused_fp32(r, theta, f, static_cast<float>(lambda), rb, re, x_out, sb.st, s)) {
+        if (g_prof.on) {
+            ALSK_CUDA(cudaEventRecord(e1, s));
+            ALSK_CUDA(cudaEventSynchronize(e1));
+            float ms = 0.f;
+            ALSK_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+            g_prof.ms += ms;
+            g_prof.launches += 1;
+            cudaEventDestroy(e0);
+            cudaEventDestroy(e1);
+        }
+        sb.raise_if_broken(s, br);
+        return;
+    }
+    if (e0) cudaEventDestroy(e0);
+    if (e1) cudaEventDestroy(e1);
+    const int64_t chunk = device_batch_rows(f, re - rb);
+    DevBuf A(sizeof(float) * chunk * f * f, s), B(sizeof(float) * chunk * f, s);
+    for (int64_t b0 = rb; b0 < re; b0 += chunk) {
+        const int64_t b1 = std::min(re, b0 + chunk);
+        hermitian_materialize(r, theta, f, lambda, exact, b0, b1, A.as<float>(), B.as<float>(), s);
+        SolveStatus st = sb.st;
+        st.column += (b0 - rb);
+        st.pivot += (b0 - rb);
+        // solve_exact reports launch-relative rows; shift by the batch offset
+        solve_exact(A.as<float>(), B.as<float>(), b1 - b0, f, false, x_out + (b0 - rb) * f, st, s);
+        if (b0 != rb) {
+            // re-base: min_row holds a launch-relative index; check per chunk
+        }
+        unsigned long long bad = 0;
+        d2h(&bad, sb.st.min_row, 1, s);
+        ALSK_CUDA(cudaStreamSynchronize(s));
+        if (bad != ~0ull) {
+            const int64_t global = (b0 - rb) + static_cast<int64_t>(bad);
+            int32_t col = 0;
+            double piv = 0.0;
+            d2h(&col, st.column + bad, 1, s);
+            d2h(&piv, st.pivot + bad, 1, s);
+            ALSK_CUDA(cudaStreamSynchronize(s));
+            const int64_t k = (rb + global) % br;
+            t_breakdown = k;
+            fail_numerical("cholesky breakdown at batch index " + std::to_string(k) + " (pivot " +
+                           std::to_string(piv) + " at column " + std::to_string(col - 1) + ")");
+        }
+    }
+}
+
+cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
+
+}  // namespace
+}  // namespace alsk
+
+using namespace alsk;
+
+extern "C" {
+
+const char* alsk_last_error(void) { return t_error.c_str(); }
+int64_t alsk_last_breakdown_index(void) { return t_breakdown; }
+int alsk_device_available(void) {
+    int n = 0;
+    return (cudaGetDeviceCount(&n) == cudaSuccess && n > 0) ? 1 : 0;
+}
+uint64_t alsk_kernel_launch_count(void) { return g_launches.load(); }
+void alsk_profile_begin(void) { g_prof = Profile{true, 0.0, 0}; }
+void alsk_profile_end(double* total_ms, uint64_t* launches) {
+    *total_ms = g_prof.ms;
+    *launches = g_prof.launches;
+    g_prof.on = false;
+}
+const char* alsk_build_info(void) {
+    return "libalskit_cuda (sm_100a; fused fp32 hermitian+cholesky, reference-order fp64 path, "
+           "radix-sort transposes)";
+}
+
+alsk_status alsk_get_hermitian_mo_into(const alsk_csr* r, const float* theta, int64_t theta_rows,
+                                       int f, const alsk_solver_config* cfg, int64_t row_begin,
+                                       int64_t row_end, float* a_out, float* b_out) {
+    return guard([&] {
+        check_update_shapes(r, theta_rows, f);
+        if (row_begin < 0 || row_end > r->rows || row_begin > row_end)
+            fail_input("row range [" + std::to_string(row_begin) + ", " + std::to_string(row_end) +
+                       ") outside matrix");
+        const int64_t count = row_end - row_begin;
+        if (count == 0) return;
+        require_device();
+        cudaStream_t s = nullptr;
+        StagedCsr R(r, s);
+        DevBuf T(sizeof(float) * std::max<int64_t>(theta_rows * f, 1), s);
+        h2d(T.as<float>(), theta, theta_rows * f, s);
+        check_columns(R.view, row_begin, row_end, r->col_offset, r->col_offset + theta_rows, s);
+        DevBuf A(sizeof(float) * count * f * f, s), B(sizeof(float) * count * f, s);
+        hermitian_materialize(R.view, T.as<float>(), f, cfg->lambda, cfg->accumulate_double != 0,
+                              row_begin, row_end, A.as<float>(), B.as<float>(), s);
+        d2h(a_out, A.as<float>(), count * f * f, s);
+        d2h(b_out, B.as<float>(), count * f, s);
+        ALSK_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
+alsk_status alsk_get_hermitian_base(const alsk_csr* r, const float* theta, int64_t theta_rows,
+                                    int f, double lambda, int accumulate_double, float* a_out,
+                                    float* b_out) {
+    alsk_solver_config cfg{};
+    cfg.lambda = lambda;
+    cfg.accumulate_double = accumulate_double;
+    return alsk_get_hermitian_mo_into(r, theta, theta_rows, f, &cfg, 0, r->rows, a_out, b_out);
+}
+
+alsk_status alsk_local_hermitian(const alsk_csr* block, const float* theta_part,
+                                 int64_t theta_rows, int f, const alsk_solver_config* cfg,
+                                 float* a_out, float* b_out) {
+    return guard([&] {
+        const int64_t count = block->rows;
+        if (count == 0) return;
+        require_device();
+        cudaStream_t s = nullptr;
+        StagedCsr R(block, s);
+        DevBuf T(sizeof(float) * std::max<int64_t>(theta_rows * f, 1), s);
+        h2d(T.as<float>(), theta_part, theta_rows * f, s);
+        check_columns(R.view, 0, count, block->col_offset, block->col_offset + theta_rows, s);
+        DevBuf A(sizeof(float) * count * f * f, s), B(sizeof(float) * count * f, s);
+        hermitian_materialize(R.view, T.as<float>(), f, cfg->lambda, cfg->accumulate_double != 0, 0,
+                              count, A.as<float>(), B.as<float>(), s);
+        d2h(a_out, A.as<float>(), count * f * f, s);
+        d2h(b_out, B.as<float>(), count * f, s);
+        ALSK_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
+alsk_status alsk_batch_solve(const float* a, const float* b, int64_t count, int f,
+                             alsk_breakdown policy, float* x_out) {
+    return guard([&] {
+        if (count == 0) return;
+        if (f < 1) fail_input("rank must be >= 1");
+        require_device();
+        cudaStream_t s = nullptr;
+        DevBuf A(sizeof(float) * count * f * f, s), B(sizeof(float) * count * f, s),
+            X(sizeof(float) * count * f, s);
+        h2d(A.as<float>(), a, count * f * f, s);
+        h2d(B.as<float>(), b, count * f, s);
+        StatusBufs sb(count, s);
+        solve_exact(A.as<float>(), B.as<float>(), count, f, policy == ALSK_BREAKDOWN_ZERO_ROW,
+                    X.as<float>(), sb.st, s);
+        if (policy == ALSK_BREAKDOWN_FAIL) sb.raise_if_broken(s, 0);
+        d2h(x_out, X.as<float>(), count * f, s);
+        ALSK_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
+alsk_status alsk_update_x(const alsk_csr* r, const float* theta, int64_t theta_rows, int f,
+                          const alsk_solver_config* cfg, float* x_out) {
+    return guard([&] {
+        check_update_shapes(r, theta_rows, f);
+        if (r->rows == 0) return;
+        require_device();
+        cudaStream_t s = nullptr;
+        StagedCsr R(r, s);
+        DevBuf T(sizeof(float) * std::max<int64_t>(theta_rows * f, 1), s);
+        h2d(T.as<float>(), theta, theta_rows * f, s);
+        DevBuf X(sizeof(float) * r->rows * f, s);
+        update_rows_device(R.view, T.as<float>(), theta_rows, f, cfg->lambda,
+                           cfg->accumulate_double != 0, cfg->batch_rows, 0, r->rows, X.as<float>(), s);
+        d2h(x_out, X.as<float>(), r->rows * f, s);
+        ALSK_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
+alsk_status alsk_update_theta(int64_t rows, int64_t cols, int64_t nnz, const int64_t* col_ptr,
+                              const int32_t* row_idx, const float* values, const float* x,
+                              int64_t x_rows, int f, const alsk_solver_config* cfg,
+                              float* theta_out) {
+    alsk_csr rt{};
+    rt.rows = cols;
+    rt.cols = rows;
+    rt.col_offset = 0;
+    rt.nnz = nnz;
+    rt.row_ptr = col_ptr;
+    rt.col_idx = row_idx;
+    rt.values = values;
+    return alsk_update_x(&rt, x, x_rows, f, cfg, theta_out);
+}
+
+alsk_status alsk_loss(const alsk_csr* r, const float* x, int64_t x_rows, const float* theta,
+                      int64_t theta_rows, int f, double lambda, double* out) {
+    return guard([&] {
+        if (x_rows != r->rows) fail_input("x rows do not match matrix rows");
+        check_update_shapes(r, theta_rows, f);
+        require_device();
+        cudaStream_t s = nullptr;
+        StagedCsr R(r, s);
+        DevBuf X(sizeof(float) * std::max<int64_t>(x_rows * f, 1), s);
+        DevBuf T(sizeof(float) * std::max<int64_t>(theta_rows * f, 1), s);
+        h2d(X.as<float>(), x, x_rows * f, s);
+        h2d(T.as<float>(), theta, theta_rows * f, s);
+        DevBuf cn(sizeof(int64_t) * std::max<int64_t>(r->cols, 1), s);
+        column_counts(R.view, cn.as<int64_t>(), s);
+        *out = loss_device(R.view, cn.as<int64_t>(), X.as<float>(), T.as<float>(), f, lambda, s);
+    });
+}
+
+alsk_status alsk_rmse(const alsk_triplet* test, int64_t count, const float* x, int64_t x_rows,
+                      const float* theta, int64_t theta_rows, int f, double* out) {
+    return guard([&] {
+        if (count <= 0) fail_input("empty test set");
+        require_device();
+        cudaStream_t s = nullptr;
+        std::vector<int64_t> hr(count), hc(count);
+        std::vector<float> hv(count);
+        for (int64_t i = 0; i < count; ++i) {
+            hr[i] = test[i].row;
+            hc[i] = test[i].col;
+            hv[i] = test[i].value;
+        }
+        DevBuf R(sizeof(int64_t) * count, s), C(sizeof(int64_t) * count, s), V(sizeof(float) * count, s);
+        h2d(R.as<int64_t>(), hr.data(), count, s);
+        h2d(C.as<int64_t>(), hc.data(), count, s);
+        h2d(V.as<float>(), hv.data(), count, s);
+        DevBuf X(sizeof(float) * std::max<int64_t>(x_rows * f, 1), s);
+        DevBuf T(sizeof(float) * std::max<int64_t>(theta_rows * f, 1), s);
+        h2d(X.as<float>(), x, x_rows * f, s);
+        h2d(T.as<float>(), theta, theta_rows * f, s);
+        *out = rmse_device(R.as<int64_t>(), C.as<int64_t>(), V.as<float>(), count, X.as<float>(),
+                           x_rows, T.as<float>(), theta_rows, f, s);
+    });
+}
+
+alsk_status alsk_csr_to_csc(const alsk_csr* a, int64_t* col_ptr_out, int32_t* row_idx_out,
+                            float* values_out) {
+    return guard([&] {
+        require_device();
+        cudaStream_t s = nullptr;
+        StagedCsr R(a, s);
+        DevBuf cp(sizeof(int64_t) * (a->cols + 1), s);
+        DevBuf ri(sizeof(int32_t) * std::max<int64_t>(a->nnz, 1), s);
+        DevBuf vv(sizeof(float) * std::max<int64_t>(a->nnz, 1), s);
+        csr_to_csc_device(R.view, cp.as<int64_t>(), ri.as<int32_t>(), vv.as<float>(), s);
+        d2h(col_ptr_out, cp.as<int64_t>(), a->cols + 1, s);
+        d2h(row_idx_out, ri.as<int32_t>(), a->nnz, s);
+        d2h(values_out, vv.as<float>(), a->nnz, s);
+        ALSK_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
+alsk_status alsk_csc_to_csr(int64_t rows, int64_t cols, int64_t nnz, const int64_t* col_ptr,
+                            const int32_t* row_idx, const float* values, int64_t* row_ptr_out,
+                            int32_t* col_idx_out, float* values_out) {
+    // The CSC of R is the CSR of R^T; its stable transpose is the CSR of R.
+    alsk_csr t{};
+    t.rows = cols;
+    t.cols = rows;
+    t.nnz = nnz;
+    t.row_ptr = col_ptr;
+    t.col_idx = row_idx;
+    t.values = values;
+    return alsk_csr_to_csc(&t, row_ptr_out, col_idx_out, values_out);
+}
+
+alsk_status alsk_csr_from_triplets(int64_t m, int64_t n, const alsk_triplet* t, int64_t count,
+                                   int64_t* row_ptr_out, int32_t* col_idx_out, float* values_out) {
+    return guard([&] {
+        if (m < 0 || n < 0) fail_input("matrix dimensions must be non-negative");
+        require_device();
+        cudaStream_t s = nullptr;
+        std::vector<int64_t> hr(std::max<int64_t>(count, 1)), hc(std::max<int64_t>(count, 1));
+        std::vector<float> hv(std::max<int64_t>(count, 1));
+        for (int64_t i = 0; i < count; ++i) {
+            hr[i] = t[i].row;
+            hc[i] = t[i].col;
+            hv[i] = t[i].value;
+        }
+        const int64_t cn = std::max<int64_t>(count, 1);
+        DevBuf R(sizeof(int64_t) * cn, s), C(sizeof(int64_t) * cn, s), V(sizeof(float) * cn, s);
+        h2d(R.as<int64_t>(), hr.data(), count, s);
+        h2d(C.as<int64_t>(), hc.data(), count, s);
+        h2d(V.as<float>(), hv.data(), count, s);
+        DevBuf rp(sizeof(int64_t) * (m + 1), s), ci(sizeof(int32_t) * cn, s), vv(sizeof(float) * cn, s);
+        csr_from_triplets_device(m, n, R.as<int64_t>(), C.as<int64_t>(), V.as<float>(), count,
+                                 rp.as<int64_t>(), ci.as<int32_t>(), vv.as<float>(), s);
+        d2h(row_ptr_out, rp.as<int64_t>(), m + 1, s);
+        d2h(col_idx_out, ci.as<int32_t>(), count, s);
+        d2h(values_out, vv.as<float>(), count, s);
+        ALSK_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
+alsk_status alsk_grid_partition_counts(const alsk_csr* r, int p, int q, int64_t* row_cuts_out,
+                                       int64_t* col_cuts_out, int64_t* block_nnz_out) {
+    return guard([&] {
+        require_device();
+        cudaStream_t s = nullptr;
+        StagedCsr R(r, s);
+        GridDevice g = grid_partition_device(R.view, p, q, s);
+        std::copy(g.row_cuts.begin(), g.row_cuts.end(), row_cuts_out);
+        std::copy(g.col_cuts.begin(), g.col_cuts.end(), col_cuts_out);
+        std::copy(g.block_nnz.begin(), g.block_nnz.end(), block_nnz_out);
+    });
+}
+
+alsk_status alsk_grid_partition_fill(const alsk_csr* r, int p, int q, int64_t* const* block_row_ptr,
+                                     int32_t* const* block_col_idx, float* const* block_values) {
+    return guard([&] {
+        require_device();
+        cudaStream_t s = nullptr;
+        StagedCsr R(r, s);
+        GridDevice g = grid_partition_device(R.view, p, q, s);
+        for (int j = 0; j < q; ++j)
+            for (int i = 0; i < p; ++i) {
+                const size_t b = static_cast<size_t>(j) * p + i;
+                const int64_t lr = g.row_cuts[j + 1] - g.row_cuts[j], nz = g.block_nnz[b];
+                DevBuf ci(sizeof(int32_t) * std::max<int64_t>(nz, 1), s), vv(sizeof(float) * std::max<int64_t>(nz, 1), s);
+                grid_fill_block(R.view, g, i, j, ci.as<int32_t>(), vv.as<float>(), s);
+                d2h(block_row_ptr[b], g.block_row_ptr[b].as<int64_t>(), lr + 1, s);
+                d2h(block_col_idx[b], ci.as<int32_t>(), nz, s);
+                d2h(block_values[b], vv.as<float>(), nz, s);
+                ALSK_CUDA(cudaStreamSynchronize(s));
+            }
+    });
+}
+
+alsk_status alsk_parallel_reduce(const float* const* parts_a, const float* const* parts_b, int p,
+                                 int64_t count, int f, const int32_t* group_of, int two_phase,
+                                 float* const* out_a, float* const* out_b) {
+    return guard([&] {
+        const ReduceSchedule sc = build_reduce_schedule(p, group_of, two_phase != 0);
+        require_device();
+        cudaStream_t s = nullptr;
+        const int64_t ff = static_cast<int64_t>(f) * f;
+        std::vector<DevBuf> da, db;
+        std::vector<const float*> pa, pb;
+        for (int w = 0; w < p; ++w) {
+            da.emplace_back(sizeof(float) * std::max<int64_t>(count * ff, 1), s);
+            db.emplace_back(sizeof(float) * std::max<int64_t>(count * f, 1), s);
+            h2d(da.back().as<float>(), parts_a[w], count * ff, s);
+            h2d(db.back().as<float>(), parts_b[w], count * f, s);
+            pa.push_back(da.back().as<float>());
+            pb.push_back(db.back().as<float>());
+        }
+        const auto cuts = slice_cuts(count, p);
+        std::vector<DevBuf> oa, ob;
+        std::vector<float*> poa, pob;
+        for (int w = 0; w < p; ++w) {
+            const int64_t n = cuts[w + 1] - cuts[w];
+            oa.emplace_back(sizeof(float) * std::max<int64_t>(n * ff, 1), s);
+            ob.emplace_back(sizeof(float) * std::max<int64_t>(n * f, 1), s);
+            poa.push_back(oa.back().as<float>());
+            pob.push_back(ob.back().as<float>());
+        }
+        reduce_slices<float>(pa, pb, count, f, sc, poa, pob, s);
+        for (int w = 0; w < p; ++w) {
+            const int64_t n = cuts[w + 1] - cuts[w];
+            d2h(out_a[w], poa[w], n * ff, s);
+            d2h(out_b[w], pob[w], n * f, s);
+        }
+        ALSK_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
+alsk_status alsk_su_als_update_x(const alsk_csr* blocks, int p, int q, const int64_t* row_cuts,
+                                 const int64_t* col_cuts, const float* const* theta_parts, int f,
+                                 const alsk_solver_config* cfg, const int32_t* group_of,
+                                 int two_phase, float* x_out) {
+    return guard([&] {
+        if (f < 1) fail_input("rank must be >= 1");
+        const ReduceSchedule sc = build_reduce_schedule(p, group_of, two_phase != 0);
+        require_device();
+        cudaStream_t s = nullptr;
+        const bool dbl = cfg->accumulate_double != 0;
+        const int64_t ff = static_cast<int64_t>(f) * f;
+        std::vector<DevBuf> theta(p);
+        for (int i = 0; i < p; ++i) {
+            const int64_t rows = col_cuts[i + 1] - col_cuts[i];
+            theta[i].alloc(sizeof(float) * std::max<int64_t>(rows * f, 1), s);
+            h2d(theta[i].as<float>(), theta_parts[i], rows * f, s);
+        }
+        const int64_t total_rows = row_cuts[q];
+        DevBuf X(sizeof(float) * std::max<int64_t>(total_rows * f, 1), s);
+        for (int j = 0; j < q; ++j) {  // sequential model-parallel loop (parallel.hpp:532)
+            const int64_t lr = row_cuts[j + 1] - row_cuts[j];
+            if (lr == 0) continue;
+            const size_t esz = dbl ? sizeof(double) : sizeof(float);
+            std::vector<DevBuf> pa(p), pb(p);
+            for (int i = 0; i < p; ++i) {
+                const alsk_csr* b = &blocks[static_cast<size_t>(j) * p + i];
+                StagedCsr Bk(b, s);
+                const int64_t want = col_cuts[i + 1] - col_cuts[i];
+                check_columns(Bk.view, 0, lr, b->col_offset, b->col_offset + want, s);
+                pa[i].alloc(esz * lr * ff, s);
+                pb[i].alloc(esz * lr * f, s);
+                if (dbl)
+                    hermitian_materialize_d(Bk.view, theta[i].as<float>(), f, cfg->lambda, true, 0, lr,
+                                            pa[i].as<double>(), pb[i].as<double>(), false, s);
+                else
+                    hermitian_materialize(Bk.view, theta[i].as<float>(), f, cfg->lambda, false, 0, lr,
+                                          pa[i].as<float>(), pb[i].as<float>(), s);
+                ALSK_CUDA(cudaStreamSynchronize(s));  // block staging freed at scope exit
+            }
+            const auto cuts = slice_cuts(lr, p);
+            std::vector<DevBuf> oa(p), ob(p);
+            std::vector<float*> poa, pob;
+            for (int i = 0; i < p; ++i) {
+                const int64_t n = cuts[i + 1] - cuts[i];
+                oa[i].alloc(sizeof(float) * std::max<int64_t>(n * ff, 1), s);
+                ob[i].alloc(sizeof(float) * std::max<int64_t>(n * f, 1), s);
+                poa.push_back(oa[i].as<float>());
+                pob.push_back(ob[i].as<float>());
+            }
+            if (dbl) {
+                std::vector<const double*> a, b;
+                for (int i = 0; i < p; ++i) { a.push_back(pa[i].as<double>()); b.push_back(pb[i].as<double>()); }
+                reduce_slices<double>(a, b, lr, f, sc, poa, pob, s);
+            } else {
+                std::vector<const float*> a, b;
+                for (int i = 0; i < p; ++i) { a.push_back(pa[i].as<float>()); b.push_back(pb[i].as<float>()); }
+                reduce_slices<float>(a, b, lr, f, sc, poa, pob, s);
+            }
+            for (int i = 0; i < p; ++i) {
+                const int64_t n = cuts[i + 1] - cuts[i];
+                if (n == 0) continue;
+                StatusBufs sb(n, s);
+                solve_exact(poa[i], pob[i], n, f, false, X.as<float>() + (row_cuts[j] + cuts[i]) * f, sb.st, s);
+                sb.raise_if_broken(s, 0);
+            }
+        }
+        d2h(x_out, X.as<float>(), total_rows * f, s);
+        ALSK_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
+// ---- device entry points ----------------------------------------------------------
+
+alsk_status alsk_dev_update(const alsk_csr* r, const float* theta, int64_t theta_rows, int f,
+                            double lambda, alsk_precision precision, int64_t batch_rows,
+                            int64_t row_begin, int64_t row_end, float* x_out, void* stream) {
+    return guard([&] {
+        check_update_shapes(r, theta_rows, f);
+        require_device();
+        update_rows_device(dev_view(r), theta, theta_rows, f, lambda, precision == ALSK_PREC_FP64_EXACT,
+                           batch_rows, row_begin, row_end, x_out, as_stream(stream));
+    });
+}
+
+alsk_status alsk_dev_hermitian(const alsk_csr* r, const float* theta, int64_t theta_rows, int f,
+                               double lambda, alsk_precision precision, int64_t row_begin,
+                               int64_t row_end, float* a_out, float* b_out, void* stream) {
+    return guard([&] {
+        check_update_shapes(r, theta_rows, f);
+        require_device();
+        const DevCsr v = dev_view(r);
+        if (precision == ALSK_PREC_FP32 &&
+            hermitian_fused_fp32(v, theta, f, static_cast<float>(lambda), row_begin, row_end, a_out,
+                                 b_out, as_stream(stream)))
+            return;
+        hermitian_materialize(v, theta, f, lambda, precision == ALSK_PREC_FP64_EXACT, row_begin,
+                              row_end, a_out, b_out, as_stream(stream));
+    });
+}
+
+alsk_status alsk_dev_loss(const alsk_csr* r, const int64_t* col_nnz, const float* x,
+                          const float* theta, int64_t theta_rows, int f, double lambda,
+                          double* out, void* stream) {
+    return guard([&] {
+        check_update_shapes(r, theta_rows, f);
+        require_device();
+        *out = loss_device(dev_view(r), col_nnz, x, theta, f, lambda, as_stream(stream));
+    });
+}
+
+alsk_status alsk_dev_rmse(const int64_t* rows, const int64_t* cols, const float* values,
+                          int64_t count, const float* x, int64_t x_rows, const float* theta,
+                          int64_t theta_rows, int f, double* out, void* stream) {
+    return guard([&] {
+        if (count <= 0) fail_input("empty test set");
+        require_device();
+        *out = rmse_device(rows, cols, values, count, x, x_rows, theta, theta_rows, f, as_stream(stream));
+    });
+}
+
+alsk_status alsk_dev_csr_to_csc(const alsk_csr* a, int64_t* col_ptr_out, int32_t* row_idx_out,
+                                float* values_out, void* stream) {
+    return guard([&] {
+        require_device();
+        csr_to_csc_device(dev_view(a), col_ptr_out, row_idx_out, values_out, as_stream(stream));
+    });
+}
+
+alsk_status alsk_dev_partial_hermitian(const alsk_csr* r, const float* theta, int64_t theta_rows,
+                                       int f, double lambda, int64_t row_begin, int64_t row_end,
+                                       double* out_packed, void* stream) {
+    return guard([&] {
+        if (f < 1) fail_input("rank must be >= 1");
+        require_device();
+        const DevCsr v = dev_view(r);
+        check_columns(v, row_begin, row_end, r->col_offset, r->col_offset + theta_rows, as_stream(stream));
+        hermitian_materialize_d(v, theta, f, lambda, true, row_begin, row_end, out_packed, nullptr, true,
+                                as_stream(stream));
+    });
+}
+
+alsk_status alsk_dev_solve_packed(const double* packed, int64_t count, int f, float* x_out, void* stream) {
+    return guard([&] {
+        if (count <= 0) return;
+        require_device();
+        cudaStream_t s = as_stream(stream);
+        DevBuf A(sizeof(float) * count * f * f, s), B(sizeof(float) * count * f, s);
+        unpack_packed(packed, count, f, A.as<float>(), B.as<float>(), s);
+        StatusBufs sb(count, s);
+        solve_exact(A.as<float>(), B.as<float>(), count, f, false, x_out, sb.st, s);
+        sb.raise_if_broken(s, 0);
+    });
+}
+
+}  // extern "C"

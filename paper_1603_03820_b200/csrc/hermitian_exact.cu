@@ -1,0 +1,313 @@
+// Reference-order Hermitian assembly (materialised) and reference-order batched Cholesky.
+//
+// These kernels reproduce the reference's default accumulate_double=true path bit for
+// bit: every A/B entry is one thread's sequential double sum over the row's nonzeros in
+// ascending order (a float*float product is exact in double, so FMA vs mul+add cannot
+// differ), lambda*n_u is added last on the diagonal and the result rounded once to float
+// (solver.hpp:99-157). The Cholesky is right-looking, but each entry still receives its
+// updates in ascending column order with separately rounded multiply and subtract, which
+// is exactly the left-looking order of batch_solve_into (solver.hpp:223-246).
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+
+#include "kernels.cuh"
+
+namespace alsk {
+namespace {
+
+constexpr int kChunk = 32;  // nonzeros staged per shared-memory tile
+
+// Lower-triangular tile enumeration: t -> (bi, bj), bj <= bi, row-major.
+__device__ __forceinline__ void tile_coords(int t, int& bi, int& bj) {
+    int b = 0;
+    while ((b + 1) * (b + 2) / 2 <= t) ++b;
+    bi = b;
+    bj = t - b * (b + 1) / 2;
+}
+
+// One CTA per row (grid.x) and tile pass (grid.y). Thread owns a TBxTB tile of the
+// augmented (f+1)x(f+1) lower triangle: row f of the augmented matrix is B = sum r*theta.
+template <class Acc, class OutT, int TB>
+__global__ void herm_mat_kernel(const int64_t* __restrict__ row_ptr,
+                                const int32_t* __restrict__ col_idx,
+                                const float* __restrict__ values, int64_t col_lo,
+                                const float* __restrict__ theta, int f, int nb, double lambda,
+                                int64_t rb, OutT* __restrict__ A, OutT* __restrict__ B, int packed) {
+    extern __shared__ float tile[];  // kChunk x fp
+    const int fp = nb * TB;
+    const int64_t u = rb + blockIdx.x;
+    const int64_t k0 = row_ptr[u], k1 = row_ptr[u + 1];
+    const int t = blockIdx.y * blockDim.x + threadIdx.x;
+    const int ntiles = nb * (nb + 1) / 2;
+    const bool active = t < ntiles;
+    int bi = 0, bj = 0;
+    if (active) tile_coords(t, bi, bj);
+
+    Acc acc[TB][TB];
+#pragma unroll
+    for (int i = 0; i < TB; ++i)
+#pragma unroll
+        for (int j = 0; j < TB; ++j) acc[i][j] = Acc(0);
+
+    for (int64_t k = k0; k < k1; k += kChunk) {
+        const int cnt = static_cast<int>(((k1 - k) < kChunk ? (k1 - k) : (int64_t)kChunk));
+        __syncthreads();
+        for (int e = threadIdx.x; e < cnt * fp; e += blockDim.x) {
+            const int kk = e / fp, c = e - kk * fp;
+            float v = 0.f;
+            if (c < f) {
+                const int64_t row = static_cast<int64_t>(col_idx[k + kk]) - col_lo;
+                v = theta[row * f + c];
+            } else if (c == f) {
+                v = values[k + kk];
+            }
+            tile[kk * fp + c] = v;
+        }
+        __syncthreads();
+        if (active) {
+            for (int kk = 0; kk < cnt; ++kk) {
+                const float* trow = tile + kk * fp;
+                Acc a[TB], b[TB];
+#pragma unroll
+                for (int i = 0; i < TB; ++i) a[i] = static_cast<Acc>(trow[bi * TB + i]);
+#pragma unroll
+                for (int j = 0; j < TB; ++j) b[j] = static_cast<Acc>(trow[bj * TB + j]);
+#pragma unroll
+                for (int i = 0; i < TB; ++i)
+#pragma unroll
+                    for (int j = 0; j < TB; ++j) acc[i][j] += a[i] * b[j];
+            }
+        }
+    }
+    if (!active) return;
+    const Acc reg = static_cast<Acc>(lambda) * static_cast<Acc>(k1 - k0);
+    const int64_t out_row = u - rb;
+    if (packed) {  // lower-packed A then B
+        OutT* o = A + out_row * (static_cast<int64_t>(f) * (f + 1) / 2 + f);
+#pragma unroll
+        for (int ii = 0; ii < TB; ++ii)
+#pragma unroll
+            for (int jj = 0; jj < TB; ++jj) {
+                const int i = bi * TB + ii, j = bj * TB + jj;
+                if (j > i || j >= f || i > f) continue;
+                o[i * (i + 1) / 2 + j] = static_cast<OutT>(i == j ? acc[ii][jj] + reg : acc[ii][jj]);
+            }
+        return;
+    }
+    OutT* a_out = A + out_row * static_cast<int64_t>(f) * f;
+    OutT* b_out = B + out_row * f;
+#pragma unroll
+    for (int ii = 0; ii < TB; ++ii) {
+#pragma unroll
+        for (int jj = 0; jj < TB; ++jj) {
+            const int i = bi * TB + ii, j = bj * TB + jj;
+            if (j > i || j >= f || i > f) continue;
+            if (i == f) {
+                b_out[j] = static_cast<OutT>(acc[ii][jj]);
+            } else if (i == j) {
+                a_out[i * f + i] = static_cast<OutT>(acc[ii][jj] + reg);
+            } else {
+                const OutT val = static_cast<OutT>(acc[ii][jj]);
+                a_out[i * f + j] = val;
+                a_out[j * f + i] = val;
+            }
+        }
+    }
+}
+
+__global__ void check_columns_kernel(const int64_t* __restrict__ row_ptr,
+                                     const int32_t* __restrict__ col_idx, int64_t kb, int64_t ke,
+                                     int64_t col_lo, int64_t col_hi,
+                                     unsigned long long* __restrict__ first_bad) {
+    for (int64_t k = kb + blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; k < ke;
+         k += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t v = col_idx[k];
+        if (v < col_lo || v >= col_hi) atomicMin(first_bad, static_cast<unsigned long long>(k));
+    }
+}
+
+// Packed lower-triangular index.
+__device__ __forceinline__ int pk(int i, int j) { return i * (i + 1) / 2 + j; }
+
+// One CTA per system. Shared: packed lower L (double), rhs/forward vector s (double),
+// x (float).
+__global__ void solve_exact_kernel(const float* __restrict__ A, const float* __restrict__ Bv,
+                                   int f, int64_t row_base, float* __restrict__ X,
+                                   unsigned long long* __restrict__ min_row,
+                                   int32_t* __restrict__ column, double* __restrict__ pivot) {
+    extern __shared__ double sm[];
+    double* L = sm;                        // f(f+1)/2
+    double* s = L + f * (f + 1) / 2;       // f
+    float* xs = reinterpret_cast<float*>(s + f);
+    __shared__ int s_flag;
+    __shared__ int s_broke;
+    const int64_t row = blockIdx.x;
+    const float* a = A + row * static_cast<int64_t>(f) * f;
+    const float* b = Bv + row * f;
+    float* x = X + row * f;
+    const int tid = threadIdx.x, nt = blockDim.x;
+
+    // all-zero test over the full f*f storage (solver.hpp:215-220)
+    int nonzero = 0;
+    for (int e = tid; e < f * f; e += nt) nonzero |= (a[e] != 0.0f);
+    if (tid == 0) s_broke = 0;
+    if (!__syncthreads_or(nonzero)) {
+        for (int i = tid; i < f; i += nt) x[i] = 0.0f;
+        if (tid == 0) column[row] = 0;
+        return;
+    }
+    for (int i = tid; i < f; i += nt) {
+        for (int j = 0; j <= i; ++j) L[pk(i, j)] = static_cast<double>(a[i * f + j]);
+        s[i] = static_cast<double>(b[i]);
+    }
+    __syncthreads();
+
+    for (int c = 0; c < f; ++c) {
+        if (tid == 0) {
+            const double d = L[pk(c, c)];
+            if (!(d > 0.0)) {
+                s_flag = 1;
+                column[row] = c + 1;
+                pivot[row] = d;
+                atomicMin(min_row, static_cast<unsigned long long>(row_base + row));
+            } else {
+                s_flag = 0;
+                L[pk(c, c)] = sqrt(d);
+            }
+        }
+        __syncthreads();
+        if (s_flag) {
+            s_broke = 1;
+            break;
+        }
+        const double lcc = L[pk(c, c)];
+        for (int r = c + 1 + tid; r < f; r += nt) L[pk(r, c)] = __ddiv_rn(L[pk(r, c)], lcc);
+        __syncthreads();
+        // trailing update, entry (r, q) with c < q <= r: warps over rows, lanes over q
+        const int warp = tid >> 5, lane = tid & 31, nw = nt >> 5;
+        for (int r = c + 1 + warp; r < f; r += nw) {
+            const double lrc = L[pk(r, c)];
+            for (int q = c + 1 + lane; q <= r; q += 32)
+                L[pk(r, q)] = __dsub_rn(L[pk(r, q)], __dmul_rn(lrc, L[pk(q, c)]));
+        }
+        __syncthreads();
+    }
+    if (s_broke) {
+        for (int i = tid; i < f; i += nt) x[i] = 0.0f;
+        return;
+    }
+    if (tid == 0) column[row] = 0;
+    // forward substitution, column oriented: s_i -= L[i][j]*y_j for j ascending
+    // (same per-entry order as the reference's row-oriented loop, solver.hpp:249-253).
+    if (tid < 32) {
+        for (int j = 0; j < f; ++j) {
+            const double yj = __ddiv_rn(s[j], L[pk(j, j)]);
+            __syncwarp();
+            if (tid == 0) s[j] = yj;
+            for (int i = j + 1 + tid; i < f; i += 32) s[i] = __dsub_rn(s[i], __dmul_rn(L[pk(i, j)], yj));
+            __syncwarp();
+        }
+        // back substitution reads the already-rounded float x[j] (solver.hpp:254-259);
+        // its order (j ascending from i+1) is inherently sequential.
+        if (tid == 0) {
+            for (int i = f - 1; i >= 0; --i) {
+                double acc = s[i];
+                for (int j = i + 1; j < f; ++j)
+                    acc = __dsub_rn(acc, __dmul_rn(L[pk(j, i)], static_cast<double>(xs[j])));
+                xs[i] = static_cast<float>(__ddiv_rn(acc, L[pk(i, i)]));
+            }
+        }
+        __syncwarp();
+        for (int i = tid; i < f; i += 32) x[i] = xs[i];
+    }
+}
+
+}  // namespace
+
+void check_columns(const DevCsr& r, int64_t rb, int64_t re, int64_t col_lo, int64_t col_hi,
+                   cudaStream_t s) {
+    if (re <= rb) return;
+    int64_t kb = 0, ke = 0;
+    d2h(&kb, r.row_ptr + rb, 1, s);
+    d2h(&ke, r.row_ptr + re, 1, s);
+    ALSK_CUDA(cudaStreamSynchronize(s));
+    if (ke <= kb) return;
+    DevBuf flag(sizeof(unsigned long long), s);
+    ALSK_CUDA(cudaMemsetAsync(flag.as<void>(), 0xff, sizeof(unsigned long long), s));
+    const int64_t n = ke - kb;
+    const int grid = static_cast<int>(std::min<int64_t>((n + 255) / 256, num_sms() * 8));
+    check_columns_kernel<<<grid, 256, 0, s>>>(r.row_ptr, r.col_idx, kb, ke, col_lo, col_hi,
+                                              flag.as<unsigned long long>());
+    ALSK_LAUNCHED();
+    unsigned long long bad = 0;
+    d2h(&bad, flag.as<unsigned long long>(), 1, s);
+    ALSK_CUDA(cudaStreamSynchronize(s));
+    if (bad != ~0ull) {
+        int32_t v = 0;
+        d2h(&v, r.col_idx + bad, 1, s);
+        ALSK_CUDA(cudaStreamSynchronize(s));
+        fail_input("column " + std::to_string(v) + " outside partition [" + std::to_string(col_lo) +
+                   ", " + std::to_string(col_hi) + ")");
+    }
+}
+
+namespace {
+template <class Acc, class OutT>
+void launch_herm(const DevCsr& r, const float* theta, int f, double lambda, int64_t rb, int64_t re,
+                 OutT* A, OutT* B, bool packed, cudaStream_t s) {
+    const int64_t count = re - rb;
+    if (count <= 0) return;
+    constexpr int TB = 4;
+    const int nb = (f + 1 + TB - 1) / TB;
+    const int ntiles = nb * (nb + 1) / 2;
+    const int threads = std::min(512, ((ntiles + 31) / 32) * 32);
+    const int passes = (ntiles + threads - 1) / threads;
+    const size_t smem = static_cast<size_t>(kChunk) * nb * TB * sizeof(float);
+    if (smem > 200 * 1024) fail_input("rank " + std::to_string(f) + " too large for device assembly");
+    auto k = herm_mat_kernel<Acc, OutT, TB>;
+    ALSK_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const int64_t per_a = packed ? static_cast<int64_t>(f) * (f + 1) / 2 + f : static_cast<int64_t>(f) * f;
+    for (int64_t b0 = 0; b0 < count; b0 += 65535 * 16) {
+        const int64_t n = std::min<int64_t>(count - b0, 65535 * 16);
+        dim3 grid(static_cast<unsigned>(n), static_cast<unsigned>(passes));
+        k<<<grid, threads, smem, s>>>(r.row_ptr, r.col_idx, r.values, r.col_offset, theta, f, nb, lambda,
+                                      rb + b0, A + b0 * per_a, packed ? nullptr : B + b0 * f, packed ? 1 : 0);
+        ALSK_LAUNCHED();
+    }
+}
+}  // namespace
+
+void hermitian_materialize(const DevCsr& r, const float* theta, int f, double lambda,
+                           bool acc_double, int64_t rb, int64_t re, float* A, float* B,
+                           cudaStream_t s) {
+    if (acc_double) launch_herm<double, float>(r, theta, f, lambda, rb, re, A, B, false, s);
+    else launch_herm<float, float>(r, theta, f, lambda, rb, re, A, B, false, s);
+}
+
+void hermitian_materialize_d(const DevCsr& r, const float* theta, int f, double lambda, bool acc_double,
+                             int64_t rb, int64_t re, double* A, double* B, bool packed, cudaStream_t s) {
+    if (acc_double) launch_herm<double, double>(r, theta, f, lambda, rb, re, A, B, packed, s);
+    else launch_herm<float, double>(r, theta, f, lambda, rb, re, A, B, packed, s);
+}
+
+void solve_exact(const float* A, const float* B, int64_t count, int f, bool /*zero_row_policy*/,
+                 float* X, const SolveStatus& st, cudaStream_t s) {
+    // Both policies write a zero row for a broken system; the host raises for `fail`.
+    if (count <= 0) return;
+    const size_t smem = (static_cast<size_t>(f) * (f + 1) / 2 + f) * sizeof(double) + f * sizeof(float) + 16;
+    if (smem > 220 * 1024) fail_input("rank " + std::to_string(f) + " too large for device solve");
+    ALSK_CUDA(cudaFuncSetAttribute(solve_exact_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const int threads = f <= 32 ? 32 : (f <= 64 ? 64 : 128);
+    for (int64_t b0 = 0; b0 < count; b0 += (1LL << 30)) {
+        const int64_t n = std::min<int64_t>(count - b0, 1LL << 30);
+        solve_exact_kernel<<<static_cast<unsigned>(n), threads, smem, s>>>(
+            A + static_cast<size_t>(b0) * f * f, B + static_cast<size_t>(b0) * f, f,
+            b0, X + static_cast<size_t>(b0) * f, st.min_row, st.column + b0,
+            st.pivot + b0);
+        ALSK_LAUNCHED();
+    }
+}
+
+}  // namespace alsk

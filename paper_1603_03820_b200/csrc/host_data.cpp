@@ -1,0 +1,181 @@
+// Host-side data helpers of libalskit_cuda.so: seeded factor init, the holdout split and
+// the deterministic synthetic generator. These are the reference's host routines on
+// either side of the hot path (factor.hpp, common.hpp, dataio.hpp); they are sequential
+// RNG streams by specification, so they stay on the host and are restated bit-exactly.
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <random>
+#include <stdexcept>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "alskit_cuda.h"
+
+namespace {
+
+// splitmix64 finaliser (common.hpp:70-75)
+inline uint64_t mix_seed(uint64_t seed, uint64_t salt) {
+    uint64_t z = seed + 0x9e3779b97f4a7c15ULL * (salt + 1);
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+    return z ^ (z >> 31);
+}
+
+// top 24 bits of one mt19937_64 draw scaled to [0,1) (factor.hpp:41-43)
+inline float uniform_unit(std::mt19937_64& rng) {
+    return static_cast<float>(rng() >> 40) * 0x1.0p-24f;
+}
+
+// rejection-sampled draw from [0, range) (dataio.hpp:103-109)
+inline uint64_t bounded_u64(std::mt19937_64& rng, uint64_t range) {
+    const uint64_t threshold = (0 - range) % range;
+    for (;;) {
+        const uint64_t v = rng();
+        if (v >= threshold) return v % range;
+    }
+}
+
+}  // namespace
+
+extern "C" {
+
+uint64_t alsk_mix_seed(uint64_t seed, uint64_t salt) { return mix_seed(seed, salt); }
+
+// random_factor (factor.hpp:49-54)
+void alsk_random_factor(int64_t rows, int f, uint64_t seed, float* out) {
+    std::mt19937_64 rng(seed);
+    const int64_t n = rows * static_cast<int64_t>(f);
+    for (int64_t i = 0; i < n; ++i) out[i] = uniform_unit(rng);
+}
+
+// split_train_test (dataio.hpp:251-290). Called twice: with train_row_ptr == nullptr it
+// only reports k (held-out count); the second call fills the caller's buffers.
+alsk_status alsk_split_train_test(const alsk_csr* r, double holdout, uint64_t seed, int64_t* k_out,
+                                  int64_t* train_row_ptr, int32_t* train_col_idx,
+                                  float* train_values, alsk_triplet* test_out) {
+    if (!(holdout > 0.0) || !(holdout < 1.0)) return ALSK_ERR_INPUT;
+    const int64_t nnz = r->nnz;
+    const int64_t k = static_cast<int64_t>(std::floor(holdout * static_cast<double>(nnz)));
+    *k_out = k;
+    if (train_row_ptr == nullptr) return ALSK_OK;
+    std::vector<int64_t> pos(static_cast<size_t>(nnz));
+    for (int64_t i = 0; i < nnz; ++i) pos[i] = i;
+    std::mt19937_64 rng(seed);
+    for (int64_t t = 0; t < k; ++t) {
+        const int64_t j = t + static_cast<int64_t>(bounded_u64(rng, static_cast<uint64_t>(nnz - t)));
+        std::swap(pos[t], pos[j]);
+    }
+    std::vector<char> held(static_cast<size_t>(nnz), 0);
+    for (int64_t t = 0; t < k; ++t) held[static_cast<size_t>(pos[t])] = 1;
+    int64_t tr = 0, te = 0;
+    train_row_ptr[0] = 0;
+    for (int64_t u = 0; u < r->rows; ++u) {
+        for (int64_t e = r->row_ptr[u]; e < r->row_ptr[u + 1]; ++e) {
+            if (held[e]) {
+                test_out[te].row = u;
+                test_out[te].col = r->col_idx[e];
+                test_out[te].value = r->values[e];
+                ++te;
+            } else {
+                train_col_idx[tr] = r->col_idx[e];
+                train_values[tr] = r->values[e];
+                ++tr;
+            }
+        }
+        train_row_ptr[u + 1] = tr;
+    }
+    return ALSK_OK;
+}
+
+// Deterministic synthetic ratings (our own generator, not a reference
+// routine). Row u gets d_u = floor(nnz(u+1)/m) - floor(nnz u/m) distinct columns drawn by
+// Floyd's algorithm from a SplitMix64 stream seeded with mix_seed(seed, u), sorted
+// ascending. Values follow a planted rank-10 model r = <x*_u, theta*_v> + U[-0.5, 0.5)
+// with x*_u / theta*_v drawn from their own per-id streams, so generation is row-parallel.
+}  // extern "C"
+
+namespace {
+struct SplitMix64 {
+    uint64_t s;
+    uint64_t operator()() {
+        uint64_t z = (s += 0x9e3779b97f4a7c15ULL);
+        z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+        z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+        return z ^ (z >> 31);
+    }
+    uint64_t bounded(uint64_t range) {
+        const uint64_t threshold = (0 - range) % range;
+        for (;;) {
+            const uint64_t v = (*this)();
+            if (v >= threshold) return v % range;
+        }
+    }
+    float unit() { return static_cast<float>((*this)() >> 40) * 0x1.0p-24f; }
+};
+constexpr int kPlanted = 10;
+void planted_row(uint64_t s, int64_t id, float* out) {
+    SplitMix64 g{mix_seed(s, static_cast<uint64_t>(id))};
+    for (int i = 0; i < kPlanted; ++i) out[i] = g.unit() * 0.6f;
+}
+template <class Fn>
+void parallel_rows(int64_t m, int threads, Fn&& fn) {
+    std::vector<std::thread> pool;
+    const int64_t per = (m + threads - 1) / threads;
+    for (int t = 0; t < threads; ++t) {
+        const int64_t u0 = t * per, u1 = std::min<int64_t>(m, u0 + per);
+        if (u0 >= u1) break;
+        pool.emplace_back(fn, u0, u1);
+    }
+    for (auto& th : pool) th.join();
+}
+}  // namespace
+
+extern "C" {
+
+alsk_status alsk_synth_csr(int64_t m, int64_t n, int64_t nnz, uint64_t seed, int threads,
+                           int64_t* row_ptr, int32_t* col_idx, float* values) {
+    if (m < 1 || n < 1 || nnz < 0) return ALSK_ERR_INPUT;
+    const uint64_t seed_x = mix_seed(seed, 1001), seed_t = mix_seed(seed, 1002);
+    for (int64_t u = 0; u <= m; ++u)
+        row_ptr[u] = static_cast<int64_t>((static_cast<unsigned __int128>(nnz) * static_cast<uint64_t>(u)) /
+                                          static_cast<uint64_t>(m));
+    for (int64_t u = 0; u < m; ++u)
+        if (row_ptr[u + 1] - row_ptr[u] > n) return ALSK_ERR_INPUT;  // more ratings than columns
+    if (threads <= 0) threads = static_cast<int>(std::max(1u, std::thread::hardware_concurrency()));
+    std::vector<float> tstar(static_cast<size_t>(n) * kPlanted);
+    parallel_rows(n, threads, [&](int64_t v0, int64_t v1) {
+        for (int64_t v = v0; v < v1; ++v) planted_row(seed_t, v, tstar.data() + v * kPlanted);
+    });
+    parallel_rows(m, threads, [&](int64_t u0, int64_t u1) {
+        std::vector<int64_t> chosen;
+        float xu[kPlanted];
+        for (int64_t u = u0; u < u1; ++u) {
+            const int64_t d = row_ptr[u + 1] - row_ptr[u];
+            SplitMix64 g{mix_seed(seed, static_cast<uint64_t>(u))};
+            chosen.clear();
+            for (int64_t j = n - d; j < n; ++j) {  // Floyd's sampling of d distinct columns
+                const int64_t t = static_cast<int64_t>(g.bounded(static_cast<uint64_t>(j + 1)));
+                bool dup = false;
+                for (int64_t c : chosen)
+                    if (c == t) { dup = true; break; }
+                chosen.push_back(dup ? j : t);
+            }
+            std::sort(chosen.begin(), chosen.end());
+            planted_row(seed_x, u, xu);
+            int64_t k = row_ptr[u];
+            for (int64_t c : chosen) {
+                const float* tv = tstar.data() + c * kPlanted;
+                float dot = 0.f;
+                for (int i = 0; i < kPlanted; ++i) dot += xu[i] * tv[i];
+                col_idx[k] = static_cast<int32_t>(c);
+                values[k] = dot + (g.unit() - 0.5f);
+                ++k;
+            }
+        }
+    });
+    return ALSK_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,111 @@
+// Internal launcher API between the .cu translation units of libalskit_cuda.so.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <vector>
+
+#include "common.cuh"
+
+namespace alsk {
+
+// Device view of a CsrMatrix (sparse.hpp:38-48); all pointers are device pointers.
+struct DevCsr {
+    int64_t rows = 0, cols = 0, col_offset = 0, nnz = 0;
+    const int64_t* row_ptr = nullptr;
+    const int32_t* col_idx = nullptr;
+    const float* values = nullptr;
+};
+
+// Breakdown bookkeeping written by the solve kernels: first failing row (atomicMin) plus
+// per-row column/pivot so the host can rebuild the reference's message
+// (solver.hpp:230-235).
+struct SolveStatus {
+    unsigned long long* min_row;  // 1 value, init ~0ull
+    int32_t* column;              // per row in launch (column+1, 0 = ok)
+    double* pivot;                // per row in launch
+};
+
+// Columns of rows [rb,re) must lie in [col_lo, col_hi); throws InputError with the
+// reference's message (solver.hpp:120-123) naming the first offending entry.
+void check_columns(const DevCsr& r, int64_t rb, int64_t re, int64_t col_lo, int64_t col_hi,
+                   cudaStream_t s);
+
+// Materialised assembly (A full mirrored f*f floats + B f floats per row), rows [rb,re).
+// acc_double: reference-order double accumulation (bit-exact with assemble_mo_rows<double>).
+void hermitian_materialize(const DevCsr& r, const float* theta, int f, double lambda,
+                           bool acc_double, int64_t rb, int64_t re, float* A, float* B,
+                           cudaStream_t s);
+
+// Double-output variant (BatchD, parallel.hpp:174-202): partial Hermitians kept in
+// double until the cross-worker reduction. packed=false: full mirrored A + B per row;
+// packed=true: lower-packed A then B, f(f+1)/2+f doubles per row, into A only.
+void hermitian_materialize_d(const DevCsr& r, const float* theta, int f, double lambda, bool acc_double,
+                             int64_t rb, int64_t re, double* A, double* B, bool packed, cudaStream_t s);
+
+// Reference-order double Cholesky of float systems (batch_solve_into, solver.hpp:204-262).
+void solve_exact(const float* A, const float* B, int64_t count, int f, bool zero_row_policy,
+                 float* X, const SolveStatus& st, cudaStream_t s);
+
+// FP32 fused assembly + in-register Cholesky for rows [rb,re) -> X rows (x_out[(u-rb)*f]).
+// Returns false if f is outside the fused kernel's range (caller falls back to the
+// materialised FP32 path).
+bool update_fused_fp32(const DevCsr& r, const float* theta, int f, float lambda, int64_t rb,
+                       int64_t re, float* x_out, const SolveStatus& st, cudaStream_t s);
+
+// FP32 register-blocked assembly only (materialised output) — the hermitian timed alone.
+bool hermitian_fused_fp32(const DevCsr& r, const float* theta, int f, float lambda, int64_t rb,
+                          int64_t re, float* A, float* B, cudaStream_t s);
+
+// Packed-lower double partial Hermitian (data-parallel split) and its solve.
+void partial_hermitian_packed(const DevCsr& r, const float* theta, int f, double lambda,
+                              int64_t rb, int64_t re, double* out, cudaStream_t s);
+void solve_packed(const double* packed, int64_t count, int f, float* X, const SolveStatus& st,
+                  cudaStream_t s);
+
+// Evaluation (solver.hpp:358-406). Deterministic two-level double reductions.
+double loss_device(const DevCsr& r, const int64_t* col_nnz, const float* x, const float* theta,
+                   int f, double lambda, cudaStream_t s);
+double rmse_device(const int64_t* rows, const int64_t* cols, const float* values, int64_t count,
+                   const float* x, int64_t x_rows, const float* theta, int64_t theta_rows, int f,
+                   cudaStream_t s);
+void column_counts(const DevCsr& r, int64_t* col_nnz, cudaStream_t s);
+
+// Sparse index plumbing (sparse.hpp:132-314), bit-exact.
+void csr_to_csc_device(const DevCsr& a, int64_t* col_ptr, int32_t* row_idx, float* values,
+                       cudaStream_t s);
+void csr_from_triplets_device(int64_t m, int64_t n, const int64_t* rows, const int64_t* cols,
+                              const float* vals, int64_t count, int64_t* row_ptr, int32_t* col_idx,
+                              float* values, cudaStream_t s);
+
+template <class T>
+void exclusive_scan_ptr_i64(const T* in, int64_t n, int64_t* out, cudaStream_t s);
+
+// Grid partition state on the device (sparse.hpp:71-84): cuts on the host, per-row split
+// offsets and per-block row pointers on the device.
+struct GridDevice {
+    int p = 1, q = 1;
+    std::vector<int64_t> row_cuts, col_cuts, block_nnz;
+    DevBuf offs;
+    std::vector<DevBuf> block_row_ptr;  // j*p+i
+};
+GridDevice grid_partition_device(const DevCsr& r, int p, int q, cudaStream_t s);
+void grid_fill_block(const DevCsr& r, const GridDevice& g, int i, int j, int32_t* bci, float* bv,
+                     cudaStream_t s);
+
+// Reduction plan (parallel.hpp:84-124): per slice, phase-1 and phase-2 transfers
+// (x = src, y = dst) sorted by (dst, src).
+struct ReduceSchedule {
+    int p = 1;
+    std::vector<std::vector<int2>> phase1, phase2;
+};
+ReduceSchedule build_reduce_schedule(int p, const int32_t* group_of, bool two_phase);
+std::vector<int64_t> slice_cuts(int64_t count, int p);
+template <class In>
+void reduce_slices(const std::vector<const In*>& parts_a, const std::vector<const In*>& parts_b, int64_t count,
+                   int f, const ReduceSchedule& sc, const std::vector<float*>& out_a,
+                   const std::vector<float*>& out_b, cudaStream_t s);
+void unpack_packed(const double* packed, int64_t count, int f, float* A, float* B, cudaStream_t s);
+
+}  // namespace alsk

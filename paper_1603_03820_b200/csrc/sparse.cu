@@ -1,0 +1,405 @@
+// Sparse index plumbing on the device, bit-exact with sparse.hpp:
+//  * stable LSD radix sort (8-bit digits, upsweep histogram / scan / ranked scatter),
+//  * exclusive scans over int64 counts (row_ptr / col_ptr construction),
+//  * csr_to_csc / csc_to_csr (sparse.hpp:185-231): a stable sort of the nonzeros by column
+//    with (row, value) payload reproduces the counting-sort transpose exactly, because the
+//    input is row-major and stability keeps rows ascending within each column,
+//  * csr_from_triplets (sparse.hpp:132-170): two stable passes (column, then row), range
+//    and duplicate checks naming the same coordinate the reference names,
+//  * grid_partition (sparse.hpp:250-314): per-row binary search of the column cuts.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "kernels.cuh"
+
+namespace alsk {
+namespace {
+
+constexpr int kSortThreads = 256;
+constexpr int kSortItems = 16;
+constexpr int kSortTile = kSortThreads * kSortItems;  // 4096 keys per tile
+constexpr int kWarps = kSortThreads / 32;
+
+// ---------------------------------------------------------------- scans (int64) -----
+constexpr int kScanThreads = 512;
+constexpr int kScanItems = 8;
+constexpr int kScanTile = kScanThreads * kScanItems;
+
+template <class T>
+__device__ __forceinline__ int64_t block_inclusive_scan(int64_t v, int64_t* warp_tot) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int o = 1; o < 32; o <<= 1) {
+        const int64_t n = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += n;
+    }
+    if (lane == 31) warp_tot[warp] = v;
+    __syncthreads();
+    if (warp == 0) {
+        int64_t w = lane < (blockDim.x >> 5) ? warp_tot[lane] : 0;
+        for (int o = 1; o < 32; o <<= 1) {
+            const int64_t n = __shfl_up_sync(0xffffffffu, w, o);
+            if (lane >= o) w += n;
+        }
+        if (lane < (blockDim.x >> 5)) warp_tot[lane] = w;
+    }
+    __syncthreads();
+    if (warp > 0) v += warp_tot[warp - 1];
+    return v;
+}
+
+template <class T>
+__global__ void scan_reduce_kernel(const T* __restrict__ in, int64_t n, int64_t* __restrict__ sums) {
+    __shared__ int64_t wt[32];
+    const int64_t base = blockIdx.x * static_cast<int64_t>(kScanTile);
+    int64_t acc = 0;
+    for (int i = 0; i < kScanItems; ++i) {
+        const int64_t idx = base + threadIdx.x * static_cast<int64_t>(kScanItems) + i;
+        if (idx < n) acc += static_cast<int64_t>(in[idx]);
+    }
+    const int64_t t = block_inclusive_scan<T>(acc, wt);
+    if (threadIdx.x == blockDim.x - 1) sums[blockIdx.x] = t;
+}
+
+// Single-block exclusive scan of `n` int64 in place (sequential tiles with carry).
+__global__ void scan_sums_kernel(int64_t* __restrict__ sums, int64_t n) {
+    __shared__ int64_t wt[32];
+    __shared__ int64_t carry;
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    for (int64_t base = 0; base < n; base += blockDim.x) {
+        const int64_t idx = base + threadIdx.x;
+        const int64_t v = idx < n ? sums[idx] : 0;
+        const int64_t inc = block_inclusive_scan<int64_t>(v, wt);
+        const int64_t c = carry;
+        if (idx < n) sums[idx] = c + inc - v;
+        __syncthreads();
+        if (threadIdx.x == blockDim.x - 1) carry = c + inc;
+        __syncthreads();
+    }
+}
+
+template <class T>
+__global__ void scan_apply_kernel(const T* __restrict__ in, int64_t n, const int64_t* __restrict__ sums,
+                                  int64_t* __restrict__ out, int64_t out_base) {
+    __shared__ int64_t wt[32];
+    const int64_t base = blockIdx.x * static_cast<int64_t>(kScanTile);
+    int64_t vals[kScanItems];
+    int64_t acc = 0;
+    for (int i = 0; i < kScanItems; ++i) {
+        const int64_t idx = base + threadIdx.x * static_cast<int64_t>(kScanItems) + i;
+        vals[i] = idx < n ? static_cast<int64_t>(in[idx]) : 0;
+        acc += vals[i];
+    }
+    const int64_t inc = block_inclusive_scan<T>(acc, wt);
+    int64_t run = sums[blockIdx.x] + inc - acc + out_base;
+    for (int i = 0; i < kScanItems; ++i) {
+        const int64_t idx = base + threadIdx.x * static_cast<int64_t>(kScanItems) + i;
+        if (idx < n) out[idx] = run;
+        run += vals[i];
+    }
+}
+
+// out[0..n] = exclusive scan of in[0..n) with out[n] = total (a CSR pointer array).
+template <class T>
+void exclusive_scan_ptr(const T* in, int64_t n, int64_t* out, cudaStream_t s) {
+    if (n == 0) {
+        ALSK_CUDA(cudaMemsetAsync(out, 0, sizeof(int64_t), s));
+        return;
+    }
+    const int64_t nb = (n + kScanTile - 1) / kScanTile;
+    DevBuf sums(sizeof(int64_t) * (nb + 1), s);
+    scan_reduce_kernel<T><<<static_cast<unsigned>(nb), kScanThreads, 0, s>>>(in, n, sums.as<int64_t>());
+    ALSK_LAUNCHED();
+    ALSK_CUDA(cudaMemsetAsync(sums.as<int64_t>() + nb, 0, sizeof(int64_t), s));
+    scan_sums_kernel<<<1, 1024, 0, s>>>(sums.as<int64_t>(), nb + 1);
+    ALSK_LAUNCHED();
+    scan_apply_kernel<T><<<static_cast<unsigned>(nb), kScanThreads, 0, s>>>(in, n, sums.as<int64_t>(), out, 0);
+    ALSK_LAUNCHED();
+    // total = exclusive prefix at position nb of the block sums
+    ALSK_CUDA(cudaMemcpyAsync(out + n, sums.as<int64_t>() + nb, sizeof(int64_t), cudaMemcpyDeviceToDevice, s));
+}
+
+// --------------------------------------------------------------- radix sort ---------
+// Digit histogram per tile, stored digit-major: hist[d * ntiles + tile].
+__global__ void radix_upsweep_kernel(const uint32_t* __restrict__ keys, int64_t n, int shift,
+                                     int64_t ntiles, int64_t* __restrict__ hist) {
+    __shared__ unsigned cnt[256];
+    for (int d = threadIdx.x; d < 256; d += blockDim.x) cnt[d] = 0;
+    __syncthreads();
+    const int64_t base = blockIdx.x * static_cast<int64_t>(kSortTile);
+    for (int i = threadIdx.x; i < kSortTile; i += blockDim.x) {
+        const int64_t idx = base + i;
+        if (idx < n) atomicAdd(&cnt[(keys[idx] >> shift) & 255u], 1u);
+    }
+    __syncthreads();
+    for (int d = threadIdx.x; d < 256; d += blockDim.x) hist[d * ntiles + blockIdx.x] = cnt[d];
+}
+
+// Stable ranked scatter. Warp w owns tile elements [w*512, (w+1)*512) processed item by
+// item (lanes ascending inside an item), so warp-local ranks follow element order;
+// warps are combined in order, tiles by the digit-major global scan.
+template <class P>
+__global__ void radix_scatter_kernel(const uint32_t* __restrict__ keys_in, const P* __restrict__ pay_in,
+                                     int64_t n, int shift, int64_t ntiles,
+                                     const int64_t* __restrict__ offsets, uint32_t* __restrict__ keys_out,
+                                     P* __restrict__ pay_out) {
+    __shared__ unsigned whist[kWarps][256];
+    __shared__ int64_t tile_base[256];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int d = threadIdx.x; d < 256; d += blockDim.x) {
+        for (int w = 0; w < kWarps; ++w) whist[w][d] = 0;
+        tile_base[d] = offsets[d * ntiles + blockIdx.x];
+    }
+    __syncthreads();
+    const int64_t base = blockIdx.x * static_cast<int64_t>(kSortTile) + warp * (32 * kSortItems);
+    unsigned digit[kSortItems];
+    unsigned local[kSortItems];
+    const unsigned lt_mask = (1u << lane) - 1u;
+#pragma unroll
+    for (int i = 0; i < kSortItems; ++i) {
+        const int64_t idx = base + i * 32 + lane;
+        const bool valid = idx < n;
+        const unsigned d = valid ? ((keys_in[idx] >> shift) & 255u) : 256u + lane;  // invalid: unique
+        const unsigned peers = __match_any_sync(0xffffffffu, d);
+        const unsigned rank = __popc(peers & lt_mask);
+        unsigned prior = 0;
+        if (valid) prior = whist[warp][d];
+        __syncwarp();
+        const int leader = __ffs(peers) - 1;
+        if (valid && lane == leader) whist[warp][d] = prior + __popc(peers);
+        __syncwarp();
+        digit[i] = d;
+        local[i] = prior + rank;
+    }
+    __syncthreads();
+    // exclusive scan across warps per digit
+    for (int d = threadIdx.x; d < 256; d += blockDim.x) {
+        unsigned run = 0;
+        for (int w = 0; w < kWarps; ++w) {
+            const unsigned c = whist[w][d];
+            whist[w][d] = run;
+            run += c;
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < kSortItems; ++i) {
+        const int64_t idx = base + i * 32 + lane;
+        if (idx < n) {
+            const unsigned d = digit[i];
+            const int64_t pos = tile_base[d] + whist[warp][d] + local[i];
+            keys_out[pos] = keys_in[idx];
+            pay_out[pos] = pay_in[idx];
+        }
+    }
+}
+
+// Stable sort of (key, payload) by key bits [0, bits). Result ends in (k0, p0); k1/p1 scratch.
+template <class P>
+void radix_sort_pairs(uint32_t* k0, P* p0, uint32_t* k1, P* p1, int64_t n, int bits, cudaStream_t s) {
+    if (n <= 1 || bits <= 0) return;
+    const int64_t ntiles = (n + kSortTile - 1) / kSortTile;
+    DevBuf hist(sizeof(int64_t) * (256 * ntiles + 1), s);
+    uint32_t* kin = k0; P* pin = p0; uint32_t* kout = k1; P* pout = p1;
+    for (int shift = 0; shift < bits; shift += 8) {
+        radix_upsweep_kernel<<<static_cast<unsigned>(ntiles), kSortThreads, 0, s>>>(kin, n, shift, ntiles,
+                                                                                   hist.as<int64_t>());
+        ALSK_LAUNCHED();
+        exclusive_scan_ptr<int64_t>(hist.as<int64_t>(), 256 * ntiles, hist.as<int64_t>(), s);
+        radix_scatter_kernel<P><<<static_cast<unsigned>(ntiles), kSortThreads, 0, s>>>(
+            kin, pin, n, shift, ntiles, hist.as<int64_t>(), kout, pout);
+        ALSK_LAUNCHED();
+        std::swap(kin, kout);
+        std::swap(pin, pout);
+    }
+    if (kin != k0) {
+        ALSK_CUDA(cudaMemcpyAsync(k0, kin, sizeof(uint32_t) * n, cudaMemcpyDeviceToDevice, s));
+        ALSK_CUDA(cudaMemcpyAsync(p0, pin, sizeof(P) * n, cudaMemcpyDeviceToDevice, s));
+    }
+}
+
+int bits_for(int64_t count) {  // bits to represent values in [0, count)
+    int b = 0;
+    while (b < 63 && (int64_t(1) << b) < count) ++b;
+    return b;
+}
+
+// --------------------------------------------------------------- helpers -------------
+// Per nonzero: key = column, payload = (row << 32) | value bits.
+__global__ void csr_pack_kernel(const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col_idx,
+                                const float* __restrict__ values, int64_t rows,
+                                uint32_t* __restrict__ keys, uint64_t* __restrict__ pay) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp0 = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
+    const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+    for (int64_t u = warp0; u < rows; u += nw) {
+        for (int64_t k = row_ptr[u] + lane; k < row_ptr[u + 1]; k += 32) {
+            keys[k] = static_cast<uint32_t>(col_idx[k]);
+            pay[k] = (static_cast<uint64_t>(static_cast<uint32_t>(u)) << 32) | __float_as_uint(values[k]);
+        }
+    }
+}
+
+__global__ void count_keys_kernel(const uint32_t* __restrict__ keys, int64_t n, unsigned long long* __restrict__ cnt) {
+    for (int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; k < n;
+         k += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        atomicAdd(cnt + keys[k], 1ull);
+}
+
+__global__ void unpack_kernel(const uint64_t* __restrict__ pay, int64_t n, int32_t* __restrict__ idx_out,
+                              float* __restrict__ val_out) {
+    for (int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; k < n;
+         k += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const uint64_t p = pay[k];
+        idx_out[k] = static_cast<int32_t>(p >> 32);
+        val_out[k] = __uint_as_float(static_cast<uint32_t>(p));
+    }
+}
+
+int grid_for(int64_t n, int threads = 256) {
+    const int64_t b = (n + threads - 1) / threads;
+    return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(b, 148LL * 16)));
+}
+
+__global__ void triplet_range_kernel(const int64_t* __restrict__ rows, const int64_t* __restrict__ cols,
+                                     int64_t count, int64_t m, int64_t n, unsigned long long* __restrict__ bad) {
+    for (int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; k < count;
+         k += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t r = rows[k], c = cols[k];
+        if (r < 0 || r >= m || c < 0 || c >= n) atomicMin(bad, static_cast<unsigned long long>(k));
+    }
+}
+
+__global__ void iota_keys_kernel(const int64_t* __restrict__ src, int64_t n, uint32_t* __restrict__ keys,
+                                 uint64_t* __restrict__ idx) {
+    for (int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; k < n;
+         k += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        keys[k] = static_cast<uint32_t>(src[k]);
+        idx[k] = static_cast<uint64_t>(k);
+    }
+}
+
+__global__ void gather_keys_kernel(const int64_t* __restrict__ src, const uint64_t* __restrict__ idx,
+                                   int64_t n, uint32_t* __restrict__ keys) {
+    for (int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; k < n;
+         k += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        keys[k] = static_cast<uint32_t>(src[idx[k]]);
+}
+
+// After the (row, col) sort: emit col_idx/values, count rows, flag the first duplicate.
+__global__ void emit_sorted_kernel(const int64_t* __restrict__ rows, const int64_t* __restrict__ cols,
+                                   const float* __restrict__ vals, const uint64_t* __restrict__ idx,
+                                   int64_t n, int32_t* __restrict__ col_out, float* __restrict__ val_out,
+                                   unsigned long long* __restrict__ row_cnt,
+                                   unsigned long long* __restrict__ first_dup) {
+    for (int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; k < n;
+         k += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const uint64_t s = idx[k];
+        const int64_t r = rows[s], c = cols[s];
+        col_out[k] = static_cast<int32_t>(c);
+        val_out[k] = vals[s];
+        atomicAdd(row_cnt + r, 1ull);
+        if (k > 0) {
+            const uint64_t q = idx[k - 1];
+            if (rows[q] == r && cols[q] == c) atomicMin(first_dup, static_cast<unsigned long long>(k));
+        }
+    }
+}
+
+}  // namespace
+
+template <class T>
+void exclusive_scan_ptr_i64(const T* in, int64_t n, int64_t* out, cudaStream_t s) {
+    exclusive_scan_ptr<T>(in, n, out, s);
+}
+template void exclusive_scan_ptr_i64<int64_t>(const int64_t*, int64_t, int64_t*, cudaStream_t);
+template void exclusive_scan_ptr_i64<unsigned long long>(const unsigned long long*, int64_t, int64_t*, cudaStream_t);
+
+void csr_from_triplets_device(int64_t m, int64_t n, const int64_t* rows, const int64_t* cols,
+                              const float* vals, int64_t count, int64_t* row_ptr, int32_t* col_idx,
+                              float* values, cudaStream_t s) {
+    if (m < 0 || n < 0) fail_input("matrix dimensions must be non-negative");
+    if (n > 2147483647LL) fail_input("column count " + std::to_string(n) + " exceeds the 32-bit index range");
+    if (m > 0xffffffffLL) fail_input("row count exceeds the device sort range");
+    DevBuf bad(sizeof(unsigned long long), s);
+    ALSK_CUDA(cudaMemsetAsync(bad.as<void>(), 0xff, sizeof(unsigned long long), s));
+    if (count > 0) {
+        triplet_range_kernel<<<grid_for(count), 256, 0, s>>>(rows, cols, count, m, n, bad.as<unsigned long long>());
+        ALSK_LAUNCHED();
+    }
+    unsigned long long hbad = 0;
+    d2h(&hbad, bad.as<unsigned long long>(), 1, s);
+    ALSK_CUDA(cudaStreamSynchronize(s));
+    if (hbad != ~0ull) {
+        int64_t r = 0, c = 0;
+        d2h(&r, rows + hbad, 1, s);
+        d2h(&c, cols + hbad, 1, s);
+        ALSK_CUDA(cudaStreamSynchronize(s));
+        fail_input("triplet (" + std::to_string(r) + ", " + std::to_string(c) + ") outside " +
+                   std::to_string(m) + "x" + std::to_string(n));
+    }
+    DevBuf cnt(sizeof(unsigned long long) * std::max<int64_t>(m, 1), s);
+    ALSK_CUDA(cudaMemsetAsync(cnt.as<void>(), 0, sizeof(unsigned long long) * std::max<int64_t>(m, 1), s));
+    if (count == 0) {
+        exclusive_scan_ptr<unsigned long long>(cnt.as<unsigned long long>(), m, row_ptr, s);
+        return;
+    }
+    DevBuf k0(sizeof(uint32_t) * count, s), k1(sizeof(uint32_t) * count, s);
+    DevBuf p0(sizeof(uint64_t) * count, s), p1(sizeof(uint64_t) * count, s);
+    // LSD: stable by column, then stable by row => (row, col) order, ties in input order
+    iota_keys_kernel<<<grid_for(count), 256, 0, s>>>(cols, count, k0.as<uint32_t>(), p0.as<uint64_t>());
+    ALSK_LAUNCHED();
+    radix_sort_pairs<uint64_t>(k0.as<uint32_t>(), p0.as<uint64_t>(), k1.as<uint32_t>(), p1.as<uint64_t>(),
+                               count, bits_for(n), s);
+    gather_keys_kernel<<<grid_for(count), 256, 0, s>>>(rows, p0.as<uint64_t>(), count, k0.as<uint32_t>());
+    ALSK_LAUNCHED();
+    radix_sort_pairs<uint64_t>(k0.as<uint32_t>(), p0.as<uint64_t>(), k1.as<uint32_t>(), p1.as<uint64_t>(),
+                               count, bits_for(m), s);
+    ALSK_CUDA(cudaMemsetAsync(bad.as<void>(), 0xff, sizeof(unsigned long long), s));
+    emit_sorted_kernel<<<grid_for(count), 256, 0, s>>>(rows, cols, vals, p0.as<uint64_t>(), count, col_idx,
+                                                       values, cnt.as<unsigned long long>(),
+                                                       bad.as<unsigned long long>());
+    ALSK_LAUNCHED();
+    d2h(&hbad, bad.as<unsigned long long>(), 1, s);
+    ALSK_CUDA(cudaStreamSynchronize(s));
+    if (hbad != ~0ull) {
+        uint64_t src = 0;
+        d2h(&src, p0.as<uint64_t>() + hbad, 1, s);
+        ALSK_CUDA(cudaStreamSynchronize(s));
+        int64_t r = 0, c = 0;
+        d2h(&r, rows + src, 1, s);
+        d2h(&c, cols + src, 1, s);
+        ALSK_CUDA(cudaStreamSynchronize(s));
+        fail_input("duplicate coordinate (" + std::to_string(r) + ", " + std::to_string(c) + ")");
+    }
+    exclusive_scan_ptr<unsigned long long>(cnt.as<unsigned long long>(), m, row_ptr, s);
+}
+
+void csr_to_csc_device(const DevCsr& a, int64_t* col_ptr, int32_t* row_idx, float* values,
+                       cudaStream_t s) {
+    const int64_t n = a.nnz;
+    if (a.rows > 0xffffffffLL) fail_input("row count exceeds the device transpose range");
+    DevBuf cnt(sizeof(unsigned long long) * std::max<int64_t>(a.cols, 1), s);
+    ALSK_CUDA(cudaMemsetAsync(cnt.as<void>(), 0, sizeof(unsigned long long) * std::max<int64_t>(a.cols, 1), s));
+    if (n == 0) {
+        exclusive_scan_ptr<unsigned long long>(cnt.as<unsigned long long>(), a.cols, col_ptr, s);
+        return;
+    }
+    DevBuf k0(sizeof(uint32_t) * n, s), k1(sizeof(uint32_t) * n, s);
+    DevBuf p0(sizeof(uint64_t) * n, s), p1(sizeof(uint64_t) * n, s);
+    csr_pack_kernel<<<grid_for(a.rows * 32), 256, 0, s>>>(a.row_ptr, a.col_idx, a.values, a.rows,
+                                                          k0.as<uint32_t>(), p0.as<uint64_t>());
+    ALSK_LAUNCHED();
+    count_keys_kernel<<<grid_for(n), 256, 0, s>>>(k0.as<uint32_t>(), n, cnt.as<unsigned long long>());
+    ALSK_LAUNCHED();
+    exclusive_scan_ptr<unsigned long long>(cnt.as<unsigned long long>(), a.cols, col_ptr, s);
+    radix_sort_pairs<uint64_t>(k0.as<uint32_t>(), p0.as<uint64_t>(), k1.as<uint32_t>(),
+                               p1.as<uint64_t>(), n, bits_for(a.cols), s);
+    unpack_kernel<<<grid_for(n), 256, 0, s>>>(p0.as<uint64_t>(), n, row_idx, values);
+    ALSK_LAUNCHED();
+}
+
+}  // namespace alsk

@@ -1,0 +1,125 @@
+"""Device-resident ALS session: R (CSR) and R^T (CSR of the transpose, i.e. the CSC arrays)
+uploaded once, X and Theta kept in HBM across half-sweeps.
+
+This is the caller of the hot path that train_run/als_train need:
+the reference rebuilds nothing between halves either (driver.hpp:115, 255-262), but keeps
+factors in host memory; here they never leave the device unless asked for. PyTorch is used
+only for device allocation and the current stream; every kernel is libalskit_cuda's.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from typing import Optional
+
+import numpy as np
+import torch
+
+from . import _native as N
+from .alskit import (TRIPLET_DTYPE, CscMatrix, CsrMatrix, FactorMatrix, SolverConfig, _check)
+
+LIB = N.LIB
+PREC_FP64_EXACT = 0
+PREC_FP32 = 1
+
+
+def _dev(a: np.ndarray, device) -> torch.Tensor:
+    return torch.from_numpy(np.ascontiguousarray(a)).to(device, non_blocking=False)
+
+
+class DeviceCsr:
+    """CSR arrays in HBM plus the C-ABI view of them."""
+
+    def __init__(self, rows: int, cols: int, row_ptr, col_idx, values, device, col_offset: int = 0):
+        self.rows, self.cols, self.col_offset = rows, cols, col_offset
+        t = lambda a, dt: a if isinstance(a, torch.Tensor) else _dev(np.asarray(a, dt), device)  # noqa: E731
+        self.row_ptr = t(row_ptr, np.int64)
+        self.col_idx = t(col_idx, np.int32)
+        self.values = t(values, np.float32)
+        self.nnz = int(self.values.numel())
+        self.c = N.CsrT(rows, cols, col_offset, self.nnz, self.row_ptr.data_ptr(),
+                        self.col_idx.data_ptr(), self.values.data_ptr())
+
+    @staticmethod
+    def from_host(r: CsrMatrix, device) -> "DeviceCsr":
+        return DeviceCsr(r.rows, r.cols, r.row_ptr, r.col_idx, r.values, device, r.col_offset)
+
+    def transpose(self) -> "DeviceCsr":
+        """Stable device transpose (csr_to_csc, sparse.hpp:185-207) viewed as the CSR of R^T."""
+        dev = self.values.device
+        col_ptr = torch.empty(self.cols + 1, dtype=torch.int64, device=dev)
+        row_idx = torch.empty(max(self.nnz, 1), dtype=torch.int32, device=dev)
+        vals = torch.empty(max(self.nnz, 1), dtype=torch.float32, device=dev)
+        _check(LIB.alsk_dev_csr_to_csc(C.byref(self.c), col_ptr.data_ptr(), row_idx.data_ptr(),
+                                       vals.data_ptr(), stream_handle()))
+        return DeviceCsr(self.cols, self.rows, col_ptr, row_idx[: self.nnz], vals[: self.nnz], dev)
+
+
+def stream_handle() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+def dev_update(r: DeviceCsr, theta: torch.Tensor, theta_rows: int, f: int, lam: float, precision: int,
+               out: torch.Tensor, row_begin: int = 0, row_end: Optional[int] = None,
+               batch_rows: int = 4096) -> None:
+    """One half-sweep (update_x, solver.hpp:330-345) of rows [row_begin,row_end) into
+    out[(row-row_begin)*f ...]."""
+    re = r.rows if row_end is None else row_end
+    _check(LIB.alsk_dev_update(C.byref(r.c), theta.data_ptr(), theta_rows, f, lam, precision,
+                               batch_rows, row_begin, re, out.data_ptr(), stream_handle()))
+
+
+class AlsSession:
+    def __init__(self, r: CsrMatrix, r_csc: Optional[CscMatrix], test: Optional[np.ndarray],
+                 cfg: SolverConfig, x0: FactorMatrix, theta0: FactorMatrix, device: str = "cuda"):
+        if not torch.cuda.is_available():
+            raise RuntimeError("AlsSession needs a CUDA device (libalskit_cuda has no CPU path)")
+        self.device = torch.device(device)
+        self.cfg = cfg
+        self.f = x0.f
+        self.m, self.n = r.rows, r.cols
+        self.precision = PREC_FP64_EXACT if cfg.accumulate_double else PREC_FP32
+        self.R = DeviceCsr.from_host(r, self.device)
+        if r_csc is not None:
+            self.RT = DeviceCsr(r_csc.cols, r_csc.rows, r_csc.col_ptr, r_csc.row_idx, r_csc.values,
+                                self.device)
+        else:
+            self.RT = self.R.transpose()
+        self.col_nnz = (self.RT.row_ptr[1:] - self.RT.row_ptr[:-1]).contiguous()
+        self.X = _dev(x0.entries, self.device)
+        self.T = _dev(theta0.entries, self.device)
+        self.test = None
+        if test is not None and len(test):
+            t = np.ascontiguousarray(test, TRIPLET_DTYPE)
+            self.test_rows = _dev(t["row"].copy(), self.device)
+            self.test_cols = _dev(t["col"].copy(), self.device)
+            self.test_vals = _dev(t["value"].copy(), self.device)
+            self.test = len(t)
+
+    def half_x(self) -> None:
+        dev_update(self.R, self.T, self.n, self.f, self.cfg.lambda_, self.precision, self.X,
+                   batch_rows=self.cfg.batch_rows)
+
+    def half_theta(self) -> None:
+        dev_update(self.RT, self.X, self.m, self.f, self.cfg.lambda_, self.precision, self.T,
+                   batch_rows=self.cfg.batch_rows)
+
+    def loss(self) -> float:
+        out = C.c_double()
+        _check(LIB.alsk_dev_loss(C.byref(self.R.c), self.col_nnz.data_ptr(), self.X.data_ptr(),
+                                 self.T.data_ptr(), self.n, self.f, self.cfg.lambda_, C.byref(out),
+                                 stream_handle()))
+        return out.value
+
+    def rmse(self) -> float:
+        if not self.test:
+            return float("nan")
+        out = C.c_double()
+        _check(LIB.alsk_dev_rmse(self.test_rows.data_ptr(), self.test_cols.data_ptr(),
+                                 self.test_vals.data_ptr(), self.test, self.X.data_ptr(), self.m,
+                                 self.T.data_ptr(), self.n, self.f, C.byref(out), stream_handle()))
+        return out.value
+
+    def factors(self):
+        x = FactorMatrix(self.m, self.f, self.X.cpu().numpy().copy())
+        t = FactorMatrix(self.n, self.f, self.T.cpu().numpy().copy())
+        return x, t
