@@ -99,6 +99,9 @@ void alsk_profile_begin(void);
 void alsk_profile_end(double* total_ms, uint64_t* launches);
 /* Measured FP32 FFMA throughput of the current device in TFLOP/s (roofline denominator). */
 double alsk_fp32_peak_probe(void);
+/* TFLOP/s of the Hermitian register-blocked inner loop alone (operands resident in shared
+ * memory, no gather, no barriers) at `ctas_per_sm` 96-thread CTAs per SM. */
+double alsk_herm_loop_probe(int ctas_per_sm, int variant);
 
 /* ---- host-buffer drop-in entry points (synchronous) ------------------------------- */
 

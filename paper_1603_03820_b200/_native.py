@@ -49,6 +49,7 @@ _SIGS = {
     "alsk_profile_begin": (None, []),
     "alsk_profile_end": (None, [f64p, C.POINTER(u64)]),
     "alsk_fp32_peak_probe": (C.c_double, []),
+    "alsk_herm_loop_probe": (C.c_double, [C.c_int, C.c_int]),
     "alsk_get_hermitian_mo_into": (C.c_int, [CsrP, vp, i64, C.c_int, CfgP, i64, i64, vp, vp]),
     "alsk_get_hermitian_base": (C.c_int, [CsrP, vp, i64, C.c_int, C.c_double, C.c_int, vp, vp]),
     "alsk_local_hermitian": (C.c_int, [CsrP, vp, i64, C.c_int, CfgP, vp, vp]),

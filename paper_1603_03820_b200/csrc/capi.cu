@@ -142,7 +142,7 @@ void update_rows_device(const DevCsr& r, const float* theta, int64_t theta_rows,
         ALSK_CUDA(cudaEventCreate(&e1));
         ALSK_CUDA(cudaEventRecord(e0, s));
     }
-    if (!exact && update_fused_fp32(r, theta, f, static_cast<float>(lambda), rb, re, x_out, sb.st, s)) {
+    if (!exact && update_fused_fp32(r, theta, theta_rows, f, static_cast<float>(lambda), rb, re, x_out, sb.st, s)) {
         if (g_prof.on) {
             ALSK_CUDA(cudaEventRecord(e1, s));
             ALSK_CUDA(cudaEventSynchronize(e1));
@@ -591,7 +591,7 @@ alsk_status alsk_dev_hermitian(const alsk_csr* r, const float* theta, int64_t th
         require_device();
         const DevCsr v = dev_view(r);
         if (precision == ALSK_PREC_FP32 &&
-            hermitian_fused_fp32(v, theta, f, static_cast<float>(lambda), row_begin, row_end, a_out,
+            hermitian_fused_fp32(v, theta, theta_rows, f, static_cast<float>(lambda), row_begin, row_end, a_out,
                                  b_out, as_stream(stream)))
             return;
         hermitian_materialize(v, theta, f, lambda, precision == ALSK_PREC_FP64_EXACT, row_begin,

@@ -36,6 +36,22 @@ inline void count_launch(uint64_t n = 1) { g_launches.fetch_add(n, std::memory_o
 
 void set_breakdown_index(int64_t k);
 
+// Keep freed stream-ordered memory in the device pool instead of returning it to the
+// driver at every synchronisation (the default threshold of 0 made per-call scratch
+// allocations re-map physical memory and stall for hundreds of milliseconds).
+inline void retain_pool_memory() {
+    static bool done = false;
+    if (done) return;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t thr = ~0ull;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    done = true;
+}
+
 // Owning device allocation (cudaMallocAsync on the given stream when available).
 class DevBuf {
 public:
@@ -49,6 +65,7 @@ public:
         reset();
         s_ = s;
         n_ = bytes;
+        retain_pool_memory();
         if (bytes) ALSK_CUDA(cudaMallocAsync(&p_, bytes, s));
     }
     void reset() {

@@ -5,23 +5,26 @@
 // assemble_mo_rows (solver.hpp:99-157) followed by batch_solve_into (solver.hpp:204-262).
 //
 // Design (B200):
-//  * Augmented outer product. Each gathered factor row theta_v is staged in shared memory
-//    as theta'_v = [theta_v, r_uv, 0...] (length FP = 8*NB >= f+1). The lower triangle of
-//    sum theta' theta'^T holds A_u in rows/cols < f and B_u in row f, so the bias is the
-//    same FMA stream as the Hermitian (cuMF's get_bias folded into get_hermitian).
+//  * Augmented outer product. Each gathered factor row theta_v (stride ldt = f rounded up
+//    to a multiple of 4, zero padded) is staged in shared memory as
+//    theta'_v = [theta_v, 0.., r_uv at column `aug` = ldt, 0..] of width FP = 8*NB. The
+//    lower triangle of sum theta' theta'^T holds A_u in rows/cols < f and B_u in row aug,
+//    so the bias is the same FMA stream as the Hermitian.
 //  * Register blocking. Thread t owns one 8x8 tile (bi,bj), bj<=bi, of the lower
 //    triangle: 64 FP32 accumulators, 4 LDS.128 per 64 FFMA. f=100 -> NB=13, 91 tiles,
-//    96 threads. The 8-float block halves are XOR-swizzled by bit 2 of the block index so
-//    eight consecutive tiles of a quarter-warp hit eight distinct 16-byte bank groups.
-//  * Gather. Factor rows are copied global->shared with cp.async (LDGSTS, 16 B per lane,
-//    L2-only .cg) into a double-buffered chunk of 32 nonzeros, overlapping the next
-//    chunk's gather with the current chunk's FMAs.
-//  * Cholesky in registers. The factorisation is a sequence of rank-1 downdates, i.e. the
-//    same outer product with the current column of L: per column c the owners publish
-//    column c to shared memory, one barrier, every thread downdates its tile. The
-//    augmented row turns into y = L^{-1} B on the way (forward substitution for free).
+//    96 threads.
+//  * Gather by TMA bulk copies. Lane k of warp 0 issues one cp.async.bulk (global ->
+//    shared, ldt*4 bytes, completion counted on the stage's mbarrier) for the k-th
+//    nonzero of a 32-nonzero chunk; a 3-stage ring keeps two chunks in flight while the
+//    FMAs consume the third. Stages are handed back through per-stage "empty" mbarriers
+//    (one arrive per warp), so warps never wait on each other inside the stream.
+//  * Blocked Cholesky in registers. Per 8-column block: the diagonal-tile owner factors
+//    its 8x8 block and publishes it; the panel owners solve their tiles against it
+//    (forward substitution, 8 independent rows each) and publish the panel transposed;
+//    every trailing tile takes the rank-8 downdate, which is the Hermitian inner loop
+//    again. Two barriers per block column. The augmented row becomes y = L^{-1} B.
 //  * Back substitution L^T x = y by warp 0 from a packed copy of L in shared memory
-//    (aliasing the gather buffers), column-oriented with warp shuffles.
+//    (aliasing the stage ring), column-oriented with warp shuffles.
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -31,7 +34,8 @@
 namespace alsk {
 namespace {
 
-constexpr int KC = 32;  // nonzeros per staged chunk
+constexpr int KC = 32;     // nonzeros per staged chunk (one bulk copy per lane of warp 0)
+constexpr int STAGES = 3;  // ring depth
 
 template <int NB>
 struct FusedShape {
@@ -39,157 +43,135 @@ struct FusedShape {
     static constexpr int NTILES = NB * (NB + 1) / 2;      // lower-triangular 8x8 tiles
     static constexpr int NT = ((NTILES + 31) / 32) * 32;  // threads per CTA
     static constexpr int LDT = FP;                        // row stride of a staged chunk
-    static constexpr int TILE_FLOATS = 2 * KC * LDT;      // double-buffered gather area
+    static constexpr int RING_FLOATS = STAGES * KC * LDT;
     static constexpr int LPK_FLOATS = FP * (FP + 1) / 2 + FP;  // packed L + y (upper bound)
-    static constexpr int UNION_FLOATS = TILE_FLOATS > LPK_FLOATS ? TILE_FLOATS : LPK_FLOATS;
-    // + column exchange buffer (2*FP) + dinv (FP)
-    static constexpr size_t SMEM = (UNION_FLOATS + 3 * FP) * sizeof(float);
+    static constexpr int UNION_FLOATS = RING_FLOATS > LPK_FLOATS ? RING_FLOATS : LPK_FLOATS;
+    // + panel (8 x FP) + diag block (64) + dinv (FP) + flags (8) + mbarriers (STAGES x 2 floats)
+    static constexpr int EXTRA_FLOATS = 8 * FP + 64 + FP + 8 + 4 * STAGES + 2;
+    static constexpr size_t SMEM = (UNION_FLOATS + EXTRA_FLOATS) * sizeof(float) + 16;
 };
 
-__device__ __forceinline__ int swz_block_half(int blk, int h) { return 2 * blk + (h ^ ((blk >> 2) & 1)); }
-// physical float offset of logical column c within a staged row
-__device__ __forceinline__ int phys_col(int c) {
-    const int blk = c >> 3, h = (c >> 2) & 1, q = c & 3;
-    return 4 * swz_block_half(blk, h) + q;
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    uint32_t done = 0;
+    do {
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+            : "=r"(done)
+            : "r"(smem_u32(bar)), "r"(parity)
+            : "memory");
+    } while (!done);
 }
 
-__device__ __forceinline__ void cp_async16(float* smem, const float* gmem) {
-    const unsigned saddr = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(saddr), "l"(gmem));
-}
-__device__ __forceinline__ void cp_async4(float* smem, const float* gmem) {
-    const unsigned saddr = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(saddr), "l"(gmem));
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::); }
-__device__ __forceinline__ void cp_async_wait_1() { asm volatile("cp.async.wait_group 1;\n" ::); }
-
-__device__ __forceinline__ void tile_coords(int t, int& bi, int& bj) {
-    int b = 0;
-    while ((b + 1) * (b + 2) / 2 <= t) ++b;
-    bi = b;
-    bj = t - b * (b + 1) / 2;
-}
-
-// Stage nonzeros [k, k+cnt) of the current row into buffer `dst` (KC x LDT floats).
-template <int NB>
-__device__ __forceinline__ void stage_chunk(float* dst, const int32_t* __restrict__ col_idx,
-                                            const float* __restrict__ values,
-                                            const float* __restrict__ theta, int64_t col_lo,
-                                            int f, bool vec16, int64_t k, int cnt) {
-    using S = FusedShape<NB>;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    constexpr int NW = S::NT / 32;
-    if (vec16) {
-        const int q4 = f >> 2;  // 16-byte pieces per factor row
-        for (int kk = warp; kk < cnt; kk += NW) {
-            const int64_t v = static_cast<int64_t>(col_idx[k + kk]) - col_lo;
-            const float* src = theta + v * f;
-            float* row = dst + kk * S::LDT;
-            for (int c4 = lane; c4 < q4; c4 += 32) {
-                const int c = c4 * 4;
-                cp_async16(row + phys_col(c), src + c);
-            }
-            if (lane == 31) row[phys_col(f)] = values[k + kk];
-        }
-    } else {
-        for (int kk = warp; kk < cnt; kk += NW) {
-            const int64_t v = static_cast<int64_t>(col_idx[k + kk]) - col_lo;
-            const float* src = theta + v * f;
-            float* row = dst + kk * S::LDT;
-            for (int c = lane; c < f; c += 32) cp_async4(row + phys_col(c), src + c);
-            if (lane == 31) row[phys_col(f)] = values[k + kk];
-        }
+// Column-major enumeration of the lower-triangular tiles: column bj holds tiles
+// (bj..NB-1, bj). The trailing tiles of block column bc (bj > bc) are then a suffix of the
+// enumeration and the panel tiles a contiguous run, so the Cholesky phases occupy as few
+// warps as possible.
+__device__ __forceinline__ void tile_coords_colmajor(int t, int nb, int& bi, int& bj) {
+    int c = 0;
+    while (t >= nb - c) {
+        t -= nb - c;
+        ++c;
     }
+    bj = c;
+    bi = c + t;
 }
 
-// Zero the padding columns (f+1 .. FP-1) of both staging buffers; column f is rewritten
-// with r_uv per staged nonzero, columns < f by the gather.
-template <int NB>
-__device__ __forceinline__ void zero_padding(float* tile, int f) {
-    using S = FusedShape<NB>;
-    const int pad = S::FP - (f + 1);
-    if (pad <= 0) return;
-    for (int e = threadIdx.x; e < 2 * KC * pad; e += S::NT) {
-        const int row = e / pad, c = f + 1 + (e - row * pad);
-        tile[row * S::LDT + phys_col(c)] = 0.f;
-    }
-}
-
-// Accumulate the augmented outer products of the current row into acc (8x8 tile).
-template <int NB>
-__device__ __forceinline__ void accumulate_row(float (&acc)[8][8], float* tile,
-                                               const int32_t* __restrict__ col_idx,
-                                               const float* __restrict__ values,
-                                               const float* __restrict__ theta, int64_t col_lo,
-                                               int f, bool vec16, int64_t k0, int64_t k1,
-                                               bool active, int offA0, int offA1, int offB0,
-                                               int offB1) {
-    using S = FusedShape<NB>;
-    const int64_t n = k1 - k0;
-    if (n <= 0) return;
-    const int nchunks = static_cast<int>((n + KC - 1) / KC);
-    stage_chunk<NB>(tile, col_idx, values, theta, col_lo, f, vec16, k0,
-                    static_cast<int>((n < KC ? n : (int64_t)KC)));
-    cp_async_commit();
-    for (int ch = 0; ch < nchunks; ++ch) {
-        float* cur = tile + (ch & 1) * KC * S::LDT;
-        const int cnt = static_cast<int>(((n - (int64_t)ch * KC) < KC ? (n - (int64_t)ch * KC) : (int64_t)KC));
-        if (ch + 1 < nchunks) {
-            const int64_t kn = k0 + static_cast<int64_t>(ch + 1) * KC;
-            stage_chunk<NB>(tile + ((ch + 1) & 1) * KC * S::LDT, col_idx, values, theta, col_lo, f,
-                            vec16, kn, static_cast<int>(((k1 - kn) < KC ? (k1 - kn) : (int64_t)KC)));
-            cp_async_commit();
-            cp_async_wait_1();
-        } else {
-            cp_async_wait_all();
-        }
-        __syncthreads();
-        if (active) {
+// acc[ii][jj] += sign * sum_k  rowsA[k][ia+ii] * rowsB[k][jb+jj]  over k in [0,cnt) of a
+// k-major buffer with row stride LDT (the Hermitian inner loop; also the rank-8 downdate).
+template <int LDT, bool NEG>
+__device__ __forceinline__ void outer_accumulate(float (&acc)[8][8], const float* buf, int cnt, int ia, int jb) {
 #pragma unroll 2
-            for (int kk = 0; kk < cnt; ++kk) {
-                const float* trow = cur + kk * S::LDT;
-                const float4 a0 = *reinterpret_cast<const float4*>(trow + offA0);
-                const float4 a1 = *reinterpret_cast<const float4*>(trow + offA1);
-                const float4 b0 = *reinterpret_cast<const float4*>(trow + offB0);
-                const float4 b1 = *reinterpret_cast<const float4*>(trow + offB1);
-                const float a[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
-                const float b[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+    for (int kk = 0; kk < cnt; ++kk) {
+        const float* trow = buf + kk * LDT;
+        const float4 a0 = *reinterpret_cast<const float4*>(trow + ia);
+        const float4 a1 = *reinterpret_cast<const float4*>(trow + ia + 4);
+        const float4 b0 = *reinterpret_cast<const float4*>(trow + jb);
+        const float4 b1 = *reinterpret_cast<const float4*>(trow + jb + 4);
+        const float a[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+        const float b[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
 #pragma unroll
-                for (int i = 0; i < 8; ++i)
+        for (int i = 0; i < 8; ++i)
 #pragma unroll
-                    for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
-            }
-        }
-        __syncthreads();  // buffer `cur` is restaged two chunks later
+            for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(NEG ? -a[i] : a[i], b[j], acc[i][j]);
     }
+}
+
+// Issue the bulk copies of chunk `ch` (nonzeros [k0+ch*KC, ...)) into its ring stage.
+// Called by all lanes of warp 0.
+template <int NB>
+__device__ __forceinline__ void issue_chunk(float* ring, uint64_t* bars, const int32_t* __restrict__ col_idx,
+                                            const float* __restrict__ values, const float* __restrict__ theta,
+                                            int64_t col_lo, int ldt, int aug, int64_t k0, int64_t n, int ch) {
+    using S = FusedShape<NB>;
+    const int lane = threadIdx.x & 31;
+    const int64_t kb = k0 + static_cast<int64_t>(ch) * KC;
+    const int64_t left = n - static_cast<int64_t>(ch) * KC;
+    const int cnt = static_cast<int>(left < KC ? left : KC);
+    const int st = ch % STAGES;
+    float* buf = ring + st * KC * S::LDT;
+    const uint32_t row_bytes = static_cast<uint32_t>(ldt) * 4u;
+    float* row = buf + lane * S::LDT;
+    int64_t v = 0;
+    if (lane < cnt) {
+        v = static_cast<int64_t>(col_idx[kb + lane]) - col_lo;
+        row[aug] = values[kb + lane];
+    }
+    __syncwarp();  // the rating writes happen-before lane 0's releasing arrive
+    if (lane == 0) mbar_expect_tx(&bars[st], row_bytes * static_cast<uint32_t>(cnt));
+    __syncwarp();
+    if (lane < cnt) bulk_g2s(row, theta + v * ldt, row_bytes, &bars[st]);
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
 }
 
 template <int NB, bool SOLVE>
 __global__ void __launch_bounds__(FusedShape<NB>::NT, (NB >= 14 ? 2 : 4))
 fused_update_kernel(const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col_idx,
-                    const float* __restrict__ values, int64_t col_lo,
-                    const float* __restrict__ theta, int f, float lambda, int64_t rb,
-                    float* __restrict__ out_x, float* __restrict__ out_a, float* __restrict__ out_b,
+                    const float* __restrict__ values, int64_t col_lo, const float* __restrict__ theta,
+                    int f, int ldt, float lambda, int64_t rb, float* __restrict__ out_x,
+                    float* __restrict__ out_a, float* __restrict__ out_b,
                     unsigned long long* __restrict__ min_row, int32_t* __restrict__ column,
                     double* __restrict__ pivot, int64_t status_base) {
     using S = FusedShape<NB>;
     extern __shared__ __align__(16) float smem[];
-    float* tile = smem;                      // union: gather chunks | packed L
-    float* colbuf = smem + S::UNION_FLOATS;  // 2 x FP
-    float* dinv = colbuf + 2 * S::FP;        // FP
+    float* ring = smem;                            // STAGES x KC x LDT  | later: packed L + y
+    float* panel = smem + S::UNION_FLOATS;         // 8 x FP (k-major: panel[k*FP + row])
+    float* dblk = panel + 8 * S::FP;               // 8 x 8 factored diagonal block
+    float* dinv = dblk + 64;                       // FP: 1 / L[c][c]
+    int* flags = reinterpret_cast<int*>(dinv + S::FP);  // [0] breakdown column+1, [1] pivot bits
+    uint64_t* bars = reinterpret_cast<uint64_t*>(
+        (reinterpret_cast<uintptr_t>(flags + 8) + 7) & ~static_cast<uintptr_t>(7));
 
     const int tid = threadIdx.x;
+    const int warp = tid >> 5;
+    const int aug = ldt;  // augmented (rating) column
     const int64_t row = blockIdx.x;
     const int64_t u = rb + row;
     const int64_t k0 = row_ptr[u], k1 = row_ptr[u + 1];
+    const int64_t n = k1 - k0;
     const bool active = tid < S::NTILES;
     int bi = 0, bj = 0;
-    if (active) tile_coords(tid, bi, bj);
-    const int offA0 = 4 * swz_block_half(bi, 0), offA1 = 4 * swz_block_half(bi, 1);
-    const int offB0 = 4 * swz_block_half(bj, 0), offB1 = 4 * swz_block_half(bj, 1);
-    const bool vec16 = ((f & 3) == 0) && ((reinterpret_cast<uintptr_t>(theta) & 15) == 0);
+    if (active) tile_coords_colmajor(tid, NB, bi, bj);
+    const int ia = 8 * bi, jb = 8 * bj;
 
     float acc[8][8];
 #pragma unroll
@@ -197,16 +179,49 @@ fused_update_kernel(const int64_t* __restrict__ row_ptr, const int32_t* __restri
 #pragma unroll
         for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
 
-    zero_padding<NB>(tile, f);
-    accumulate_row<NB>(acc, tile, col_idx, values, theta, col_lo, f, vec16, k0, k1, active, offA0,
-                       offA1, offB0, offB1);
+    // zero the ring once (padding columns must read as 0); init stage barriers
+    for (int e = tid; e < S::RING_FLOATS / 4; e += S::NT) reinterpret_cast<float4*>(ring)[e] = make_float4(0, 0, 0, 0);
+    uint64_t* empty = bars + STAGES;  // consumer release: one arrive per warp
+    if (tid == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(&bars[s], 1);
+            mbar_init(&empty[s], S::NT / 32);
+        }
+        flags[0] = 0;
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+    __syncthreads();
+
+    // ---- Hermitian + bias: stream the row's factor rows through the TMA ring ----
+    const int nchunks = static_cast<int>((n + KC - 1) / KC);
+    if (warp == 0) {
+        for (int ch = 0; ch < STAGES - 1 && ch < nchunks; ++ch)
+            issue_chunk<NB>(ring, bars, col_idx, values, theta, col_lo, ldt, aug, k0, n, ch);
+    }
+    for (int ch = 0; ch < nchunks; ++ch) {
+        const int nx = ch + STAGES - 1;
+        if (warp == 0 && nx < nchunks) {
+            // refill the stage consumed at iteration ch-1 once every warp released it
+            mbar_wait(&empty[nx % STAGES], static_cast<uint32_t>(((nx / STAGES) - 1) & 1));
+            issue_chunk<NB>(ring, bars, col_idx, values, theta, col_lo, ldt, aug, k0, n, nx);
+        }
+        const int st = ch % STAGES;
+        mbar_wait(&bars[st], static_cast<uint32_t>((ch / STAGES) & 1));
+        const int64_t left = n - static_cast<int64_t>(ch) * KC;
+        const int cnt = static_cast<int>(left < KC ? left : KC);
+        if (active) outer_accumulate<S::LDT, false>(acc, ring + st * KC * S::LDT, cnt, ia, jb);
+        __syncwarp();
+        if ((tid & 31) == 0) mbar_arrive(&empty[st]);
+    }
+    __syncthreads();  // all chunks consumed before the ring is reused
 
     // lambda * n_u on the diagonal (solver.hpp:141,152), float arithmetic
-    const float reg = lambda * static_cast<float>(k1 - k0);
+    const float reg = lambda * static_cast<float>(n);
     if (active && bi == bj) {
 #pragma unroll
         for (int i = 0; i < 8; ++i)
-            if (8 * bi + i < f) acc[i][i] += reg;
+            if (ia + i < f) acc[i][i] += reg;
     }
 
     if constexpr (!SOLVE) {
@@ -217,100 +232,114 @@ fused_update_kernel(const int64_t* __restrict__ row_ptr, const int32_t* __restri
         for (int ii = 0; ii < 8; ++ii)
 #pragma unroll
             for (int jj = 0; jj < 8; ++jj) {
-                const int i = 8 * bi + ii, j = 8 * bj + jj;
-                if (j > i || j >= f || i > f) continue;
-                if (i == f) {
+                const int i = ia + ii, j = jb + jj;
+                if (j > i || j >= f) continue;
+                if (i == aug) {
                     b_out[j] = acc[ii][jj];
-                } else {
+                } else if (i < f) {
                     a_out[i * f + j] = acc[ii][jj];
                     a_out[j * f + i] = acc[ii][jj];
                 }
             }
         return;
     } else {
+        float* x = out_x + row * f;
         // all-zero A (empty row with lambda*0, or zero factors) => x = 0 (solver.hpp:215-220)
         int nz = 0;
         if (active) {
 #pragma unroll
             for (int ii = 0; ii < 8; ++ii)
 #pragma unroll
-                for (int jj = 0; jj < 8; ++jj) {
-                    const int i = 8 * bi + ii, j = 8 * bj + jj;
-                    if (i < f && j <= i) nz |= (acc[ii][jj] != 0.f);
-                }
+                for (int jj = 0; jj < 8; ++jj)
+                    if (ia + ii < f && jb + jj <= ia + ii) nz |= (acc[ii][jj] != 0.f);
         }
-        float* x = out_x + row * f;
         if (!__syncthreads_or(nz)) {
             for (int i = tid; i < f; i += S::NT) x[i] = 0.f;
             if (tid == 0) column[row] = 0;
             return;
         }
 
-        // ---- in-register right-looking Cholesky of the augmented system ----
-        bool broke = false;
-        for (int c = 0; c < f; ++c) {
-            const int bc = c >> 3, jc = c & 7;
-            float* cb = colbuf + (c & 1) * S::FP;
-            if (active && bj == bc) {
+        // ---- blocked right-looking Cholesky in registers ----
+        const int nbc = (f + 7) >> 3;  // block columns holding real columns
+        for (int bc = 0; bc < nbc; ++bc) {
+            // (A) diagonal tile owner factors its 8x8 block (real columns only)
+            if (active && bi == bc && bj == bc) {
+                int bad = 0;
 #pragma unroll
-                for (int jj = 0; jj < 8; ++jj)
-                    if (jj == jc) {
-#pragma unroll
-                        for (int ii = 0; ii < 8; ++ii) cb[8 * bi + ii] = acc[ii][jj];
+                for (int c = 0; c < 8; ++c) {
+                    if (bad || 8 * bc + c >= f) continue;
+                    const float d = acc[c][c];
+                    if (!(d > 0.f)) {
+                        bad = 8 * bc + c + 1;
+                        flags[1] = __float_as_int(d);
+                        continue;
                     }
+                    const float l = sqrtf(d), inv = 1.0f / l;
+                    acc[c][c] = l;
+                    dinv[8 * bc + c] = inv;
+#pragma unroll
+                    for (int r = c + 1; r < 8; ++r) acc[r][c] *= inv;
+#pragma unroll
+                    for (int r = c + 1; r < 8; ++r)
+#pragma unroll
+                        for (int q = c + 1; q <= r; ++q) acc[r][q] = fmaf(-acc[r][c], acc[q][c], acc[r][q]);
+                }
+                flags[0] = bad;
+#pragma unroll
+                for (int r = 0; r < 8; ++r)
+#pragma unroll
+                    for (int c = 0; c < 8; ++c) dblk[r * 8 + c] = acc[r][c];
             }
             __syncthreads();
-            const float d = cb[c];
-            if (!(d > 0.f)) {  // uniform across the CTA
+            if (flags[0]) {  // uniform: breakdown at column flags[0]-1
                 if (tid == 0) {
-                    column[row] = c + 1;
-                    pivot[row] = static_cast<double>(d);
+                    column[row] = flags[0];
+                    pivot[row] = static_cast<double>(__int_as_float(flags[1]));
                     atomicMin(min_row, static_cast<unsigned long long>(status_base + row));
                 }
-                broke = true;
-                break;
+                for (int i = tid; i < f; i += S::NT) x[i] = 0.f;
+                return;
             }
-            const float rinv = rsqrtf(d);
-            if (tid == 0) dinv[c] = rinv;
-            if (active && bj >= bc) {
-                float li[8], lj[8];
+            // (B) panel tiles (bi > bc, bj == bc): L_panel = P * L_cc^{-T}, row by row forward
+            //     substitution; publish transposed (k-major) for the rank-8 downdate
+            if (active && bj == bc && bi > bc) {
 #pragma unroll
-                for (int ii = 0; ii < 8; ++ii) li[ii] = cb[8 * bi + ii] * rinv;
+                for (int c = 0; c < 8; ++c) {
+                    const float di = (8 * bc + c < f) ? dinv[8 * bc + c] : 0.f;
 #pragma unroll
-                for (int jj = 0; jj < 8; ++jj) lj[jj] = cb[8 * bj + jj] * rinv;
-                const bool diag = (bi == bj);
+                    for (int r = 0; r < 8; ++r) {
+                        float s = acc[r][c];
 #pragma unroll
-                for (int ii = 0; ii < 8; ++ii)
-#pragma unroll
-                    for (int jj = 0; jj < 8; ++jj) {
-                        const bool upd = (8 * bj + jj > c) && (!diag || ii >= jj);
-                        if (upd) acc[ii][jj] = fmaf(-li[ii], lj[jj], acc[ii][jj]);
+                        for (int k = 0; k < c; ++k) s = fmaf(-acc[r][k], dblk[c * 8 + k], s);
+                        acc[r][c] = s * di;
                     }
-                if (bj == bc) {
+                }
 #pragma unroll
-                    for (int jj = 0; jj < 8; ++jj)
-                        if (jj == jc) {
-#pragma unroll
-                            for (int ii = 0; ii < 8; ++ii) acc[ii][jj] = li[ii];
-                        }
+                for (int c = 0; c < 8; ++c) {
+                    float4* dst = reinterpret_cast<float4*>(panel + c * S::FP + ia);
+                    dst[0] = make_float4(acc[0][c], acc[1][c], acc[2][c], acc[3][c]);
+                    dst[1] = make_float4(acc[4][c], acc[5][c], acc[6][c], acc[7][c]);
                 }
             }
-        }
-        if (broke) {
-            for (int i = tid; i < f; i += S::NT) x[i] = 0.f;
-            return;
+            __syncthreads();
+            // (C) trailing tiles (bj > bc): rank-8 downdate with the published panel
+            if (active && bj > bc) outer_accumulate<S::FP, true>(acc, panel, 8, ia, jb);
         }
         if (tid == 0) column[row] = 0;
 
-        // ---- dump packed L (rows < f) and y (row f) into the gather area ----
-        float* lpk = tile;
+        // ---- dump packed L (rows < f) and y (row aug) into the ring area ----
+        __syncthreads();
+        float* lpk = ring;
+        float* yrow = lpk + f * (f + 1) / 2;
         if (active) {
 #pragma unroll
             for (int ii = 0; ii < 8; ++ii)
 #pragma unroll
                 for (int jj = 0; jj < 8; ++jj) {
-                    const int i = 8 * bi + ii, j = 8 * bj + jj;
-                    if (i <= f && j < f && j <= i) lpk[i * (i + 1) / 2 + j] = acc[ii][jj];
+                    const int i = ia + ii, j = jb + jj;
+                    if (j >= f || j > i) continue;
+                    if (i < f) lpk[i * (i + 1) / 2 + j] = acc[ii][jj];
+                    else if (i == aug) yrow[j] = acc[ii][jj];
                 }
         }
         __syncthreads();
@@ -319,7 +348,6 @@ fused_update_kernel(const int64_t* __restrict__ row_ptr, const int32_t* __restri
         if (tid < 32) {
             const int lane = tid;
             constexpr int G = (S::FP + 31) / 32;
-            const float* yrow = lpk + f * (f + 1) / 2;
             float yv[G];
 #pragma unroll
             for (int g = 0; g < G; ++g) {
@@ -351,33 +379,59 @@ fused_update_kernel(const int64_t* __restrict__ row_ptr, const int32_t* __restri
 }
 
 template <int NB, bool SOLVE>
-void launch_fused(const DevCsr& r, const float* theta, int f, float lambda, int64_t rb, int64_t re,
+void launch_fused(const DevCsr& r, const float* theta, int f, int ldt, float lambda, int64_t rb, int64_t re,
                   float* x, float* a, float* b, const SolveStatus* st, cudaStream_t s) {
     using S = FusedShape<NB>;
     auto k = fused_update_kernel<NB, SOLVE>;
     ALSK_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMEM));
     constexpr int64_t kMaxGrid = 1LL << 30;
     for (int64_t b0 = rb; b0 < re; b0 += kMaxGrid) {
-        const int64_t n = std::min<int64_t>(re - b0, kMaxGrid);
+        const int64_t cnt = std::min<int64_t>(re - b0, kMaxGrid);
         const int64_t off = b0 - rb;
-        k<<<static_cast<unsigned>(n), S::NT, S::SMEM, s>>>(
-            r.row_ptr, r.col_idx, r.values, r.col_offset, theta, f, lambda, b0,
+        k<<<static_cast<unsigned>(cnt), S::NT, S::SMEM, s>>>(
+            r.row_ptr, r.col_idx, r.values, r.col_offset, theta, f, ldt, lambda, b0,
             x ? x + off * f : nullptr, a ? a + off * f * f : nullptr, b ? b + off * f : nullptr,
-            st ? st->min_row : nullptr, st ? st->column + off : nullptr,
-            st ? st->pivot + off : nullptr, off);
+            st ? st->min_row : nullptr, st ? st->column + off : nullptr, st ? st->pivot + off : nullptr, off);
         ALSK_LAUNCHED();
     }
 }
 
+// theta with a row stride that is a multiple of 4 floats and a 16-byte aligned base, as the
+// bulk copies require; copies (zero padded) only when the caller's layout does not qualify.
+struct StridedTheta {
+    const float* ptr;
+    int ldt;
+    DevBuf owned;
+};
+
+void strided_theta(StridedTheta& t, const float* theta, int64_t theta_rows, int f, cudaStream_t s) {
+    t.ptr = theta;
+    t.ldt = f;
+    const bool ok = (f % 4 == 0) && ((reinterpret_cast<uintptr_t>(theta) & 15) == 0);
+    if (ok) return;
+    t.ldt = (f + 3) & ~3;
+    const int64_t rows = std::max<int64_t>(theta_rows, 1);
+    t.owned.alloc(sizeof(float) * rows * t.ldt, s);
+    ALSK_CUDA(cudaMemsetAsync(t.owned.as<void>(), 0, sizeof(float) * rows * t.ldt, s));
+    if (theta_rows > 0)
+        ALSK_CUDA(cudaMemcpy2DAsync(t.owned.as<float>(), sizeof(float) * t.ldt, theta, sizeof(float) * f,
+                                    sizeof(float) * f, theta_rows, cudaMemcpyDeviceToDevice, s));
+    t.ptr = t.owned.as<float>();
+}
+
 template <bool SOLVE>
-bool dispatch(const DevCsr& r, const float* theta, int f, float lambda, int64_t rb, int64_t re,
-              float* x, float* a, float* b, const SolveStatus* st, cudaStream_t s) {
-    const int need = (f + 1 + 7) / 8;
+bool dispatch(const DevCsr& r, const float* theta, int64_t theta_rows, int f, float lambda, int64_t rb,
+              int64_t re, float* x, float* a, float* b, const SolveStatus* st, cudaStream_t s) {
+    const int ldt = (f + 3) & ~3;
+    const int need = (ldt + 1 + 7) / 8;
+    if (need > 16) return false;
     if (re <= rb) return true;
-#define ALSK_FUSED_CASE(NBV)                                                     \
-    if (need <= NBV) {                                                          \
-        launch_fused<NBV, SOLVE>(r, theta, f, lambda, rb, re, x, a, b, st, s); \
-        return true;                                                            \
+    StridedTheta th;
+    strided_theta(th, theta, theta_rows, f, s);
+#define ALSK_FUSED_CASE(NBV)                                                                     \
+    if (need <= NBV) {                                                                          \
+        launch_fused<NBV, SOLVE>(r, th.ptr, f, th.ldt, lambda, rb, re, x, a, b, st, s);         \
+        return true;                                                                            \
     }
     ALSK_FUSED_CASE(2)
     ALSK_FUSED_CASE(4)
@@ -391,14 +445,14 @@ bool dispatch(const DevCsr& r, const float* theta, int f, float lambda, int64_t 
 
 }  // namespace
 
-bool update_fused_fp32(const DevCsr& r, const float* theta, int f, float lambda, int64_t rb,
+bool update_fused_fp32(const DevCsr& r, const float* theta, int64_t theta_rows, int f, float lambda, int64_t rb,
                        int64_t re, float* x_out, const SolveStatus& st, cudaStream_t s) {
-    return dispatch<true>(r, theta, f, lambda, rb, re, x_out, nullptr, nullptr, &st, s);
+    return dispatch<true>(r, theta, theta_rows, f, lambda, rb, re, x_out, nullptr, nullptr, &st, s);
 }
 
-bool hermitian_fused_fp32(const DevCsr& r, const float* theta, int f, float lambda, int64_t rb,
+bool hermitian_fused_fp32(const DevCsr& r, const float* theta, int64_t theta_rows, int f, float lambda, int64_t rb,
                           int64_t re, float* A, float* B, cudaStream_t s) {
-    return dispatch<false>(r, theta, f, lambda, rb, re, nullptr, A, B, nullptr, s);
+    return dispatch<false>(r, theta, theta_rows, f, lambda, rb, re, nullptr, A, B, nullptr, s);
 }
 
 }  // namespace alsk

@@ -51,12 +51,12 @@ void solve_exact(const float* A, const float* B, int64_t count, int f, bool zero
 // FP32 fused assembly + in-register Cholesky for rows [rb,re) -> X rows (x_out[(u-rb)*f]).
 // Returns false if f is outside the fused kernel's range (caller falls back to the
 // materialised FP32 path).
-bool update_fused_fp32(const DevCsr& r, const float* theta, int f, float lambda, int64_t rb,
-                       int64_t re, float* x_out, const SolveStatus& st, cudaStream_t s);
+bool update_fused_fp32(const DevCsr& r, const float* theta, int64_t theta_rows, int f, float lambda,
+                       int64_t rb, int64_t re, float* x_out, const SolveStatus& st, cudaStream_t s);
 
 // FP32 register-blocked assembly only (materialised output) — the hermitian timed alone.
-bool hermitian_fused_fp32(const DevCsr& r, const float* theta, int f, float lambda, int64_t rb,
-                          int64_t re, float* A, float* B, cudaStream_t s);
+bool hermitian_fused_fp32(const DevCsr& r, const float* theta, int64_t theta_rows, int f, float lambda,
+                          int64_t rb, int64_t re, float* A, float* B, cudaStream_t s);
 
 // Packed-lower double partial Hermitian (data-parallel split) and its solve.
 void partial_hermitian_packed(const DevCsr& r, const float* theta, int f, double lambda,

@@ -17,7 +17,7 @@ if [[ $STEP == all || $STEP == ncu ]]; then
   timeout 900 /usr/local/cuda/bin/ncu --metrics gpu__time_duration.sum --clock-control none -c 60 --csv \
      --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu > gpurun_out/ncu_bench.log 2>&1
   echo "ncu launches exit $?" >> gpurun_out/status.txt
-  timeout 900 /usr/local/cuda/bin/ncu --set full --clock-control none --import-source on -k regex:fused_update -s 2 -c 1 \
+  timeout 900 /usr/local/cuda/bin/ncu --set full --clock-control none --import-source on -k regex:fused_update -s 2 -c 2 \
      -o gpurun_out/prof_fused python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu > gpurun_out/ncu_full.log 2>&1
   echo "ncu full exit $?" >> gpurun_out/status.txt
 fi
