@@ -199,7 +199,7 @@ def run_ours(args):
     import torch.distributed as dist
     from paper_1603_03820_b200 import _native as N
     from paper_1603_03820_b200 import alskit as A
-    from paper_1603_03820_b200.session import DeviceCsr, dev_update, PREC_FP32
+    from paper_1603_03820_b200.session import DeviceCsr, PREC_FP32
 
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
@@ -211,24 +211,11 @@ def run_ours(args):
     nz_train = int(train.row_ptr[-1])
     R = DeviceCsr.from_host(train, dev)
     RT = R.transpose()
-    # padded, equal-count row slices for the in-place all-gather (NCCL needs equal counts)
-    cx, ct = -(-m // world), -(-n // world)
-    X = torch.zeros(cx * world * f, dtype=torch.float32, device=dev)
-    T = torch.zeros(ct * world * f, dtype=torch.float32, device=dev)
-    X[: m * f].copy_(torch.from_numpy(A.random_factor(m, f, 42).entries))
-    T[: n * f].copy_(torch.from_numpy(A.random_factor(n, f, A.mix_seed(42, 1)).entries))
-    xr = (rank * cx, min(m, (rank + 1) * cx))
-    tr = (rank * ct, min(n, (rank + 1) * ct))
-
-    def half(Rd, theta, theta_rows, out, rows, chunk, rng):
-        if rng[1] > rng[0]:
-            dev_update(Rd, theta, theta_rows, f, lam, PREC_FP32, out[rng[0] * f:], rng[0], rng[1])
-        if world > 1:
-            dist.all_gather_into_tensor(out, out[rank * chunk * f:(rank + 1) * chunk * f])
-
-    def step():
-        half(R, T, n, X, m, cx, xr)
-        half(RT, X, m, T, n, ct, tr)
+    from paper_1603_03820_b200.distributed import ModelParallelALS
+    als = ModelParallelALS(R, RT, m, n, f, lam, PREC_FP32,
+                           torch.from_numpy(A.random_factor(m, f, 42).entries).to(dev),
+                           torch.from_numpy(A.random_factor(n, f, A.mix_seed(42, 1)).entries).to(dev))
+    step = als.step
 
     for _ in range(args.warmup):
         step()
@@ -263,6 +250,7 @@ def run_ours(args):
         rows = torch.from_numpy(tt["row"].copy()).to(dev)
         cols = torch.from_numpy(tt["col"].copy()).to(dev)
         vals = torch.from_numpy(tt["value"].copy()).to(dev)
+        X, T = als.factors()
         A._check(N.LIB.alsk_dev_rmse(rows.data_ptr(), cols.data_ptr(), vals.data_ptr(), len(tt), X.data_ptr(), m,
                                      T.data_ptr(), n, f, C.byref(out), torch.cuda.current_stream().cuda_stream))
         rmse = out.value

@@ -227,6 +227,21 @@ alsk_status alsk_dev_hermitian(const alsk_csr* r, const float* theta, int64_t th
                                double lambda, alsk_precision precision, int64_t row_begin,
                                int64_t row_end, float* a_out, float* b_out, void* stream);
 
+/* ---- device-resident session (als_train / train_run caller) ---- */
+/* R (CSR) and R^T (the CSC arrays of R, read as the CSR of R^T) are uploaded once; X and
+ * Theta stay in HBM across half-sweeps. Host copies are made only on request. */
+typedef struct alsk_session alsk_session;
+alsk_status alsk_session_create(const alsk_csr* r, const int64_t* col_ptr, const int32_t* row_idx,
+                                const float* csc_values, const alsk_triplet* test, int64_t test_count,
+                                int f, double lambda, alsk_precision precision, int64_t batch_rows,
+                                const float* x0, const float* theta0, alsk_session** out);
+alsk_status alsk_session_half_x(alsk_session* s);      /* X = update_x(R, Theta)   */
+alsk_status alsk_session_half_theta(alsk_session* s);  /* Theta = update_x(R^T, X) */
+alsk_status alsk_session_loss(alsk_session* s, double* out);
+alsk_status alsk_session_rmse(alsk_session* s, double* out); /* NaN when there is no test set */
+alsk_status alsk_session_factors(alsk_session* s, float* x_out, float* theta_out);
+void alsk_session_destroy(alsk_session* s);
+
 /* ---- host data helpers (dataio/factor restatements used by the drivers) ------------ */
 
 /* random_factor (factor.hpp:49-54) and mix_seed (common.hpp:70-75), bit-exact. */

@@ -71,5 +71,27 @@ def build(verbose: bool = False) -> Path:
     return LIB
 
 
+CPP_TESTS = [ROOT / "tests" / "cpp" / "dropin_test.cpp"]
+
+
+def build_cpp_tests(verbose: bool = False) -> list[Path]:
+    """Compile the C++ drop-in API tests (include/alskit/*.hpp over libalskit_cuda.so)."""
+    lib = build(verbose)
+    outs = []
+    for src in CPP_TESTS:
+        exe = src.with_suffix("")
+        if exe.exists() and exe.stat().st_mtime >= max(src.stat().st_mtime, lib.stat().st_mtime,
+                                                         max(h.stat().st_mtime for h in (INCLUDE / "alskit").glob("*.hpp"))):
+            outs.append(exe)
+            continue
+        cmd = ["g++", "-std=c++20", "-O2", f"-I{INCLUDE}", str(src), f"-L{PKG}", "-lalskit_cuda",
+               "-Wl,-rpath,$ORIGIN/../../paper_1603_03820_b200", "-o", str(exe)]
+        res = subprocess.run(cmd, capture_output=True, text=True)
+        if res.returncode != 0:
+            raise RuntimeError(f"C++ drop-in test build failed\n{res.stderr[-4000:]}")
+        outs.append(exe)
+    return outs
+
+
 if __name__ == "__main__":
     print(build(verbose=True))

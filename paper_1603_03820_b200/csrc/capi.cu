@@ -7,6 +7,7 @@
 #include <atomic>
 #include <cstdio>
 #include <cstring>
+#include <limits>
 #include <string>
 #include <vector>
 
@@ -651,6 +652,138 @@ alsk_status alsk_dev_solve_packed(const double* packed, int64_t count, int f, fl
         solve_exact(A.as<float>(), B.as<float>(), count, f, false, x_out, sb.st, s);
         sb.raise_if_broken(s, 0);
     });
+}
+
+// ---- device-resident session ------------------------------------------------------
+struct alsk_session {
+    int64_t m = 0, n = 0, nnz = 0, test_count = 0;
+    int f = 0;
+    double lambda = 0.0;
+    alsk_precision precision = ALSK_PREC_FP32;
+    int64_t batch_rows = 4096;
+    cudaStream_t stream = nullptr;
+    DevBuf rp, ci, rv, cp, ri, cv, col_nnz, X, T, tr, tc, tv;
+    DevCsr R, RT;
+};
+
+alsk_status alsk_session_create(const alsk_csr* r, const int64_t* col_ptr, const int32_t* row_idx,
+                                const float* csc_values, const alsk_triplet* test, int64_t test_count,
+                                int f, double lambda, alsk_precision precision, int64_t batch_rows,
+                                const float* x0, const float* theta0, alsk_session** out) {
+    return guard([&] {
+        if (f < 1) fail_input("rank must be >= 1");
+        require_device();
+        auto* S = new alsk_session();
+        try {
+            S->m = r->rows;
+            S->n = r->cols;
+            S->nnz = r->nnz;
+            S->f = f;
+            S->lambda = lambda;
+            S->precision = precision;
+            S->batch_rows = batch_rows;
+            ALSK_CUDA(cudaStreamCreateWithFlags(&S->stream, cudaStreamNonBlocking));
+            cudaStream_t s = S->stream;
+            const int64_t nz = std::max<int64_t>(r->nnz, 1);
+            S->rp.alloc(sizeof(int64_t) * (S->m + 1), s);
+            S->ci.alloc(sizeof(int32_t) * nz, s);
+            S->rv.alloc(sizeof(float) * nz, s);
+            h2d(S->rp.as<int64_t>(), r->row_ptr, S->m + 1, s);
+            h2d(S->ci.as<int32_t>(), r->col_idx, r->nnz, s);
+            h2d(S->rv.as<float>(), r->values, r->nnz, s);
+            S->R = DevCsr{S->m, S->n, 0, r->nnz, S->rp.as<int64_t>(), S->ci.as<int32_t>(), S->rv.as<float>()};
+            S->cp.alloc(sizeof(int64_t) * (S->n + 1), s);
+            S->ri.alloc(sizeof(int32_t) * nz, s);
+            S->cv.alloc(sizeof(float) * nz, s);
+            if (col_ptr) {
+                h2d(S->cp.as<int64_t>(), col_ptr, S->n + 1, s);
+                h2d(S->ri.as<int32_t>(), row_idx, r->nnz, s);
+                h2d(S->cv.as<float>(), csc_values, r->nnz, s);
+            } else {
+                csr_to_csc_device(S->R, S->cp.as<int64_t>(), S->ri.as<int32_t>(), S->cv.as<float>(), s);
+            }
+            S->RT = DevCsr{S->n, S->m, 0, r->nnz, S->cp.as<int64_t>(), S->ri.as<int32_t>(), S->cv.as<float>()};
+            S->col_nnz.alloc(sizeof(int64_t) * std::max<int64_t>(S->n, 1), s);
+            column_counts(S->R, S->col_nnz.as<int64_t>(), s);
+            S->X.alloc(sizeof(float) * std::max<int64_t>(S->m * f, 1), s);
+            S->T.alloc(sizeof(float) * std::max<int64_t>(S->n * f, 1), s);
+            h2d(S->X.as<float>(), x0, S->m * f, s);
+            h2d(S->T.as<float>(), theta0, S->n * f, s);
+            S->test_count = test_count;
+            if (test_count > 0) {
+                std::vector<int64_t> hr(test_count), hc(test_count);
+                std::vector<float> hv(test_count);
+                for (int64_t i = 0; i < test_count; ++i) {
+                    hr[i] = test[i].row;
+                    hc[i] = test[i].col;
+                    hv[i] = test[i].value;
+                }
+                S->tr.alloc(sizeof(int64_t) * test_count, s);
+                S->tc.alloc(sizeof(int64_t) * test_count, s);
+                S->tv.alloc(sizeof(float) * test_count, s);
+                h2d(S->tr.as<int64_t>(), hr.data(), test_count, s);
+                h2d(S->tc.as<int64_t>(), hc.data(), test_count, s);
+                h2d(S->tv.as<float>(), hv.data(), test_count, s);
+                ALSK_CUDA(cudaStreamSynchronize(s));
+            }
+            ALSK_CUDA(cudaStreamSynchronize(s));
+        } catch (...) {
+            delete S;
+            throw;
+        }
+        *out = S;
+    });
+}
+
+alsk_status alsk_session_half_x(alsk_session* S) {
+    return guard([&] {
+        update_rows_device(S->R, S->T.as<float>(), S->n, S->f, S->lambda, S->precision == ALSK_PREC_FP64_EXACT,
+                           S->batch_rows, 0, S->m, S->X.as<float>(), S->stream);
+    });
+}
+
+alsk_status alsk_session_half_theta(alsk_session* S) {
+    return guard([&] {
+        update_rows_device(S->RT, S->X.as<float>(), S->m, S->f, S->lambda, S->precision == ALSK_PREC_FP64_EXACT,
+                           S->batch_rows, 0, S->n, S->T.as<float>(), S->stream);
+    });
+}
+
+alsk_status alsk_session_loss(alsk_session* S, double* out) {
+    return guard([&] {
+        *out = loss_device(S->R, S->col_nnz.as<int64_t>(), S->X.as<float>(), S->T.as<float>(), S->f, S->lambda,
+                           S->stream);
+    });
+}
+
+alsk_status alsk_session_rmse(alsk_session* S, double* out) {
+    return guard([&] {
+        if (S->test_count <= 0) {
+            *out = std::numeric_limits<double>::quiet_NaN();
+            return;
+        }
+        *out = rmse_device(S->tr.as<int64_t>(), S->tc.as<int64_t>(), S->tv.as<float>(), S->test_count,
+                           S->X.as<float>(), S->m, S->T.as<float>(), S->n, S->f, S->stream);
+    });
+}
+
+alsk_status alsk_session_factors(alsk_session* S, float* x_out, float* theta_out) {
+    return guard([&] {
+        if (x_out) d2h(x_out, S->X.as<float>(), S->m * S->f, S->stream);
+        if (theta_out) d2h(theta_out, S->T.as<float>(), S->n * S->f, S->stream);
+        ALSK_CUDA(cudaStreamSynchronize(S->stream));
+    });
+}
+
+void alsk_session_destroy(alsk_session* S) {
+    if (!S) return;
+    cudaStream_t s = S->stream;
+    if (s) cudaStreamSynchronize(s);
+    delete S;  // DevBufs free on their stream
+    if (s) {
+        cudaDeviceSynchronize();
+        cudaStreamDestroy(s);
+    }
 }
 
 }  // extern "C"

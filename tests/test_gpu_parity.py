@@ -391,3 +391,31 @@ def test_als_train_ml1m_shape_rmse_parity(A, orc, gpu):
         assert abs(tr - o_train) <= 1e-4, (acc, tr, o_train)
         js = [h.train_j for h in res.history]
         assert all(b <= a * (1 + 1e-6) for a, b in zip(js, js[1:]))
+
+
+# ------------------------------------------------------------------ multi-GPU paths, 1 device
+def test_distributed_paths_single_device(A, orc, gpu):
+    """ModelParallelALS and DataParallelThetaHalf with the CUDA compute at world size 1:
+    the model-parallel step equals update_x/update_theta; the data-parallel Theta-half
+    (double partials -> round once -> reference-order solve) is bit-identical to the FP64
+    update_x of R^T."""
+    import torch
+    from paper_1603_03820_b200.distributed import DataParallelThetaHalf, ModelParallelALS
+    from paper_1603_03820_b200.session import DeviceCsr, PREC_FP64_EXACT
+    r, th = rand_csr(A, orc, 777, 300, 120, 6000, 16)
+    dev = torch.device("cuda")
+    R = DeviceCsr.from_host(r, dev)
+    RT = R.transpose()
+    x0 = A.random_factor(300, 16, 42)
+    als = ModelParallelALS(R, RT, 300, 120, 16, 0.05, PREC_FP64_EXACT, torch.from_numpy(x0.entries).to(dev),
+                           torch.from_numpy(th.entries).to(dev))
+    als.step()
+    X, T = als.factors()
+    cfg = A.SolverConfig(f=16, lambda_=0.05)
+    x1 = A.update_x(r, th, cfg)
+    t1 = A.update_theta(A.csr_to_csc(r), x1, cfg)
+    assert np.array_equal(X.cpu().numpy(), x1.entries) and np.array_equal(T.cpu().numpy(), t1.entries)
+    dp = DataParallelThetaHalf(RT, 300, 120, 16, 0.05)
+    T2 = torch.zeros(120 * 16, dtype=torch.float32, device=dev)
+    dp.half_theta(X, T2)
+    assert np.array_equal(T2.cpu().numpy(), t1.entries)
