@@ -13,7 +13,7 @@
 #include <vector>
 
 #include "alskit/alskit.hpp"  // from /root/reference/proj/include, namespace alskit_ref
-#include "alskit_cuda.h"
+#include "../include/alskit_cuda.h"  // our C ABI types only (by path: -I points at the reference)
 
 namespace R = alskit_ref;
 
