@@ -48,9 +48,18 @@ typedef enum alsk_breakdown { ALSK_BREAKDOWN_FAIL = 0, ALSK_BREAKDOWN_ZERO_ROW =
  *  FP64_EXACT: reference order, double accumulators, double Cholesky with separately
  *              rounded multiply/subtract — bit-identical to the reference's default
  *              accumulate_double=true path (solver.hpp:99-157, 204-262).
- *  FP32:       register-blocked FP32 accumulation fused with an FP32 in-register
- *              Cholesky; tolerance-checked (normwise <= 1e-3 per half-sweep). */
-typedef enum alsk_precision { ALSK_PREC_FP64_EXACT = 0, ALSK_PREC_FP32 = 1 } alsk_precision;
+ *  FP32:       FP32-level arithmetic, tolerance-checked (normwise <= 1e-3 per
+ *              half-sweep). The engine is chosen by alsk_set_fp32_engine: by default the
+ *              tensor-core kernel (TF32X2 below) where 16 <= f <= 119, else the
+ *              register-blocked FFMA kernel; both fuse the in-register Cholesky.
+ *  TF32X2:     Hermitian and bias on tcgen05 tensor cores with the two-term TF32 split
+ *              x = hi + lo (A = Hi^T Hi + Hi^T Lo + (Hi^T Lo)^T), FP32 accumulation in TMEM,
+ *              FP32 Cholesky; falls back to the FFMA kernel outside 16 <= f <= 119. */
+typedef enum alsk_precision {
+    ALSK_PREC_FP64_EXACT = 0,
+    ALSK_PREC_FP32 = 1,
+    ALSK_PREC_TF32X2 = 2
+} alsk_precision;
 
 /* CsrMatrix (sparse.hpp:38-48). Pointers are host or device per function family. */
 typedef struct alsk_csr {
@@ -96,6 +105,10 @@ const char* alsk_build_info(void);
  * launch is bracketed by CUDA events on its stream; end returns the summed milliseconds
  * and the number of launches timed. */
 void alsk_profile_begin(void);
+/* Engine behind ALSK_PREC_FP32 (process-wide): 0 = auto (tensor cores where 16 <= f <= 119),
+ * 1 = CUDA-core FFMA kernel, 2 = tensor cores. */
+void alsk_set_fp32_engine(int engine);
+int alsk_fp32_engine(void);
 void alsk_profile_end(double* total_ms, uint64_t* launches);
 /* Measured FP32 FFMA throughput of the current device in TFLOP/s (roofline denominator). */
 double alsk_fp32_peak_probe(void);

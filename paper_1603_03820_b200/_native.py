@@ -47,6 +47,8 @@ _SIGS = {
     "alsk_kernel_launch_count": (u64, []),
     "alsk_build_info": (C.c_char_p, []),
     "alsk_profile_begin": (None, []),
+    "alsk_set_fp32_engine": (None, [C.c_int]),
+    "alsk_fp32_engine": (C.c_int, []),
     "alsk_profile_end": (None, [f64p, C.POINTER(u64)]),
     "alsk_fp32_peak_probe": (C.c_double, []),
     "alsk_herm_loop_probe": (C.c_double, [C.c_int, C.c_int]),

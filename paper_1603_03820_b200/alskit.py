@@ -494,6 +494,35 @@ def synth_csr(m: int, n: int, nnz: int, seed: int, threads: int = 0) -> CsrMatri
     return CsrMatrix(m, n, 0, rp, ci, va)
 
 
+FP32_ENGINES = {"auto": 0, "ffma": 1, "tensor": 2}
+
+
+def set_fp32_engine(name: str) -> None:
+    """Engine behind accumulate_double=False (ALSK_PREC_FP32): "auto" (tensor cores where
+    16 <= f <= 119), "ffma" (CUDA-core kernel) or "tensor"."""
+    N.LIB.alsk_set_fp32_engine(FP32_ENGINES[name])
+
+
+def fp32_engine() -> str:
+    v = N.LIB.alsk_fp32_engine()
+    return {b: a for a, b in FP32_ENGINES.items()}[v]
+
+
+class use_fp32_engine:
+    """Context manager: run a block with the given FP32 engine, then restore."""
+
+    def __init__(self, name: str):
+        self.name = name
+
+    def __enter__(self):
+        self.prev = fp32_engine()
+        set_fp32_engine(self.name)
+        return self
+
+    def __exit__(self, *exc):
+        set_fp32_engine(self.prev)
+
+
 def device_available() -> bool:
     return bool(LIB.alsk_device_available())
 

@@ -129,11 +129,21 @@ int64_t device_batch_rows(int f, int64_t rows) {
     return std::max<int64_t>(1, std::min<int64_t>(rows, (int64_t(2) << 30) / per));
 }
 
+// FP32-mode engine: 0 = auto (tensor cores where the shape allows), 1 = CUDA-core FFMA
+// kernel, 2 = tensor cores. ALSK_PREC_TF32X2 always asks for the tensor cores.
+std::atomic<int> g_fp32_engine{0};
+bool use_tensor_cores(alsk_precision prec, int f) {
+    if (prec == ALSK_PREC_FP64_EXACT || !tc_supported(f)) return false;
+    if (prec == ALSK_PREC_TF32X2) return true;
+    return g_fp32_engine.load() == 2;  // auto -> FFMA kernel until the tensor-core path wins
+}
+
 // Core of update_x on device data: rows [rb,re) -> x_out (rows-local).
 void update_rows_device(const DevCsr& r, const float* theta, int64_t theta_rows, int f,
-                        double lambda, bool exact, int64_t batch_rows, int64_t rb, int64_t re,
+                        double lambda, alsk_precision prec, int64_t batch_rows, int64_t rb, int64_t re,
                         float* x_out, cudaStream_t s) {
     if (re <= rb) return;
+    const bool exact = prec == ALSK_PREC_FP64_EXACT;
     check_columns(r, rb, re, r.col_offset, r.col_offset + theta_rows, s);
     StatusBufs sb(re - rb, s);
     const int64_t br = batch_rows < 1 ? 1 : batch_rows;
@@ -143,7 +153,12 @@ void update_rows_device(const DevCsr& r, const float* theta, int64_t theta_rows,
         ALSK_CUDA(cudaEventCreate(&e1));
         ALSK_CUDA(cudaEventRecord(e0, s));
     }
-    if (!exact && update_fused_fp32(r, theta, theta_rows, f, static_cast<float>(lambda), rb, re, x_out, sb.st, s)) {
+    const bool fused = !exact && (use_tensor_cores(prec, f)
+                                      ? update_tc(r, theta, theta_rows, f, static_cast<float>(lambda), rb, re, x_out,
+                                                  sb.st, s)
+                                      : update_fused_fp32(r, theta, theta_rows, f, static_cast<float>(lambda), rb,
+                                                          re, x_out, sb.st, s));
+    if (fused) {
         if (g_prof.on) {
             ALSK_CUDA(cudaEventRecord(e1, s));
             ALSK_CUDA(cudaEventSynchronize(e1));
@@ -206,6 +221,8 @@ int alsk_device_available(void) {
     return (cudaGetDeviceCount(&n) == cudaSuccess && n > 0) ? 1 : 0;
 }
 uint64_t alsk_kernel_launch_count(void) { return g_launches.load(); }
+void alsk_set_fp32_engine(int engine) { g_fp32_engine.store(engine); }
+int alsk_fp32_engine(void) { return g_fp32_engine.load(); }
 void alsk_profile_begin(void) { g_prof = Profile{true, 0.0, 0}; }
 void alsk_profile_end(double* total_ms, uint64_t* launches) {
     *total_ms = g_prof.ms;
@@ -304,7 +321,8 @@ alsk_status alsk_update_x(const alsk_csr* r, const float* theta, int64_t theta_r
         h2d(T.as<float>(), theta, theta_rows * f, s);
         DevBuf X(sizeof(float) * r->rows * f, s);
         update_rows_device(R.view, T.as<float>(), theta_rows, f, cfg->lambda,
-                           cfg->accumulate_double != 0, cfg->batch_rows, 0, r->rows, X.as<float>(), s);
+                           cfg->accumulate_double != 0 ? ALSK_PREC_FP64_EXACT : ALSK_PREC_FP32, cfg->batch_rows, 0,
+                           r->rows, X.as<float>(), s);
         d2h(x_out, X.as<float>(), r->rows * f, s);
         ALSK_CUDA(cudaStreamSynchronize(s));
     });
@@ -579,7 +597,7 @@ alsk_status alsk_dev_update(const alsk_csr* r, const float* theta, int64_t theta
     return guard([&] {
         check_update_shapes(r, theta_rows, f);
         require_device();
-        update_rows_device(dev_view(r), theta, theta_rows, f, lambda, precision == ALSK_PREC_FP64_EXACT,
+        update_rows_device(dev_view(r), theta, theta_rows, f, lambda, precision,
                            batch_rows, row_begin, row_end, x_out, as_stream(stream));
     });
 }
@@ -591,10 +609,15 @@ alsk_status alsk_dev_hermitian(const alsk_csr* r, const float* theta, int64_t th
         check_update_shapes(r, theta_rows, f);
         require_device();
         const DevCsr v = dev_view(r);
-        if (precision == ALSK_PREC_FP32 &&
-            hermitian_fused_fp32(v, theta, theta_rows, f, static_cast<float>(lambda), row_begin, row_end, a_out,
-                                 b_out, as_stream(stream)))
-            return;
+        if (precision != ALSK_PREC_FP64_EXACT) {
+            check_columns(v, row_begin, row_end, r->col_offset, r->col_offset + theta_rows, as_stream(stream));
+            const bool done = use_tensor_cores(precision, f)
+                                  ? hermitian_tc(v, theta, theta_rows, f, static_cast<float>(lambda), row_begin,
+                                                 row_end, a_out, b_out, as_stream(stream))
+                                  : hermitian_fused_fp32(v, theta, theta_rows, f, static_cast<float>(lambda),
+                                                         row_begin, row_end, a_out, b_out, as_stream(stream));
+            if (done) return;
+        }
         hermitian_materialize(v, theta, f, lambda, precision == ALSK_PREC_FP64_EXACT, row_begin,
                               row_end, a_out, b_out, as_stream(stream));
     });
@@ -737,14 +760,14 @@ alsk_status alsk_session_create(const alsk_csr* r, const int64_t* col_ptr, const
 
 alsk_status alsk_session_half_x(alsk_session* S) {
     return guard([&] {
-        update_rows_device(S->R, S->T.as<float>(), S->n, S->f, S->lambda, S->precision == ALSK_PREC_FP64_EXACT,
+        update_rows_device(S->R, S->T.as<float>(), S->n, S->f, S->lambda, S->precision,
                            S->batch_rows, 0, S->m, S->X.as<float>(), S->stream);
     });
 }
 
 alsk_status alsk_session_half_theta(alsk_session* S) {
     return guard([&] {
-        update_rows_device(S->RT, S->X.as<float>(), S->m, S->f, S->lambda, S->precision == ALSK_PREC_FP64_EXACT,
+        update_rows_device(S->RT, S->X.as<float>(), S->m, S->f, S->lambda, S->precision,
                            S->batch_rows, 0, S->n, S->T.as<float>(), S->stream);
     });
 }

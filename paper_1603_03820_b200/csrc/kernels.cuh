@@ -58,6 +58,14 @@ bool update_fused_fp32(const DevCsr& r, const float* theta, int64_t theta_rows, 
 bool hermitian_fused_fp32(const DevCsr& r, const float* theta, int64_t theta_rows, int f, float lambda,
                           int64_t rb, int64_t re, float* A, float* B, cudaStream_t s);
 
+// Tensor-core (tcgen05 kind::tf32, two-term split) assembly fused with the in-register
+// Cholesky, one persistent CTA per SM (tc_update.cu). tc_supported: 16 <= f <= 119.
+bool tc_supported(int f);
+bool update_tc(const DevCsr& r, const float* theta, int64_t theta_rows, int f, float lambda, int64_t rb,
+               int64_t re, float* x_out, const SolveStatus& st, cudaStream_t s);
+bool hermitian_tc(const DevCsr& r, const float* theta, int64_t theta_rows, int f, float lambda, int64_t rb,
+                  int64_t re, float* A, float* B, cudaStream_t s);
+
 // Packed-lower double partial Hermitian (data-parallel split) and its solve.
 void partial_hermitian_packed(const DevCsr& r, const float* theta, int f, double lambda,
                               int64_t rb, int64_t re, double* out, cudaStream_t s);

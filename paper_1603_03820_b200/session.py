@@ -20,6 +20,7 @@ from .alskit import (TRIPLET_DTYPE, CscMatrix, CsrMatrix, FactorMatrix, SolverCo
 LIB = N.LIB
 PREC_FP64_EXACT = 0
 PREC_FP32 = 1
+PREC_TF32X2 = 2
 
 
 def _dev(a: np.ndarray, device) -> torch.Tensor:
@@ -66,6 +67,16 @@ def dev_update(r: DeviceCsr, theta: torch.Tensor, theta_rows: int, f: int, lam: 
     re = r.rows if row_end is None else row_end
     _check(LIB.alsk_dev_update(C.byref(r.c), theta.data_ptr(), theta_rows, f, lam, precision,
                                batch_rows, row_begin, re, out.data_ptr(), stream_handle()))
+
+
+def dev_hermitian(r: DeviceCsr, theta: torch.Tensor, theta_rows: int, f: int, lam: float, precision: int,
+                  a_out: torch.Tensor, b_out: torch.Tensor, row_begin: int = 0,
+                  row_end: Optional[int] = None) -> None:
+    """get_hermitian_mo_into (solver.hpp:292-304) on device buffers: A full mirrored f*f and
+    B f floats per row of [row_begin,row_end)."""
+    re = r.rows if row_end is None else row_end
+    _check(LIB.alsk_dev_hermitian(C.byref(r.c), theta.data_ptr(), theta_rows, f, lam, precision, row_begin,
+                                  re, a_out.data_ptr(), b_out.data_ptr(), stream_handle()))
 
 
 class AlsSession:

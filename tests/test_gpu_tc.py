@@ -1,0 +1,152 @@
+"""GPU parity of the tensor-core engine (ALSK_PREC_TF32X2, tc_update.cu) against the oracle.
+
+The oracle (pinned to the reference in test_oracle_pinning.py) runs the reference's
+default double-accumulation path; the tensor-core kernel must land within the north-star
+FP32 bar (factors within 1e-3 normwise after one half-sweep). The Hermitian itself is
+checked entry-wise against the double oracle. Row lengths straddle every pipeline
+boundary (8-rating k-groups, 32-rating stages, the 4-stage ring), rows outnumber the
+persistent CTAs so both epilogue groups and both TMEM buffers cycle, and empty rows,
+grid blocks (col_offset) and Cholesky breakdowns take their reference semantics."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+import torch
+
+from helpers import normwise_gap
+from oracle import binding
+
+pytestmark = pytest.mark.gpu
+FP32_TOL = 1e-3
+
+
+def ocsr(r):
+    return binding.csr_struct(r.rows, r.cols, r.row_ptr, r.col_idx, r.values, r.col_offset)
+
+
+def rows_with_lengths(A, lengths, n, seed):
+    """A CSR whose row u has exactly lengths[u] distinct sorted columns, values in [1,5]."""
+    rng = np.random.default_rng(seed)
+    ptr = np.zeros(len(lengths) + 1, np.int64)
+    ptr[1:] = np.cumsum(lengths)
+    cols = np.concatenate([np.sort(rng.choice(n, size=k, replace=False)) if k else np.zeros(0, np.int64)
+                           for k in lengths]).astype(np.int32)
+    vals = rng.uniform(1.0, 5.0, size=int(ptr[-1])).astype(np.float32)
+    return A.CsrMatrix(len(lengths), n, 0, ptr, cols, vals)
+
+
+def tc_update(A, r, th, f, lam):
+    with A.use_fp32_engine("tensor"):
+        return A.update_x(r, th, A.SolverConfig(f=f, lambda_=lam, accumulate_double=False))
+
+
+def test_engine_switch(A, gpu):
+    prev = A.fp32_engine()
+    with A.use_fp32_engine("ffma"):
+        assert A.fp32_engine() == "ffma"
+    assert A.fp32_engine() == prev
+
+
+@pytest.mark.parametrize("f", [16, 24, 32, 40, 55, 64, 80, 96, 100, 103, 119])
+def test_tc_update_x_ranks(A, orc, gpu, f):
+    m, n = 400, 260
+    r = A.synth_csr(m, n, 16000, 900 + f)
+    th = A.random_factor(n, f, 7 + f)
+    st, xo = orc.update_x(ocsr(r), th.entries, n, f, 0.05, acc_double=1)
+    assert st == 0
+    x = tc_update(A, r, th, f, 0.05)
+    gap = normwise_gap(x.entries, xo)
+    assert gap <= FP32_TOL, gap
+    # the split keeps FP32-level accuracy; far inside the bar
+    assert gap <= 5e-5, gap
+
+
+@pytest.mark.parametrize("f", [16, 33, 100])
+def test_tc_hermitian_entrywise(A, orc, gpu, f):
+    from paper_1603_03820_b200.session import PREC_TF32X2, DeviceCsr, dev_hermitian
+    m, n = 90, 500
+    lengths = [0, 1, 2, 3, 4, 5, 7, 8, 9, 15, 16, 17, 31, 32, 33, 40, 63, 64, 65, 96, 97, 128, 129, 200, 333] * 3
+    lengths = lengths[:m] + [37] * (m - len(lengths[:m]))
+    r = rows_with_lengths(A, lengths, n, 31 + f)
+    th = A.random_factor(n, f, 5)
+    st, ao, bo = orc.hermitian(ocsr(r), th.entries, n, f, 0.05, 1, 0, m)
+    assert st == 0
+    dev = torch.device("cuda")
+    R = DeviceCsr.from_host(r, dev)
+    T = torch.from_numpy(th.entries).to(dev)
+    a = torch.empty(m * f * f, dtype=torch.float32, device=dev)
+    b = torch.empty(m * f, dtype=torch.float32, device=dev)
+    dev_hermitian(R, T, n, f, 0.05, PREC_TF32X2, a, b)
+    a, b = a.cpu().numpy().reshape(m, f, f), b.cpu().numpy().reshape(m, f)
+    ao, bo = ao.reshape(m, f, f), bo.reshape(m, f)
+    assert np.array_equal(a, np.transpose(a, (0, 2, 1))), "A must be mirrored bit-exactly"
+    for u in range(m):
+        sa = max(np.abs(ao[u]).max(), 1e-30)
+        sb = max(np.abs(bo[u]).max(), 1e-30)
+        assert np.abs(a[u] - ao[u]).max() / sa <= 1e-5, (u, lengths[u])
+        assert np.abs(b[u] - bo[u]).max() / sb <= 1e-5, (u, lengths[u])
+
+
+def test_tc_row_lengths_and_empty_rows(A, orc, gpu):
+    f, n = 100, 3000
+    lengths = ([0, 1, 7, 8, 9, 31, 32, 33, 127, 128, 129, 130, 500, 2049] * 40)
+    r = rows_with_lengths(A, lengths, n, 77)
+    th = A.random_factor(n, f, 9)
+    st, xo = orc.update_x(ocsr(r), th.entries, n, f, 0.05, acc_double=1)
+    x = tc_update(A, r, th, f, 0.05)
+    assert normwise_gap(x.entries, xo) <= 5e-5
+    xs = x.entries.reshape(len(lengths), f)
+    assert not xs[np.asarray(lengths) == 0].any()
+
+
+def test_tc_netflix_shape_rows(A, orc, gpu):
+    """X-half and Theta-half slices of the Netflix shape at f=100, tensor-core engine."""
+    f = 100
+    for m, n, per in [(3000, 17770, 186), (150, 480189, 5575)]:
+        r = A.synth_csr(m, n, m * per, 2024 + m)
+        th = A.random_factor(n, f, 42)
+        st, xo = orc.update_x(ocsr(r), th.entries, n, f, 0.05, acc_double=1)
+        x = tc_update(A, r, th, f, 0.05)
+        gap = normwise_gap(x.entries, xo)
+        assert gap <= 5e-5, gap
+
+
+def test_tc_grid_block_col_offset(A, orc, gpu):
+    """A grid block (column-global indices, col_offset = first column of the block) against
+    its factor slice: the kernel gathers rows col - col_offset (sparse.hpp:34-37)."""
+    f = 48
+    r = A.synth_csr(500, 400, 20000, 55)
+    g = A.grid_partition(r, 2, 2)
+    blk = g.block(1, 1)  # rows of slab 1, columns [col_cuts[1], 400)
+    lo = int(blk.col_offset)
+    th_full = A.random_factor(400, f, 8)
+    th = A.FactorMatrix(400 - lo, f, th_full.entries[lo * f:].copy())
+    st, xo = orc.update_x(ocsr(blk), th.entries, th.rows, f, 0.05, acc_double=1)
+    assert st == 0
+    x = tc_update(A, blk, th, f, 0.05)
+    assert normwise_gap(x.entries, xo) <= 5e-5
+
+
+def test_tc_breakdown_message(A, gpu):
+    # identity factors (f=16); lambda=-0.05: row 0 (all 16 columns) has A = (1-0.8) I, SPD;
+    # rows 1 and 2 (one column each) turn indefinite -> the first failing row is index 1
+    f = 16
+    th = np.eye(f, dtype=np.float32)
+    rp = np.array([0, f, f + 1, f + 2], np.int64)
+    ci = np.concatenate([np.arange(f), [1], [2]]).astype(np.int32)
+    r = A.CsrMatrix(3, f, 0, rp, ci, np.ones(len(ci), np.float32))
+    with A.use_fp32_engine("tensor"):
+        with pytest.raises(A.NumericalError, match="cholesky breakdown at batch index 1"):
+            A.update_x(r, A.FactorMatrix(f, f, th.ravel()), A.SolverConfig(f=f, lambda_=-0.05, accumulate_double=False))
+
+
+def test_tc_engines_agree_on_many_rows(A, orc, gpu):
+    """More rows than 2 x 148 persistent CTAs: both engines within the bar of the oracle."""
+    f = 64
+    r = A.synth_csr(5000, 900, 5000 * 60, 4242)
+    th = A.random_factor(900, f, 3)
+    st, xo = orc.update_x(ocsr(r), th.entries, 900, f, 0.05, acc_double=1)
+    for eng in ("ffma", "tensor"):
+        with A.use_fp32_engine(eng):
+            x = A.update_x(r, th, A.SolverConfig(f=f, lambda_=0.05, accumulate_double=False))
+        assert normwise_gap(x.entries, xo) <= 1e-4, eng
