@@ -66,6 +66,18 @@ bool update_tc(const DevCsr& r, const float* theta, int64_t theta_rows, int f, f
 bool hermitian_tc(const DevCsr& r, const float* theta, int64_t theta_rows, int f, float lambda, int64_t rb,
                   int64_t re, float* A, float* B, cudaStream_t s);
 
+// Packed Hermitian rows: lower A (lambda n_u included) then b, f(f+1)/2 + f floats, row
+// stride rounded to 4 floats so every row is 16-byte aligned for bulk copies.
+__host__ __device__ inline int64_t packed_stride(int f) { return ((static_cast<int64_t>(f) * (f + 1) / 2 + f) + 3) & ~int64_t(3); }
+
+// Batched FP32 solves of packed rows (status rows reported at status_off + i):
+//  packed_solve       - tensor-core Cholesky, matrix resident in TMEM (tc_solve.cu);
+//  packed_solve_tiles - CUDA-core 8x8 register-tile Cholesky (chol_solve.cu).
+bool packed_solve(const float* packed, int64_t count, int f, float* x, const SolveStatus& st, int64_t status_off,
+                  cudaStream_t s);
+bool packed_solve_tiles(const float* packed, int64_t count, int f, float* x, const SolveStatus& st,
+                        int64_t status_off, cudaStream_t s);
+
 // Packed-lower double partial Hermitian (data-parallel split) and its solve.
 void partial_hermitian_packed(const DevCsr& r, const float* theta, int f, double lambda,
                               int64_t rb, int64_t re, double* out, cudaStream_t s);

@@ -33,8 +33,9 @@ __device__ __forceinline__ void fence_barrier_init() {
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
 }
-// Spin on the phase with the given parity. A deadlock traps after ~10 s of SM clock
-// instead of hanging the device.
+// Wait for the phase with the given parity (spinning try_wait: a suspend-time hint parks
+// the warp and the wake-up then costs microseconds, which short per-step waits cannot
+// afford). A deadlock traps after ~10 s of SM clock instead of hanging the device.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     uint32_t done = 0;
     uint32_t spins = 0;
@@ -45,7 +46,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
             : "=r"(done)
             : "r"(smem_u32(bar)), "r"(parity)
             : "memory");
-        if (!done && ((++spins & 1023u) == 0)) {
+        if (!done && ((++spins & 255u) == 0)) {
             const long long now = clock64();
             if (t0 == 0) t0 = now;
             else if (now - t0 > 20000000000ll) __trap();
@@ -137,6 +138,16 @@ __device__ __forceinline__ uint32_t sw128_offset(int k, int c16) {
 // K-major operand tile of 32 ratings: byte offset of (feature i, rating k).
 __device__ __forceinline__ uint32_t kmajor_offset(int i, int k) {
     return static_cast<uint32_t>((i >> 3) * 1024 + (i & 7) * 128 + ((((k >> 2) ^ (i & 7))) << 4) + (k & 3) * 4);
+}
+
+// 16-byte global -> shared copy through L2 only (LDGSTS).
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(src) : "memory");
+}
+// Arrive on `bar` once all cp.async issued so far by this thread have landed; the arrival
+// counts against the barrier's expected count.
+__device__ __forceinline__ void cp_async_arrive_noinc(uint64_t* bar) {
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(smem_u32(bar)) : "memory");
 }
 
 __device__ __forceinline__ float4 ldg_nc_f4(const float* p) {

@@ -20,22 +20,25 @@
 //                registers -> shared memory (segment sums, symmetrisation, lambda n_u) ->
 //                8x8 tiles in registers -> blocked right-looking Cholesky -> back
 //                substitution -> x_u.
-//   warps 8-11 : split warps: read the TMA-landed rating-major rows, split tf32 hi/lo and
+//   warps 8-11 : split warps: read the staged rating-major rows, split tf32 hi/lo and
 //                write them transposed into the K-major operand tile (lane = rating), with
 //                zero padding of partial k-groups.
 //   warp 12    : MMA issuer (one thread), owns the TMEM allocation (2 buffers x 256 columns).
-//   warp 13    : TMA issuer: cp.async.bulk.tensor tile::gather4, 4 factor rows x 32
-//                features per instruction, into a 128B-swizzled rating-major staging ring.
+//   warp 13    : loader: the only reader of the CSR arrays (4-chunk register prefetch queue);
+//                copies each gathered factor row with cp.async (one coalesced row per
+//                instruction) into a rating-major staging ring, completion counted per lane
+//                on the stage mbarrier (cp.async.mbarrier.arrive.noinc).
 // Pipelines: staging ring (raw_full / raw_empty, 4 deep), operand ring (hl_full / hl_empty,
 // 2 deep, released by tcgen05.commit) and the TMEM double buffer (tfull / tempty), one TMEM
 // job per row segment.
-#include <cuda.h>
 #include <cuda_runtime.h>
-#include <cudaTypedefs.h>
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdio>
+#include <cstdlib>
 #include <mutex>
+#include <vector>
 
 #include "kernels.cuh"
 #include "tc_common.cuh"
@@ -45,8 +48,6 @@ namespace {
 using namespace tc;
 
 constexpr int KC = 32;                   // ratings per stage (four k-groups of 8)
-constexpr int MNB = 4;                   // feature blocks of 32 (M = 128 rows)
-constexpr int RAW_BYTES = KC * MNB * 128;   // 16 KB: one staged chunk, rating-major
 constexpr int HL_BYTES = 256 * KC * 4;      // 32 KB: H rows [0,NF) then 2L rows [NF,2NF), K-major
 constexpr int HL_STAGES = 2;
 constexpr int SEG_CHUNKS = 16;              // TMEM accumulation segment: 16 x 32 ratings
@@ -54,19 +55,28 @@ constexpr int NTHREADS = 448;
 constexpr int TMEM_COLS = 512;           // two buffers x 256 columns (D0 @ +0, D1 @ +NF)
 
 // ---- shared-memory plan (host and device agree) ----
+// Staged factor rows keep the caller's row length rounded to 4 (mod 8) floats: with an odd
+// number of 16-byte chunks per row, a quarter-warp reading one chunk of 8 consecutive rows
+// touches 8 distinct bank groups.
+__host__ __device__ inline int staging_stride(int ldt) { return (ldt % 8 == 4) ? ldt : ldt + 4; }
+
 struct TcPlan {
-    int f, sld, stages, nb;
+    int f, sld, stages, nb, rs, raw_bytes;
     int s_floats, grp_floats;
-    size_t ring_bytes, grp_bytes, bar_off, total;
-    __host__ __device__ TcPlan(int f_, int nb_, int stages_) : f(f_), stages(stages_), nb(nb_) {
+    size_t hl_off, ring_bytes, grp_bytes, bar_off, info_off, total;
+    __host__ __device__ TcPlan(int f_, int nb_, int stages_, int ldt) : f(f_), stages(stages_), nb(nb_) {
+        rs = staging_stride(ldt);
+        raw_bytes = (KC * rs * 4 + 127) & ~127;
         sld = (f + 1) | 1;  // >= f+1 columns (A and B); odd: row writes and column reads conflict-free
         s_floats = ((f + 1) * sld + 3) & ~3;  // keep the float4 panel 16-byte aligned
         const int fp = 8 * nb;
         grp_floats = (s_floats + 8 * fp + 64 + fp + 8 + 3) & ~3;
-        ring_bytes = static_cast<size_t>(stages) * RAW_BYTES + static_cast<size_t>(HL_STAGES) * HL_BYTES;
+        hl_off = (static_cast<size_t>(stages) * raw_bytes + 1023) & ~static_cast<size_t>(1023);  // UMMA atoms: 1 KB
+        ring_bytes = hl_off + static_cast<size_t>(HL_STAGES) * HL_BYTES;
         grp_bytes = static_cast<size_t>(grp_floats) * 4;
         bar_off = (ring_bytes + 2 * grp_bytes + 15) & ~static_cast<size_t>(15);
-        total = bar_off + static_cast<size_t>(2 * stages + 2 * HL_STAGES + 6) * 8 + 16 + 1024;  // + align slack
+        info_off = bar_off + static_cast<size_t>(2 * stages + 2 * HL_STAGES + 6) * 8 + 16;
+        total = info_off + static_cast<size_t>(stages) * (KC * 4 + 16) + HL_STAGES * 16 + 1024;  // + align slack
     }
 };
 
@@ -98,23 +108,66 @@ __device__ __forceinline__ void outer_accumulate(float (&acc)[8][8], const float
     }
 }
 
-__device__ __forceinline__ void tma_gather4(const CUtensorMap* map, uint32_t dst, uint64_t* bar, int col, int r0,
-                                            int r1, int r2, int r3) {
-    asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
-        " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];\n" ::"r"(dst),
-        "l"(reinterpret_cast<uint64_t>(map)), "r"(col), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(smem_u32(bar))
-        : "memory");
-}
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
                  : "memory");
 }
 
-__device__ __forceinline__ int chunk_count(int64_t n, int64_t c0) {
-    const int64_t left = n - c0;
-    return left < KC ? static_cast<int>(left) : KC;
-}
+// Metadata the TMA warp forwards with every staged chunk (and the split warps with every
+// operand stage): rating count (-1 = end of work) and segment flags for the MMA issuer.
+struct ChunkInfo {
+    int cnt;
+    uint32_t flags;  // bit0: first chunk of a TMEM segment, bit1: last, bit2: owner group
+    int pad0, pad1;
+};
+constexpr uint32_t CH_FIRST = 1u, CH_LAST = 2u, CH_OWNER1 = 4u;
+
+// Walks the CTA's chunk sequence (rows j = blockIdx.x + t*gridDim.x, 32 ratings per chunk,
+// empty rows skipped) one step ahead of its consumer; the next row's extent is prefetched
+// so row changes do not expose a dependent load.
+struct ChunkWalker {
+    const int64_t* row_ptr;
+    int64_t rb, nrows, j, k0, n, c0, nj, nk0, nn;
+    int t, nt;
+    __device__ void load_next(int64_t from, int tfrom) {
+        nj = from;
+        nt = tfrom;
+        nk0 = nn = 0;
+        while (nj < nrows) {
+            nk0 = row_ptr[rb + nj];
+            nn = row_ptr[rb + nj + 1] - nk0;
+            if (nn > 0) break;
+            nj += gridDim.x;
+            ++nt;
+        }
+    }
+    __device__ ChunkWalker(const int64_t* rp, int64_t rb_, int64_t nrows_) : row_ptr(rp), rb(rb_), nrows(nrows_) {
+        load_next(blockIdx.x, 0);
+        j = nj, k0 = nk0, n = nn, t = nt, c0 = 0;
+        load_next(j + gridDim.x, t + 1);
+    }
+    __device__ bool valid() const { return j < nrows; }
+    __device__ ChunkInfo info() const {
+        ChunkInfo ci{};
+        if (!valid()) {
+            ci.cnt = -1;
+            return ci;
+        }
+        const int64_t left = n - c0;
+        ci.cnt = left < KC ? static_cast<int>(left) : KC;
+        const int64_t ch = c0 / KC;
+        ci.flags = ((ch % SEG_CHUNKS) == 0 ? CH_FIRST : 0u) |
+                   ((c0 + KC >= n || (ch % SEG_CHUNKS) == SEG_CHUNKS - 1) ? CH_LAST : 0u) | ((t & 1) ? CH_OWNER1 : 0u);
+        return ci;
+    }
+    __device__ void advance() {
+        c0 += KC;
+        if (c0 >= n) {
+            j = nj, k0 = nk0, n = nn, t = nt, c0 = 0;
+            if (j < nrows) load_next(j + gridDim.x, t + 1);
+        }
+    }
+};
 
 struct RowIter {  // the CTA's row sequence j = blockIdx.x + t * gridDim.x
     int64_t j, nrows;
@@ -126,13 +179,22 @@ struct RowIter {  // the CTA's row sequence j = blockIdx.x + t * gridDim.x
 // One epilogue group's Cholesky of the augmented tile set (rows < f: A lower; row f: B) and
 // the back substitution; x written to xrow. Mirrors fused_fp32.cu's blocked algorithm with
 // group-scoped named barriers. Returns the breakdown column+1 (0 = ok).
-template <int NB>
+template <int NB, int GT = 128>
 __device__ __forceinline__ void group_solve(float (&acc)[8][8], bool active, int bi, int bj, int e, int f,
                                             float* lpk, float* panel, float* dblk, float* dinv, int* flags,
                                             uint32_t bar_id, float* __restrict__ xrow, int32_t* col_out,
-                                            double* piv_out, unsigned long long* min_row, int64_t status_row) {
+                                            double* piv_out, unsigned long long* min_row, int64_t status_row,
+                                            bool prof, long long (&pc)[6]) {
     constexpr int FP = 8 * NB;
     const int ia = 8 * bi, jb = 8 * bj;
+    long long tq = prof ? clock64() : 0;
+    auto lap = [&](int slot) {
+        if (prof) {
+            const long long now = clock64();
+            pc[slot] += now - tq;
+            tq = now;
+        }
+    };
     const int aug = f;
     // all-zero A => x = 0 (solver.hpp:215-220)
     int nz = 0;
@@ -144,13 +206,13 @@ __device__ __forceinline__ void group_solve(float (&acc)[8][8], bool active, int
                 if (ia + ii < f && jb + jj <= ia + ii) nz |= (acc[ii][jj] != 0.f);
     }
     if (e == 0) flags[2] = 0;
-    named_barrier(bar_id, 128);
+    named_barrier(bar_id, GT);
     if (nz) flags[2] = 1;
-    named_barrier(bar_id, 128);
+    named_barrier(bar_id, GT);
     if (!flags[2]) {
-        for (int i = e; i < f; i += 128) xrow[i] = 0.f;
+        for (int i = e; i < f; i += GT) xrow[i] = 0.f;
         if (e == 0) *col_out = 0;
-        named_barrier(bar_id, 128);
+        named_barrier(bar_id, GT);
         return;
     }
     const int nbc = (f + 7) >> 3;
@@ -182,17 +244,18 @@ __device__ __forceinline__ void group_solve(float (&acc)[8][8], bool active, int
 #pragma unroll
                 for (int c = 0; c < 8; ++c) dblk[r * 8 + c] = acc[r][c];
         }
-        named_barrier(bar_id, 128);
+        named_barrier(bar_id, GT);
+        lap(0);
         if (flags[0]) {
             if (e == 0) {
                 *col_out = flags[0];
                 *piv_out = static_cast<double>(__int_as_float(flags[1]));
                 atomicMin(min_row, static_cast<unsigned long long>(status_row));
             }
-            for (int i = e; i < f; i += 128) xrow[i] = 0.f;
-            named_barrier(bar_id, 128);
+            for (int i = e; i < f; i += GT) xrow[i] = 0.f;
+            named_barrier(bar_id, GT);
             if (e == 0) flags[0] = 0;
-            named_barrier(bar_id, 128);
+            named_barrier(bar_id, GT);
             return;
         }
         if (active && bj == bc && bi > bc) {
@@ -214,8 +277,10 @@ __device__ __forceinline__ void group_solve(float (&acc)[8][8], bool active, int
                 dst[1] = make_float4(acc[4][c], acc[5][c], acc[6][c], acc[7][c]);
             }
         }
-        named_barrier(bar_id, 128);
+        named_barrier(bar_id, GT);
+        lap(1);
         if (active && bj > bc) outer_accumulate<FP, true>(acc, panel, 8, ia, jb);
+        lap(2);
     }
     if (e == 0) *col_out = 0;
     // packed L (rows < f) and y (row aug) for the back substitution
@@ -231,7 +296,7 @@ __device__ __forceinline__ void group_solve(float (&acc)[8][8], bool active, int
                 else if (i == aug) yrow[j] = acc[ii][jj];
             }
     }
-    named_barrier(bar_id, 128);
+    named_barrier(bar_id, GT);
     if (e < 32) {
         const int lane = e;
         constexpr int G = (FP + 31) / 32;
@@ -262,7 +327,8 @@ __device__ __forceinline__ void group_solve(float (&acc)[8][8], bool active, int
             if (j < f) xrow[j] = yv[g];
         }
     }
-    named_barrier(bar_id, 128);  // lpk / dinv reused by the group's next row
+    named_barrier(bar_id, GT);  // lpk / dinv reused by the group's next row
+    lap(3);
 }
 
 __device__ __forceinline__ int64_t row_segments(int64_t n) {
@@ -270,25 +336,38 @@ __device__ __forceinline__ int64_t row_segments(int64_t n) {
     return (nch + SEG_CHUNKS - 1) / SEG_CHUNKS;
 }
 
-template <int NB, bool SOLVE>
+// MODE_SOLVE: fused Cholesky + solves -> x rows. MODE_FULL: A (full, mirrored) + B rows
+// (get_hermitian layout). MODE_PACKED: lower-packed A then B, f(f+1)/2+f floats per row, for
+// the separate batched solve.
+enum { MODE_SOLVE = 0, MODE_FULL = 1, MODE_PACKED = 2 };
+
+template <int NB, int MODE>
 __global__ void __launch_bounds__(NTHREADS, 1)
-tc_update_kernel(const __grid_constant__ CUtensorMap tmap, const int64_t* __restrict__ row_ptr,
+tc_update_kernel(const float* __restrict__ theta, int ldt, const int64_t* __restrict__ row_ptr,
                  const int32_t* __restrict__ col_idx, const float* __restrict__ values, int64_t col_lo, int f,
                  float lambda, int64_t rb, int64_t nrows, int stages, float* __restrict__ out_x,
                  float* __restrict__ out_a, float* __restrict__ out_b, unsigned long long* __restrict__ min_row,
-                 int32_t* __restrict__ column, double* __restrict__ pivot, int64_t status_base) {
+                 int32_t* __restrict__ column, double* __restrict__ pivot, int64_t status_base,
+                 long long* __restrict__ prof) {
     constexpr int FP = 8 * NB;
     constexpr int NTILES = NB * (NB + 1) / 2;
     static_assert(NTILES <= 128, "tile set must fit one 128-thread epilogue group");
+    // optional per-warp cycle accounting (ALSK_TC_PROF=1): pc[] slots per role, see launch_tc
+    long long pc[6] = {0, 0, 0, 0, 0, 0};
+    long long tp0 = 0;
+#define TP(v) long long v = prof ? clock64() : 0
+#define TA(v, slot) \
+    if (prof) pc[slot] += clock64() - v
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw_addr = smem_u32(smem_raw);
     uint8_t* base = smem_raw + (((raw_addr + 1023u) & ~1023u) - raw_addr);
-    const TcPlan P(f, NB, stages);
+    const TcPlan P(f, NB, stages, ldt);
+    const int RAW = P.raw_bytes;
     // augmented features per operand half; a multiple of 16 keeps every 16-column TMEM load of
     // the second half aligned
     const int NF = (f + 1 + 15) & ~15;
-    uint8_t* ring = base;                                          // stages x RAW_BYTES
-    uint8_t* hl = base + static_cast<size_t>(stages) * RAW_BYTES;  // HL_STAGES x HL_BYTES
+    uint8_t* ring = base;                                    // stages x RAW: rating-major staging
+    uint8_t* hl = base + P.hl_off;                           // HL_STAGES x HL_BYTES, 1 KB aligned
     float* grp0 = reinterpret_cast<float*>(base + P.ring_bytes);
     uint64_t* bars = reinterpret_cast<uint64_t*>(base + P.bar_off);
     uint64_t* raw_full = bars;
@@ -301,11 +380,14 @@ tc_update_kernel(const __grid_constant__ CUtensorMap tmap, const int64_t* __rest
     uint64_t* tfull = hl_empty + HL_STAGES;
     uint64_t* tempty = tfull + 4;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+    ChunkInfo* raw_info = reinterpret_cast<ChunkInfo*>(base + P.info_off);  // [stages]
+    float* raw_vals = reinterpret_cast<float*>(raw_info + stages);          // [stages][KC]
+    ChunkInfo* hl_info = reinterpret_cast<ChunkInfo*>(raw_vals + stages * KC);  // [HL_STAGES]
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
         for (int s = 0; s < stages; ++s) {
-            mbar_init(&raw_full[s], 1);
+            mbar_init(&raw_full[s], 33);  // 32 cp.async arrivals + the publishing lane
             mbar_init(&raw_empty[s], 4);
         }
         for (int s = 0; s < HL_STAGES; ++s) {
@@ -324,37 +406,82 @@ tc_update_kernel(const __grid_constant__ CUtensorMap tmap, const int64_t* __rest
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    if (prof) tp0 = clock64();
 
     if (warp == 13) {
-        // ---------------- TMA issuer ----------------
-        const int nblk = (f + 31) >> 5;  // feature blocks of 32 holding real features
-        uint32_t ctr = 0;
-        for (RowIter it(nrows); it.more(); it.next()) {
-            const int64_t u = rb + it.j;
-            const int64_t k0 = row_ptr[u], n = row_ptr[u + 1] - k0;
-            for (int64_t c0 = 0; c0 < n; c0 += KC, ++ctr) {
+        // ---------------- loader (sole reader of the CSR arrays) ----------------
+        // A 4-deep register queue holds the column indices and ratings of upcoming chunks, so
+        // their global loads are in flight long before the chunk is staged. Each factor row
+        // is copied by cp.async (LDGSTS, 16 bytes per lane, one coalesced row per
+        // instruction) and completion is counted on the stage's mbarrier per lane.
+        constexpr int D = 4;
+        const int n16 = ldt >> 2;  // 16-byte pieces per factor row
+        const int rs4 = P.rs * 4;
+        ChunkWalker w(row_ptr, rb, nrows);
+        ChunkInfo qi[D];
+        int qc[D];
+        float qv[D];
+#pragma unroll
+        for (int d = 0; d < D; ++d) {
+            qi[d] = w.info();
+            qc[d] = 0;
+            qv[d] = 0.f;
+            if (qi[d].cnt > 0 && lane < qi[d].cnt) {
+                qc[d] = col_idx[w.k0 + w.c0 + lane];
+                qv[d] = values[w.k0 + w.c0 + lane];
+            }
+            if (w.valid()) w.advance();
+        }
+        // Slot d of the queue is consumed and refilled in place (static register names): a
+        // register holding an in-flight load is next read D chunks later, so the loads never
+        // stall the loop.
+        bool done = false;
+        for (uint32_t ctr0 = 0; !done; ctr0 += D) {
+#pragma unroll
+            for (int d = 0; d < D; ++d) {
+                if (done) break;
+                const uint32_t ctr = ctr0 + d;
+                const ChunkInfo ci = qi[d];
+                const int v = qc[d] - static_cast<int>(col_lo);
+                const float rv = qv[d];
+                qi[d] = w.info();
+                qc[d] = 0;
+                qv[d] = 0.f;
+                if (qi[d].cnt > 0 && lane < qi[d].cnt) {
+                    qc[d] = col_idx[w.k0 + w.c0 + lane];
+                    qv[d] = values[w.k0 + w.c0 + lane];
+                }
+                if (w.valid()) w.advance();
+
                 const int s = ctr % stages;
                 const uint32_t ph = (ctr / stages) & 1u;
-                const int cnt = chunk_count(n, c0);
-                int v = 0;
-                if (lane < cnt) v = col_idx[k0 + c0 + lane] - static_cast<int>(col_lo);
-                const int v_first = __shfl_sync(0xffffffffu, v, lane & ~3);
-                if (lane >= cnt) v = v_first;  // pad a partial quad with a valid row
-                const int q0 = __shfl_sync(0xffffffffu, v, (lane & 7) * 4 + 0);
-                const int q1 = __shfl_sync(0xffffffffu, v, (lane & 7) * 4 + 1);
-                const int q2 = __shfl_sync(0xffffffffu, v, (lane & 7) * 4 + 2);
-                const int q3 = __shfl_sync(0xffffffffu, v, (lane & 7) * 4 + 3);
-                const int nquads = (cnt + 3) >> 2;
-                if (lane == 0) {
-                    mbar_wait(&raw_empty[s], ph ^ 1u);
-                    mbar_expect_tx(&raw_full[s], static_cast<uint32_t>(nquads * nblk * 512));
+                {
+                    TP(t0);
+                    if (lane == 0) mbar_wait(&raw_empty[s], ph ^ 1u);
+                    __syncwarp();
+                    TA(t0, 0);
                 }
-                __syncwarp();
-                if (lane < nquads) {
-                    const uint32_t dst = smem_u32(ring + s * RAW_BYTES) + (lane >> 1) * (MNB * 1024) + (lane & 1) * 512;
-                    for (int b = 0; b < nblk; ++b) tma_gather4(&tmap, dst + b * 1024, &raw_full[s], b * 32, q0, q1, q2, q3);
+                uint8_t* stage = ring + s * RAW;
+                raw_vals[s * KC + lane] = rv;
+                if (lane == 0) raw_info[s] = ci;
+                if (ci.cnt > 0) {
+                    // lane = rating slot: each lane streams its own factor row, 16 bytes per
+                    // instruction; padding slots of the last k-group get zeros
+                    const int kend = (ci.cnt + 7) & ~7;
+                    uint8_t* my = stage + lane * rs4;
+                    if (lane < ci.cnt) {
+                        const float* src = theta + static_cast<int64_t>(v) * ldt;
+                        const uint32_t dst = smem_u32(my);
+                        for (int c = 0; c < n16; ++c) cp_async16(dst + c * 16, src + 4 * c);
+                    } else if (lane < kend) {
+                        for (int c = 0; c < n16; ++c)
+                            *reinterpret_cast<float4*>(my + c * 16) = make_float4(0.f, 0.f, 0.f, 0.f);
+                    }
                 }
+                cp_async_arrive_noinc(&raw_full[s]);
                 __syncwarp();
+                if (lane == 0) mbar_arrive(&raw_full[s]);
+                if (ci.cnt < 0) done = true;
             }
         }
     } else if (warp >= 8 && warp < 12) {
@@ -363,9 +490,7 @@ tc_update_kernel(const __grid_constant__ CUtensorMap tmap, const int64_t* __rest
         // Every offset below is a per-thread constant plus a multiple of t.
         const int pw = warp - 8;
         const int k = lane;
-        const uint32_t raw_k = static_cast<uint32_t>((k >> 3) * (MNB * 1024) + (k & 7) * 128);
-        const uint32_t raw_sw0 = static_cast<uint32_t>(((pw ^ (k & 7))) << 4);
-        const uint32_t raw_sw1 = static_cast<uint32_t>((((pw + 4) ^ (k & 7))) << 4);
+        const uint32_t raw_k = static_cast<uint32_t>(k * P.rs * 4 + pw * 16);
         uint32_t kq[4];
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
@@ -373,87 +498,101 @@ tc_update_kernel(const __grid_constant__ CUtensorMap tmap, const int64_t* __rest
             kq[q] = static_cast<uint32_t>((pw >> 1) * 1024 + r8 * 128 + ((((k >> 2) ^ r8)) << 4) + (k & 3) * 4);
         }
         const uint32_t l_off = static_cast<uint32_t>(NF * 128);
-        uint32_t ctr = 0;
-        for (RowIter it(nrows); it.more(); it.next()) {
-            const int64_t u = rb + it.j;
-            const int64_t k0 = row_ptr[u], n = row_ptr[u + 1] - k0;
-            for (int64_t c0 = 0; c0 < n; c0 += KC, ++ctr) {
-                const int s = ctr % stages;
-                const int hs = ctr % HL_STAGES;
-                const int cnt = chunk_count(n, c0);
-                const bool valid = k < cnt;
-                const float r = valid ? values[k0 + c0 + k] : 0.f;
-                const float r_hi = tf32_rna(r), r_lo2 = 2.f * tf32_rna(r - r_hi);
-                mbar_wait(&raw_full[s], (ctr / stages) & 1u);
-                mbar_wait(&hl_empty[hs], ((ctr / HL_STAGES) & 1u) ^ 1u);
-                const uint8_t* raw = ring + s * RAW_BYTES + raw_k;
+        // the rating slot (feature f) lives in chunk f>>2: warp (f>>2)&3, step f>>4, element f&3
+        const bool owns_r = pw == ((f >> 2) & 3);
+        const int r8f = 4 * (pw & 1) + (f & 3);
+        const uint32_t r_off = static_cast<uint32_t>((pw >> 1) * 1024 + r8f * 128 + ((((k >> 2) ^ r8f)) << 4) +
+                                                     (k & 3) * 4 + (f >> 4) * 2048);
+        constexpr int NC16 = 2 * NB;              // 16-byte feature chunks below 8*NB
+        constexpr int TPW = (NC16 + 3) / 4;       // chunks per split warp (upper bound)
+        const int nc16 = NC16 < (NF >> 2) ? NC16 : (NF >> 2);  // never spill H rows into the L half
+        for (uint32_t ctr = 0;; ++ctr) {
+            const int s = ctr % stages;
+            const int hs = ctr % HL_STAGES;
+            TP(t0);
+            mbar_wait(&raw_full[s], (ctr / stages) & 1u);
+            TA(t0, 0);
+            const ChunkInfo ci = raw_info[s];
+            TP(t1);
+            mbar_wait(&hl_empty[hs], ((ctr / HL_STAGES) & 1u) ^ 1u);
+            TA(t1, 1);
+            TP(t2);
+            if (ci.cnt >= 0) {
+                // Padding slots of the k-group were zeroed by the loader, so the split is
+                // branch-free: h = rna_tf32(x), 2l = 2 rna_tf32(x - h) by bit ops.
+                const uint8_t* raw = ring + s * RAW + raw_k;
                 uint8_t* H = hl + hs * HL_BYTES;
 #pragma unroll
-                for (int t = 0; t < 8; ++t) {
-                    const int c16 = pw + 4 * t;
-                    if (4 * c16 > f) break;  // uniform per warp
-                    const float4 x = *reinterpret_cast<const float4*>(raw + (t >> 1) * 1024 + ((t & 1) ? raw_sw1 : raw_sw0));
-                    const float xv[4] = {x.x, x.y, x.z, x.w};
+                for (int t = 0; t < TPW; ++t) {
+                    if (pw + 4 * t < nc16) {  // uniform per warp
+                        const float4 x = *reinterpret_cast<const float4*>(__builtin_assume_aligned(raw + t * 64, 16));
+                        const float xv[4] = {x.x, x.y, x.z, x.w};
 #pragma unroll
-                    for (int q = 0; q < 4; ++q) {
-                        const int feat = 4 * c16 + q;
-                        float h, l2;
-                        if (feat < f) {
-                            h = tf32_rna(xv[q]);
-                            l2 = 2.f * tf32_rna(xv[q] - h);
-                        } else {
-                            h = feat == f ? r_hi : 0.f;
-                            l2 = feat == f ? r_lo2 : 0.f;
+                        for (int q = 0; q < 4; ++q) {
+                            const float h = __uint_as_float((__float_as_uint(xv[q]) + 0x1000u) & 0xFFFFE000u);
+                            const float l = xv[q] - h;
+                            const float l2 = 2.f * __uint_as_float((__float_as_uint(l) + 0x1000u) & 0xFFFFE000u);
+                            uint8_t* dst = H + kq[q] + t * 2048;
+                            *reinterpret_cast<float*>(dst) = h;
+                            *reinterpret_cast<float*>(dst + l_off) = l2;
                         }
-                        uint8_t* dst = H + kq[q] + t * 2048;
-                        *reinterpret_cast<float*>(dst) = valid ? h : 0.f;
-                        *reinterpret_cast<float*>(dst + l_off) = valid ? l2 : 0.f;
                     }
                 }
-                fence_proxy_async_smem();
-                __syncwarp();
-                if (lane == 0) {
-                    mbar_arrive(&raw_empty[s]);
-                    mbar_arrive(&hl_full[hs]);
+                if (owns_r) {  // overwrite feature f (zero column) with the rating
+                    const float r = raw_vals[s * KC + k];
+                    const float r_hi = tf32_rna(r), r_lo2 = 2.f * tf32_rna(r - r_hi);
+                    *reinterpret_cast<float*>(H + r_off) = r_hi;
+                    *reinterpret_cast<float*>(H + r_off + l_off) = r_lo2;
                 }
+                TA(t2, 2);
+                TP(t3);
+                fence_proxy_async_smem();
+                TA(t3, 3);
             }
+            if (pw == 0 && lane == 0) hl_info[hs] = ci;
+            __syncwarp();
+            if (lane == 0) {
+                mbar_arrive(&raw_empty[s]);
+                mbar_arrive(&hl_full[hs]);
+            }
+            if (ci.cnt < 0) break;
         }
     } else if (warp == 12) {
         // ---------------- MMA issuer ----------------
         const uint32_t idesc = idesc_tf32(128, 2 * NF);
-        uint32_t ctr = 0, job = 0;
-        int t = 0;
-        for (RowIter it(nrows); it.more(); it.next(), ++t) {
-            const int64_t u = rb + it.j;
-            const int64_t n = row_ptr[u + 1] - row_ptr[u];
-            const int owner = t & 1;
-            int64_t c0 = 0;
-            while (c0 < n) {  // one TMEM job per segment of SEG_CHUNKS chunks
-                const uint32_t b = job & 1u;
-                const uint32_t dcol = tmem + b * 256u;
-                if (lane == 0) mbar_wait(&tempty[b], ((job >> 1) & 1u) ^ 1u);
-                __syncwarp();
-                tc_fence_after();
-                for (int sc = 0; sc < SEG_CHUNKS && c0 < n; ++sc, c0 += KC, ++ctr) {
-                    const int hs = ctr % HL_STAGES;
-                    const int cnt = chunk_count(n, c0);
-                    if (lane == 0) {
-                        mbar_wait(&hl_full[hs], (ctr / HL_STAGES) & 1u);
-                        tc_fence_after();
-                        const uint32_t hb = smem_u32(hl + hs * HL_BYTES);
-                        const int ksteps = (cnt + 7) >> 3;
-                        for (int kb = 0; kb < ksteps; ++kb) {
-                            const uint64_t d = sdesc_sw128(hb + kb * 32, 16, 1024);
-                            mma_tf32(dcol, d, d, idesc, (sc > 0 || kb > 0) ? 1u : 0u);
-                        }
-                        mma_commit(&hl_empty[hs]);
-                    }
-                    __syncwarp();
+        uint32_t job = 0;
+        for (uint32_t ctr = 0;; ++ctr) {
+            const int hs = ctr % HL_STAGES;
+            ChunkInfo ci;
+            {
+                TP(t0);
+                if (lane == 0) {
+                    mbar_wait(&hl_full[hs], (ctr / HL_STAGES) & 1u);
+                    ci = hl_info[hs];
                 }
-                if (lane == 0) mma_commit(&tfull[2 * owner + b]);
-                __syncwarp();
-                ++job;
+                TA(t0, 0);
             }
+            ci.cnt = __shfl_sync(0xffffffffu, ci.cnt, 0);
+            ci.flags = __shfl_sync(0xffffffffu, ci.flags, 0);
+            if (ci.cnt < 0) break;
+            const uint32_t b = job & 1u;
+            const uint32_t dcol = tmem + b * 256u;
+            if (lane == 0) {
+                TP(t1);
+                if (ci.flags & CH_FIRST) mbar_wait(&tempty[b], ((job >> 1) & 1u) ^ 1u);
+                TA(t1, 1);
+                tc_fence_after();
+                const uint32_t hb = smem_u32(hl + hs * HL_BYTES);
+                const int ksteps = (ci.cnt + 7) >> 3;
+                for (int kb = 0; kb < ksteps; ++kb) {
+                    const uint64_t d = sdesc_sw128(hb + kb * 32, 16, 1024);
+                    mma_tf32(dcol, d, d, idesc, (!(ci.flags & CH_FIRST) || kb > 0) ? 1u : 0u);
+                }
+                mma_commit(&hl_empty[hs]);
+                if (ci.flags & CH_LAST) mma_commit(&tfull[2 * ((ci.flags & CH_OWNER1) ? 1 : 0) + b]);
+            }
+            __syncwarp();
+            if (ci.flags & CH_LAST) ++job;
         }
     } else {
         // ---------------- epilogue groups ----------------
@@ -494,9 +633,12 @@ tc_update_kernel(const __grid_constant__ CUtensorMap tmap, const int64_t* __rest
                 for (uint32_t sg = 0; sg < nseg; ++sg, ++job) {
                     const uint32_t b = job & 1u;
                     const uint32_t dcol = tmem + b * 256u + lane_base;
+                    TP(t0);
                     mbar_wait(&tfull[2 * g + b], use[b] & 1u);
+                    TA(t0, 4);
                     ++use[b];
                     tc_fence_after();
+                    TP(t1);
                     for (int c = 0; c < nch16; ++c) {
                         float d0[16], d1[16];
                         tmem_ld16(dcol + c * 16, d0);
@@ -513,7 +655,9 @@ tc_update_kernel(const __grid_constant__ CUtensorMap tmap, const int64_t* __rest
                     tc_fence_before();
                     __syncwarp();
                     if ((e & 31) == 0) mbar_arrive(&tempty[b]);
+                    TA(t1, 4);
                 }
+                TP(t2);
                 named_barrier(bar_id, 128);
                 // symmetrise in place: lower A (+ lambda n_u on the diagonal, float arithmetic as
                 // solver.hpp:141,152) and B in row f
@@ -524,7 +668,7 @@ tc_update_kernel(const __grid_constant__ CUtensorMap tmap, const int64_t* __rest
                     for (int j = 0; j < f; ++j) Srow[j] = 0.5f * (Srow[j] + S[j * sld + f]);
                 }
                 named_barrier(bar_id, 128);
-                if constexpr (!SOLVE) {
+                if constexpr (MODE == MODE_FULL) {
                     float* a_out = out_a + row * static_cast<int64_t>(f) * f;
                     float* b_out = out_b + row * static_cast<int64_t>(f);
                     for (int idx = e; idx < f * f; idx += 128) {
@@ -532,6 +676,17 @@ tc_update_kernel(const __grid_constant__ CUtensorMap tmap, const int64_t* __rest
                         a_out[idx] = j <= i ? S[i * sld + j] : S[j * sld + i];
                     }
                     for (int j = e; j < f; j += 128) b_out[j] = S[f * sld + j];
+                    named_barrier(bar_id, 128);
+                    continue;
+                } else if constexpr (MODE == MODE_PACKED) {
+                    // warp-cooperative rows: row i (lower part, then B as row f) is contiguous
+                    float* pk = out_a + row * packed_stride(f);
+                    const int wq = e >> 5, ln = e & 31;
+                    for (int i = wq; i <= f; i += 4) {
+                        const int len = i < f ? i + 1 : f;
+                        float* dst = pk + i * (i + 1) / 2;  // row f starts at f(f+1)/2
+                        for (int j = ln; j < len; j += 32) dst[j] = S[i * sld + j];
+                    }
                     named_barrier(bar_id, 128);
                     continue;
                 }
@@ -543,18 +698,30 @@ tc_update_kernel(const __grid_constant__ CUtensorMap tmap, const int64_t* __rest
                         if (active && j < f && (j <= i || i == f) && i <= f) acc[ii][jj] = S[i * sld + j];
                     }
                 named_barrier(bar_id, 128);  // S becomes the packed-L scratch
+                TA(t2, 4);
             }
-            if constexpr (!SOLVE) {
+            if constexpr (MODE == MODE_FULL) {
                 float* a_out = out_a + row * static_cast<int64_t>(f) * f;
                 for (int idx = e; idx < f * f; idx += 128) a_out[idx] = 0.f;
                 for (int j = e; j < f; j += 128) out_b[row * static_cast<int64_t>(f) + j] = 0.f;
+            } else if constexpr (MODE == MODE_PACKED) {
+                const int pkn = static_cast<int>(packed_stride(f));
+                float* pk = out_a + row * static_cast<int64_t>(pkn);
+                for (int idx = e; idx < pkn; idx += 128) pk[idx] = 0.f;
             } else {
                 group_solve<NB>(acc, active, bi, bj, e, f, S, panel, dblk, dinv, flags, bar_id,
                                 out_x + row * static_cast<int64_t>(f), column + row, pivot + row, min_row,
-                                status_base + row);
+                                status_base + row, prof != nullptr, pc);
             }
         }
     }
+    if (prof) {
+        pc[5] = clock64() - tp0;
+        if (lane == 0)
+            for (int i = 0; i < 6; ++i) prof[(static_cast<int64_t>(blockIdx.x) * 14 + warp) * 6 + i] = pc[i];
+    }
+#undef TP
+#undef TA
     tc_fence_before();
     __syncthreads();
     if (warp == 12) {
@@ -564,50 +731,44 @@ tc_update_kernel(const __grid_constant__ CUtensorMap tmap, const int64_t* __rest
 }
 
 // ---- host side ----
-PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
-    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-    static std::once_flag once;
-    std::call_once(once, [] {
-        void* p = nullptr;
-        cudaDriverEntryPointQueryResult q;
-        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
-            q == cudaDriverEntryPointSuccess)
-            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
-    });
-    if (!fn) throw Failure(ALSK_ERR_CUDA, "cuTensorMapEncodeTiled is unavailable");
-    return fn;
-}
-
-// 2-D map over the factor rows: dim0 = ldt features (contiguous), dim1 = rows; box 32 x 1
-// (gather4 fetches 4 rows of the box), 128-byte swizzle, out-of-bounds reads as zero.
-CUtensorMap factor_map(const float* theta, int64_t rows, int ldt) {
-    CUtensorMap m;
-    const cuuint64_t dims[2] = {static_cast<cuuint64_t>(ldt), static_cast<cuuint64_t>(std::max<int64_t>(rows, 1))};
-    const cuuint64_t strides[1] = {static_cast<cuuint64_t>(ldt) * 4};
-    const cuuint32_t box[2] = {32, 1};
-    const cuuint32_t estr[2] = {1, 1};
-    const CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(theta), dims, strides, box,
-                                   estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r != CUDA_SUCCESS) throw Failure(ALSK_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string(r) + ")");
-    return m;
-}
-
-template <int NB, bool SOLVE>
+template <int NB, int MODE>
 void launch_tc(const DevCsr& r, const float* theta, int64_t theta_rows, int f, int ldt, float lambda, int64_t rb,
                int64_t re, float* x, float* a, float* b, const SolveStatus* st, cudaStream_t s) {
-    int stages = 4;
-    while (stages > 2 && TcPlan(f, NB, stages).total > 227 * 1024) --stages;
-    const TcPlan P(f, NB, stages);
-    auto k = tc_update_kernel<NB, SOLVE>;
+    int stages = 6;
+    while (stages > 2 && TcPlan(f, NB, stages, ldt).total > 227 * 1024) --stages;
+    const TcPlan P(f, NB, stages, ldt);
+    auto k = tc_update_kernel<NB, MODE>;
     ALSK_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(P.total)));
-    const CUtensorMap map = factor_map(theta, theta_rows, ldt);
     const int64_t nrows = re - rb;
     const unsigned grid = static_cast<unsigned>(std::min<int64_t>(nrows, num_sms()));
-    k<<<grid, NTHREADS, P.total, s>>>(map, r.row_ptr, r.col_idx, r.values, r.col_offset, f, lambda, rb, nrows, stages,
+    static const bool want_prof = std::getenv("ALSK_TC_PROF") != nullptr;
+    DevBuf prof;
+    if (want_prof) {
+        prof.alloc(sizeof(long long) * grid * 14 * 6, s);
+        ALSK_CUDA(cudaMemsetAsync(prof.as<void>(), 0, sizeof(long long) * grid * 14 * 6, s));
+    }
+    k<<<grid, NTHREADS, P.total, s>>>(theta, ldt, r.row_ptr, r.col_idx, r.values, r.col_offset, f, lambda, rb, nrows, stages,
                                        x, a, b, st ? st->min_row : nullptr, st ? st->column : nullptr,
-                                       st ? st->pivot : nullptr, 0);
+                                       st ? st->pivot : nullptr, 0, want_prof ? prof.as<long long>() : nullptr);
     ALSK_LAUNCHED();
+    if (want_prof) {
+        std::vector<long long> h(static_cast<size_t>(grid) * 14 * 6);
+        ALSK_CUDA(cudaMemcpyAsync(h.data(), prof.as<void>(), h.size() * sizeof(long long), cudaMemcpyDeviceToHost, s));
+        ALSK_CUDA(cudaStreamSynchronize(s));
+        // per-role mean over CTAs (Mcycles): epilogue = warp 0, split = warp 8, mma = 12, tma = 13
+        const char* names[4] = {"epi(w0): diag,panel,trail,backsub,pre,total",
+                                "split(w8): raw_full,hl_empty,work,fence,-,total",
+                                "mma(w12): hl_full,tempty,-,-,-,total", "load(w13): raw_empty,-,-,-,-,total"};
+        const int ws[4] = {0, 8, 12, 13};
+        for (int r = 0; r < 4; ++r) {
+            double acc[6] = {0, 0, 0, 0, 0, 0};
+            for (unsigned c = 0; c < grid; ++c)
+                for (int i = 0; i < 6; ++i) acc[i] += static_cast<double>(h[(static_cast<size_t>(c) * 14 + ws[r]) * 6 + i]);
+            std::fprintf(stderr, "[tc-prof f=%d rows=%lld] %-46s", f, static_cast<long long>(nrows), names[r]);
+            for (int i = 0; i < 6; ++i) std::fprintf(stderr, " %9.3f", acc[i] / grid / 1e6);
+            std::fprintf(stderr, "\n");
+        }
+    }
 }
 
 struct Strided {
@@ -629,7 +790,9 @@ void strided(Strided& t, const float* theta, int64_t rows, int f, cudaStream_t s
     t.ptr = t.owned.as<float>();
 }
 
-template <bool SOLVE>
+// get_hermitian on tensor cores (MODE_FULL), or the half-sweep as tensor-core Hermitian
+// batches (MODE_PACKED into a device scratch) each followed by the batched packed solve.
+template <int MODE>
 bool dispatch_tc(const DevCsr& r, const float* theta, int64_t theta_rows, int f, float lambda, int64_t rb, int64_t re,
                  float* x, float* a, float* b, const SolveStatus* st, cudaStream_t s) {
     if (!tc_supported(f)) return false;
@@ -637,10 +800,23 @@ bool dispatch_tc(const DevCsr& r, const float* theta, int64_t theta_rows, int f,
     Strided th;
     strided(th, theta, theta_rows, f, s);
     const int nb = (f + 1 + 7) / 8;
-#define ALSK_TC_CASE(NBV)                                                                          \
-    if (nb <= NBV) {                                                                               \
-        launch_tc<NBV, SOLVE>(r, th.ptr, theta_rows, f, th.ldt, lambda, rb, re, x, a, b, st, s);  \
-        return true;                                                                               \
+    const int64_t pkn = packed_stride(f);
+    const int64_t batch = std::min<int64_t>(re - rb, std::max<int64_t>(1, (int64_t(3) << 30) / (pkn * 4)));
+    DevBuf scratch;
+    if (MODE == MODE_PACKED) scratch.alloc(sizeof(float) * batch * pkn, s);
+#define ALSK_TC_CASE(NBV)                                                                              \
+    if (nb <= NBV) {                                                                                   \
+        if (MODE == MODE_FULL) {                                                                       \
+            launch_tc<NBV, MODE_FULL>(r, th.ptr, theta_rows, f, th.ldt, lambda, rb, re, x, a, b, st, s); \
+        } else {                                                                                       \
+            for (int64_t b0 = rb; b0 < re; b0 += batch) {                                             \
+                const int64_t b1 = std::min(re, b0 + batch);                                           \
+                launch_tc<NBV, MODE_PACKED>(r, th.ptr, theta_rows, f, th.ldt, lambda, b0, b1, nullptr,  \
+                                            scratch.as<float>(), nullptr, nullptr, s);                  \
+                packed_solve(scratch.as<float>(), b1 - b0, f, x + (b0 - rb) * f, *st, b0 - rb, s);          \
+            }                                                                                          \
+        }                                                                                              \
+        return true;                                                                                   \
     }
     ALSK_TC_CASE(5)
     ALSK_TC_CASE(7)
@@ -657,12 +833,12 @@ bool tc_supported(int f) { return f >= 16 && f <= 119; }  // 2*round16(f+1) <= 2
 
 bool update_tc(const DevCsr& r, const float* theta, int64_t theta_rows, int f, float lambda, int64_t rb, int64_t re,
                float* x_out, const SolveStatus& st, cudaStream_t s) {
-    return dispatch_tc<true>(r, theta, theta_rows, f, lambda, rb, re, x_out, nullptr, nullptr, &st, s);
+    return dispatch_tc<MODE_PACKED>(r, theta, theta_rows, f, lambda, rb, re, x_out, nullptr, nullptr, &st, s);
 }
 
 bool hermitian_tc(const DevCsr& r, const float* theta, int64_t theta_rows, int f, float lambda, int64_t rb, int64_t re,
                   float* A, float* B, cudaStream_t s) {
-    return dispatch_tc<false>(r, theta, theta_rows, f, lambda, rb, re, nullptr, A, B, nullptr, s);
+    return dispatch_tc<MODE_FULL>(r, theta, theta_rows, f, lambda, rb, re, nullptr, A, B, nullptr, s);
 }
 
 }  // namespace alsk
