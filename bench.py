@@ -11,7 +11,9 @@ over NCCL after each half. Timing: CUDA events on the launchi
 between barriers + synchronize, max over ranks. Inputs (CSR 713 MB, CSC 713 MB) exceed L2,
 so no explicit flush is needed.
 
-Extra keys: roofline (fused half-sweep kernel vs the measured FP32 FFMA peak), cpu_baseline
+Extra keys: roofline (the tensor-core Hermitian kernel vs the measured dense tensor peak
+taken as TF32 = bf16/2 from MEASURED_PEAKS.json, with the FP32-FFMA-equivalent fraction the
+north star quotes beside it, and the batched-Cholesky phase), cpu_baseline
 (the UNMODIFIED reference compiled into oracle/_ref, timed on this host's cores on a bounded
 row sample, extrapolated by nonzeros), e2e (the same metric through the host-buffer C ABI:
 alsk_update_x / alsk_update_theta on pinned host buffers, H2D + D2H inside the timed region).
@@ -234,6 +236,8 @@ def run_ours(args):
         e1.record()
         torch.cuda.synchronize()
         kms, kl = C.c_double(), C.c_uint64()
+        hm, hn, sm_, sn = C.c_double(), C.c_uint64(), C.c_double(), C.c_uint64()
+        N.LIB.alsk_profile_phases(C.byref(hm), C.byref(hn), C.byref(sm_), C.byref(sn))
         N.LIB.alsk_profile_end(C.byref(kms), C.byref(kl))
     ms = e0.elapsed_time(e1) / args.steps
     launches = A.kernel_launch_count() - launches0
@@ -258,11 +262,15 @@ def run_ours(args):
     result = None
     if rank == 0:
         flops_half = nz_train * (f * (f + 1) + 2 * f)  # Nz (f(f+1) + 2f) per half-sweep
-        kernel_ms = kms.value / max(kl.value, 1)
-        peak = fp32_peak_probe()
-        nominal = 148 * 128 * 2 * 1.965e9 / 1e12
-        per_launch_flops = flops_half / world
-        achieved = per_launch_flops / (kernel_ms * 1e-3) / 1e12
+        ffma_peak = fp32_peak_probe()
+        nominal_ffma = 148 * 128 * 2 * 1.965e9 / 1e12
+        peaks = {}
+        try:
+            peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
+        except (OSError, ValueError):
+            pass
+        bf16 = peaks.get("bf16_tflops")
+        tf32_peak = bf16 / 2 if bf16 else 2250.0 / 2 * 1.0  # dense TF32 = half the dense bf16 rate
         traffic = None
         tf = ROOT / "profiles" / "traffic.json"
         if tf.exists():
@@ -270,6 +278,34 @@ def run_ours(args):
                 traffic = json.loads(tf.read_text()).get(args.config)
             except (OSError, ValueError):
                 traffic = None
+        if hn.value > 0:
+            # tensor-core engine: Hermitian launches and batched-Cholesky launches timed apart
+            herm_flops = 2 * args.steps * flops_half / world
+            herm_ms_launch = hm.value / hn.value
+            flops_launch = herm_flops / hn.value
+            achieved = flops_launch / (herm_ms_launch * 1e-3) / 1e12
+            solve_flops = args.steps * (m + n) * (f ** 3 / 3 + 2 * f * f) / world
+            roof = {"bound": "tensor", "kernel": "tc_update_kernel (tcgen05 tf32x2 Hermitian + bias, packed rows)",
+                    "achieved": achieved, "peak": tf32_peak, "unit": "TFLOP/s", "frac": achieved / tf32_peak,
+                    "peak_source": "MEASURED_PEAKS.json bf16_tflops / 2 (dense TF32)" if bf16 else
+                    "nominal dense TF32 (MEASURED_PEAKS.json absent)",
+                    "traffic": traffic, "flops_per_launch": flops_launch, "kernel_ms_avg": herm_ms_launch,
+                    "launches": int(hn.value), "kernel_share_of_step": (hm.value / args.steps) / ms,
+                    "fp32_ffma_equiv": {"peak": ffma_peak or nominal_ffma, "frac": achieved / (ffma_peak or nominal_ffma),
+                                        "peak_source": "measured FFMA probe (alsk_fp32_peak_probe)"},
+                    "solve": {"kernel": "tc_solve_kernel (TMEM-resident Cholesky, tensor-core rank-8 updates)",
+                              "ms_per_step": sm_.value / args.steps, "launches": int(sn.value),
+                              "achieved_tflops": solve_flops / (sm_.value * 1e-3) / 1e12 if sm_.value else None,
+                              "share_of_step": (sm_.value / args.steps) / ms}}
+        else:
+            kernel_ms = kms.value / max(kl.value, 1)
+            achieved = flops_half / world / (kernel_ms * 1e-3) / 1e12
+            peak = ffma_peak or nominal_ffma
+            roof = {"bound": "fp32-fma", "kernel": "fused_update_kernel<13> (hermitian+bias+cholesky+solve)",
+                    "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+                    "peak_source": "measured FFMA probe (alsk_fp32_peak_probe)", "traffic": traffic,
+                    "flops_per_launch": flops_half / world, "kernel_ms_avg": kernel_ms,
+                    "kernel_share_of_step": (kms.value / args.steps) / ms}
         result = {
             "metric": f"s/ALS-iter ({args.config}-shape f={f})",
             "value": ms / 1e3, "unit": "s/ALS-iter", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -277,15 +313,9 @@ def run_ours(args):
             "dtype": "f32", "data": "synthetic (planted rank-10 + U[-0.5,0.5) noise; SURVEY §8(d) generator)",
             "config": {"workload": args.config, "m": m, "n": n, "nnz_total": nnz, "nnz_train": nz_train, "f": f,
                        "lambda": lam, "holdout": 0.1, "parallelism": f"model-parallel rows x{world} + NCCL all-gather"
-                       if world > 1 else "single GPU", "l2": "inputs > L2 (CSR+CSC 1.4 GB), no flush"},
-            "roofline": {"bound": "fp32-fma", "kernel": "fused_update_kernel<13> (hermitian+bias+cholesky+solve)",
-                         "achieved": achieved, "peak": peak if peak else nominal,
-                         "peak_source": "measured FFMA probe (alsk_fp32_peak_probe)" if peak else
-                         "nominal 148 SM x 128 FMA/clk x 2 x 1965 MHz (MEASURED_PEAKS.json has no FP32 entry)",
-                         "peak_nominal": nominal, "unit": "TFLOP/s",
-                         "frac": achieved / (peak if peak else nominal), "traffic": traffic,
-                         "flops_per_launch": per_launch_flops, "kernel_ms_avg": kernel_ms,
-                         "kernel_share_of_step": (kms.value / args.steps) / ms},
+                       if world > 1 else "single GPU", "l2": "inputs > L2 (CSR+CSC 1.4 GB), no flush",
+                       "engine": A.fp32_engine()},
+            "roofline": roof,
             "gpu_launches": int(launches),
             "test_rmse_after_run": rmse,
         }

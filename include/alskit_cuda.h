@@ -110,6 +110,9 @@ void alsk_profile_begin(void);
 void alsk_set_fp32_engine(int engine);
 int alsk_fp32_engine(void);
 void alsk_profile_end(double* total_ms, uint64_t* launches);
+/* Per-phase kernel time of the tensor-core engine since alsk_profile_begin: the
+ * tensor-core Hermitian launches and the batched Cholesky launches. */
+void alsk_profile_phases(double* herm_ms, uint64_t* herm_launches, double* solve_ms, uint64_t* solve_launches);
 /* Measured FP32 FFMA throughput of the current device in TFLOP/s (roofline denominator). */
 double alsk_fp32_peak_probe(void);
 /* TFLOP/s of the Hermitian register-blocked inner loop alone (operands resident in shared

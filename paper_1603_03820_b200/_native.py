@@ -48,6 +48,7 @@ _SIGS = {
     "alsk_build_info": (C.c_char_p, []),
     "alsk_profile_begin": (None, []),
     "alsk_set_fp32_engine": (None, [C.c_int]),
+    "alsk_profile_phases": (None, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "alsk_fp32_engine": (C.c_int, []),
     "alsk_profile_end": (None, [f64p, C.POINTER(u64)]),
     "alsk_fp32_peak_probe": (C.c_double, []),

@@ -29,7 +29,19 @@ struct Profile {
     bool on = false;
     double ms = 0.0;
     uint64_t launches = 0;
+    double phase_ms[PHASE_COUNT] = {0.0, 0.0};
+    uint64_t phase_n[PHASE_COUNT] = {0, 0};
 } g_prof;
+
+}  // namespace
+
+bool prof_on() { return g_prof.on; }
+void prof_add(int phase, float ms) {
+    g_prof.phase_ms[phase] += ms;
+    g_prof.phase_n[phase] += 1;
+}
+
+namespace {
 
 template <class Fn>
 alsk_status guard(Fn&& fn) {
@@ -135,7 +147,7 @@ std::atomic<int> g_fp32_engine{0};
 bool use_tensor_cores(alsk_precision prec, int f) {
     if (prec == ALSK_PREC_FP64_EXACT || !tc_supported(f)) return false;
     if (prec == ALSK_PREC_TF32X2) return true;
-    return g_fp32_engine.load() == 2;  // auto -> FFMA kernel until the tensor-core path wins
+    return g_fp32_engine.load() != 1;  // auto -> tensor cores
 }
 
 // Core of update_x on device data: rows [rb,re) -> x_out (rows-local).
@@ -224,6 +236,12 @@ uint64_t alsk_kernel_launch_count(void) { return g_launches.load(); }
 void alsk_set_fp32_engine(int engine) { g_fp32_engine.store(engine); }
 int alsk_fp32_engine(void) { return g_fp32_engine.load(); }
 void alsk_profile_begin(void) { g_prof = Profile{true, 0.0, 0}; }
+void alsk_profile_phases(double* herm_ms, uint64_t* herm_launches, double* solve_ms, uint64_t* solve_launches) {
+    *herm_ms = g_prof.phase_ms[PHASE_HERMITIAN];
+    *herm_launches = g_prof.phase_n[PHASE_HERMITIAN];
+    *solve_ms = g_prof.phase_ms[PHASE_SOLVE];
+    *solve_launches = g_prof.phase_n[PHASE_SOLVE];
+}
 void alsk_profile_end(double* total_ms, uint64_t* launches) {
     *total_ms = g_prof.ms;
     *launches = g_prof.launches;

@@ -36,6 +36,35 @@ inline void count_launch(uint64_t n = 1) { g_launches.fetch_add(n, std::memory_o
 
 void set_breakdown_index(int64_t k);
 
+// Kernel-phase timing for the bench (alsk_profile_begin / alsk_profile_phases): when on,
+// launches are bracketed by CUDA events on their stream and accumulated per phase.
+enum ProfPhase { PHASE_HERMITIAN = 0, PHASE_SOLVE = 1, PHASE_COUNT = 2 };
+bool prof_on();
+void prof_add(int phase, float ms);
+class PhaseTimer {  // no-op unless profiling is on
+public:
+    PhaseTimer(int phase, cudaStream_t s) : phase_(phase), s_(s) {
+        if (!prof_on()) return;
+        cudaEventCreate(&e0_);
+        cudaEventCreate(&e1_);
+        cudaEventRecord(e0_, s_);
+    }
+    ~PhaseTimer() {
+        if (!e0_) return;
+        cudaEventRecord(e1_, s_);
+        cudaEventSynchronize(e1_);
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, e0_, e1_);
+        prof_add(phase_, ms);
+        cudaEventDestroy(e0_);
+        cudaEventDestroy(e1_);
+    }
+private:
+    int phase_;
+    cudaStream_t s_;
+    cudaEvent_t e0_ = nullptr, e1_ = nullptr;
+};
+
 // Keep freed stream-ordered memory in the device pool instead of returning it to the
 // driver at every synchronisation (the default threshold of 0 made per-call scratch
 // allocations re-map physical memory and stall for hundreds of milliseconds).

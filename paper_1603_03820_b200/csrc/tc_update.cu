@@ -24,7 +24,7 @@
 //                write them transposed into the K-major operand tile (lane = rating), with
 //                zero padding of partial k-groups.
 //   warp 12    : MMA issuer (one thread), owns the TMEM allocation (2 buffers x 256 columns).
-//   warp 13    : loader: the only reader of the CSR arrays (4-chunk register prefetch queue);
+//   warps 13-14: loaders: the only readers of the CSR arrays (4-chunk register prefetch queue);
 //                copies each gathered factor row with cp.async (one coalesced row per
 //                instruction) into a rating-major staging ring, completion counted per lane
 //                on the stage mbarrier (cp.async.mbarrier.arrive.noinc).
@@ -51,7 +51,7 @@ constexpr int KC = 32;                   // ratings per stage (four k-groups of 
 constexpr int HL_BYTES = 256 * KC * 4;      // 32 KB: H rows [0,NF) then 2L rows [NF,2NF), K-major
 constexpr int HL_STAGES = 2;
 constexpr int SEG_CHUNKS = 16;              // TMEM accumulation segment: 16 x 32 ratings
-constexpr int NTHREADS = 448;
+constexpr int NTHREADS = 480;  // 8 epilogue + 4 split + MMA + 2 loader warps
 constexpr int TMEM_COLS = 512;           // two buffers x 256 columns (D0 @ +0, D1 @ +NF)
 
 // ---- shared-memory plan (host and device agree) ----
@@ -123,33 +123,56 @@ struct ChunkInfo {
 constexpr uint32_t CH_FIRST = 1u, CH_LAST = 2u, CH_OWNER1 = 4u;
 
 // Walks the CTA's chunk sequence (rows j = blockIdx.x + t*gridDim.x, 32 ratings per chunk,
-// empty rows skipped) one step ahead of its consumer; the next row's extent is prefetched
-// so row changes do not expose a dependent load.
+// empty rows skipped) for one warp. Row extents come in batches of 32 rows, one row per
+// lane: the next batch's row_ptr loads are issued when the current batch starts, so a row
+// change is a register shuffle, never a dependent global load.
 struct ChunkWalker {
     const int64_t* row_ptr;
-    int64_t rb, nrows, j, k0, n, c0, nj, nk0, nn;
-    int t, nt;
-    __device__ void load_next(int64_t from, int tfrom) {
-        nj = from;
-        nt = tfrom;
-        nk0 = nn = 0;
-        while (nj < nrows) {
-            nk0 = row_ptr[rb + nj];
-            nn = row_ptr[rb + nj + 1] - nk0;
-            if (nn > 0) break;
-            nj += gridDim.x;
-            ++nt;
+    int64_t rb, nrows;
+    int64_t ck0, ck1, nk0, nk1;  // this lane's row of the current / next batch
+    int64_t k0, n, c0;
+    int batch, slot, t;
+    bool live;
+    __device__ void fetch(int b, int64_t& a0, int64_t& a1) const {
+        const int64_t j = blockIdx.x + static_cast<int64_t>(gridDim.x) * (32 * b + (threadIdx.x & 31));
+        a0 = a1 = 0;
+        if (j < nrows) {
+            a0 = row_ptr[rb + j];
+            a1 = row_ptr[rb + j + 1];
         }
     }
-    __device__ ChunkWalker(const int64_t* rp, int64_t rb_, int64_t nrows_) : row_ptr(rp), rb(rb_), nrows(nrows_) {
-        load_next(blockIdx.x, 0);
-        j = nj, k0 = nk0, n = nn, t = nt, c0 = 0;
-        load_next(j + gridDim.x, t + 1);
+    __device__ void seek() {  // from (batch, slot) to the first non-empty row, or the end
+        for (;;) {
+            const int64_t j = blockIdx.x + static_cast<int64_t>(gridDim.x) * (32 * batch + slot);
+            if (j >= nrows) {
+                live = false;
+                return;
+            }
+            k0 = __shfl_sync(0xffffffffu, ck0, slot);
+            n = __shfl_sync(0xffffffffu, ck1, slot) - k0;
+            c0 = 0;
+            t = 32 * batch + slot;
+            if (n > 0) return;
+            if (++slot == 32) next_batch();
+        }
     }
-    __device__ bool valid() const { return j < nrows; }
+    __device__ void next_batch() {
+        ++batch;
+        slot = 0;
+        ck0 = nk0;
+        ck1 = nk1;
+        fetch(batch + 1, nk0, nk1);
+    }
+    __device__ ChunkWalker(const int64_t* rp, int64_t rb_, int64_t nrows_)
+        : row_ptr(rp), rb(rb_), nrows(nrows_), batch(0), slot(0), t(0), live(true) {
+        fetch(0, ck0, ck1);
+        fetch(1, nk0, nk1);
+        seek();
+    }
+    __device__ bool valid() const { return live; }
     __device__ ChunkInfo info() const {
         ChunkInfo ci{};
-        if (!valid()) {
+        if (!live) {
             ci.cnt = -1;
             return ci;
         }
@@ -163,8 +186,8 @@ struct ChunkWalker {
     __device__ void advance() {
         c0 += KC;
         if (c0 >= n) {
-            j = nj, k0 = nk0, n = nn, t = nt, c0 = 0;
-            if (j < nrows) load_next(j + gridDim.x, t + 1);
+            if (++slot == 32) next_batch();
+            seek();
         }
     }
 };
@@ -387,7 +410,7 @@ tc_update_kernel(const float* __restrict__ theta, int ldt, const int64_t* __rest
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
         for (int s = 0; s < stages; ++s) {
-            mbar_init(&raw_full[s], 33);  // 32 cp.async arrivals + the publishing lane
+            mbar_init(&raw_full[s], 65);  // 2 x 32 cp.async arrivals + the publishing lane
             mbar_init(&raw_empty[s], 4);
         }
         for (int s = 0; s < HL_STAGES; ++s) {
@@ -408,13 +431,16 @@ tc_update_kernel(const float* __restrict__ theta, int ldt, const int64_t* __rest
     const uint32_t tmem = *tmem_slot;
     if (prof) tp0 = clock64();
 
-    if (warp == 13) {
-        // ---------------- loader (sole reader of the CSR arrays) ----------------
+    if (warp >= 13) {
+        // ---------------- loaders (the only readers of the CSR arrays) ----------------
+        // Two warps walk the same chunk sequence; loader ld copies the 16-byte pieces
+        // ld, ld+2, ... of every gathered row, loader 0 also publishes ratings and metadata.
         // A 4-deep register queue holds the column indices and ratings of upcoming chunks, so
         // their global loads are in flight long before the chunk is staged. Each factor row
         // is copied by cp.async (LDGSTS, 16 bytes per lane, one coalesced row per
         // instruction) and completion is counted on the stage's mbarrier per lane.
         constexpr int D = 4;
+        const int ldr = warp - 13;
         const int n16 = ldt >> 2;  // 16-byte pieces per factor row
         const int rs4 = P.rs * 4;
         ChunkWalker w(row_ptr, rb, nrows);
@@ -462,8 +488,10 @@ tc_update_kernel(const float* __restrict__ theta, int ldt, const int64_t* __rest
                     TA(t0, 0);
                 }
                 uint8_t* stage = ring + s * RAW;
-                raw_vals[s * KC + lane] = rv;
-                if (lane == 0) raw_info[s] = ci;
+                if (ldr == 0) {
+                    raw_vals[s * KC + lane] = rv;
+                    if (lane == 0) raw_info[s] = ci;
+                }
                 if (ci.cnt > 0) {
                     // lane = rating slot: each lane streams its own factor row, 16 bytes per
                     // instruction; padding slots of the last k-group get zeros
@@ -472,15 +500,15 @@ tc_update_kernel(const float* __restrict__ theta, int ldt, const int64_t* __rest
                     if (lane < ci.cnt) {
                         const float* src = theta + static_cast<int64_t>(v) * ldt;
                         const uint32_t dst = smem_u32(my);
-                        for (int c = 0; c < n16; ++c) cp_async16(dst + c * 16, src + 4 * c);
+                        for (int c = ldr; c < n16; c += 2) cp_async16(dst + c * 16, src + 4 * c);
                     } else if (lane < kend) {
-                        for (int c = 0; c < n16; ++c)
+                        for (int c = ldr; c < n16; c += 2)
                             *reinterpret_cast<float4*>(my + c * 16) = make_float4(0.f, 0.f, 0.f, 0.f);
                     }
                 }
                 cp_async_arrive_noinc(&raw_full[s]);
                 __syncwarp();
-                if (lane == 0) mbar_arrive(&raw_full[s]);
+                if (ldr == 0 && lane == 0) mbar_arrive(&raw_full[s]);
                 if (ci.cnt < 0) done = true;
             }
         }
@@ -718,7 +746,7 @@ tc_update_kernel(const float* __restrict__ theta, int ldt, const int64_t* __rest
     if (prof) {
         pc[5] = clock64() - tp0;
         if (lane == 0)
-            for (int i = 0; i < 6; ++i) prof[(static_cast<int64_t>(blockIdx.x) * 14 + warp) * 6 + i] = pc[i];
+            for (int i = 0; i < 6; ++i) prof[(static_cast<int64_t>(blockIdx.x) * 15 + warp) * 6 + i] = pc[i];
     }
 #undef TP
 #undef TA
@@ -744,15 +772,15 @@ void launch_tc(const DevCsr& r, const float* theta, int64_t theta_rows, int f, i
     static const bool want_prof = std::getenv("ALSK_TC_PROF") != nullptr;
     DevBuf prof;
     if (want_prof) {
-        prof.alloc(sizeof(long long) * grid * 14 * 6, s);
-        ALSK_CUDA(cudaMemsetAsync(prof.as<void>(), 0, sizeof(long long) * grid * 14 * 6, s));
+        prof.alloc(sizeof(long long) * grid * 15 * 6, s);
+        ALSK_CUDA(cudaMemsetAsync(prof.as<void>(), 0, sizeof(long long) * grid * 15 * 6, s));
     }
     k<<<grid, NTHREADS, P.total, s>>>(theta, ldt, r.row_ptr, r.col_idx, r.values, r.col_offset, f, lambda, rb, nrows, stages,
                                        x, a, b, st ? st->min_row : nullptr, st ? st->column : nullptr,
                                        st ? st->pivot : nullptr, 0, want_prof ? prof.as<long long>() : nullptr);
     ALSK_LAUNCHED();
     if (want_prof) {
-        std::vector<long long> h(static_cast<size_t>(grid) * 14 * 6);
+        std::vector<long long> h(static_cast<size_t>(grid) * 15 * 6);
         ALSK_CUDA(cudaMemcpyAsync(h.data(), prof.as<void>(), h.size() * sizeof(long long), cudaMemcpyDeviceToHost, s));
         ALSK_CUDA(cudaStreamSynchronize(s));
         // per-role mean over CTAs (Mcycles): epilogue = warp 0, split = warp 8, mma = 12, tma = 13
@@ -763,7 +791,7 @@ void launch_tc(const DevCsr& r, const float* theta, int64_t theta_rows, int f, i
         for (int r = 0; r < 4; ++r) {
             double acc[6] = {0, 0, 0, 0, 0, 0};
             for (unsigned c = 0; c < grid; ++c)
-                for (int i = 0; i < 6; ++i) acc[i] += static_cast<double>(h[(static_cast<size_t>(c) * 14 + ws[r]) * 6 + i]);
+                for (int i = 0; i < 6; ++i) acc[i] += static_cast<double>(h[(static_cast<size_t>(c) * 15 + ws[r]) * 6 + i]);
             std::fprintf(stderr, "[tc-prof f=%d rows=%lld] %-46s", f, static_cast<long long>(nrows), names[r]);
             for (int i = 0; i < 6; ++i) std::fprintf(stderr, " %9.3f", acc[i] / grid / 1e6);
             std::fprintf(stderr, "\n");
@@ -801,20 +829,48 @@ bool dispatch_tc(const DevCsr& r, const float* theta, int64_t theta_rows, int f,
     strided(th, theta, theta_rows, f, s);
     const int nb = (f + 1 + 7) / 8;
     const int64_t pkn = packed_stride(f);
-    const int64_t batch = std::min<int64_t>(re - rb, std::max<int64_t>(1, (int64_t(3) << 30) / (pkn * 4)));
-    DevBuf scratch;
-    if (MODE == MODE_PACKED) scratch.alloc(sizeof(float) * batch * pkn, s);
+    const int64_t batch = std::min<int64_t>(re - rb, std::max<int64_t>(1, (int64_t(1) << 30) / (pkn * 4)));
+    // packed-row scratch kept for the process (grow-only, never freed): a per-call ~1 GB
+    // allocation would otherwise sit on every host-API half-sweep. Callers are serialised on
+    // it: the lock is held until the stream has drained the batches that use it.
+    static float* scratch_ptr = nullptr;
+    static size_t scratch_bytes = 0;
+    static std::mutex scratch_mu;
+    std::unique_lock<std::mutex> lock(scratch_mu, std::defer_lock);
+    struct {
+        float* p;
+        float* as() const { return p; }
+    } scratch{nullptr};
+    if (MODE == MODE_PACKED) {
+        lock.lock();
+        const size_t need = sizeof(float) * batch * pkn;
+        if (scratch_bytes < need) {
+            ALSK_CUDA(cudaStreamSynchronize(s));
+            if (scratch_ptr) cudaFree(scratch_ptr);
+            scratch_ptr = nullptr;
+            scratch_bytes = 0;
+            ALSK_CUDA(cudaMalloc(&scratch_ptr, need));
+            scratch_bytes = need;
+        }
+        scratch.p = scratch_ptr;
+    }
 #define ALSK_TC_CASE(NBV)                                                                              \
     if (nb <= NBV) {                                                                                   \
         if (MODE == MODE_FULL) {                                                                       \
+            PhaseTimer pt(PHASE_HERMITIAN, s);                                                         \
             launch_tc<NBV, MODE_FULL>(r, th.ptr, theta_rows, f, th.ldt, lambda, rb, re, x, a, b, st, s); \
         } else {                                                                                       \
             for (int64_t b0 = rb; b0 < re; b0 += batch) {                                             \
                 const int64_t b1 = std::min(re, b0 + batch);                                           \
-                launch_tc<NBV, MODE_PACKED>(r, th.ptr, theta_rows, f, th.ldt, lambda, b0, b1, nullptr,  \
-                                            scratch.as<float>(), nullptr, nullptr, s);                  \
-                packed_solve(scratch.as<float>(), b1 - b0, f, x + (b0 - rb) * f, *st, b0 - rb, s);          \
+                {                                                                                      \
+                    PhaseTimer pt(PHASE_HERMITIAN, s);                                                 \
+                    launch_tc<NBV, MODE_PACKED>(r, th.ptr, theta_rows, f, th.ldt, lambda, b0, b1, nullptr, \
+                                                scratch.as(), nullptr, nullptr, s);              \
+                }                                                                                      \
+                PhaseTimer pt(PHASE_SOLVE, s);                                                         \
+                packed_solve(scratch.as(), b1 - b0, f, x + (b0 - rb) * f, *st, b0 - rb, s);      \
             }                                                                                          \
+            ALSK_CUDA(cudaStreamSynchronize(s)); /* the shared scratch is free again */              \
         }                                                                                              \
         return true;                                                                                   \
     }
@@ -826,6 +882,7 @@ bool dispatch_tc(const DevCsr& r, const float* theta, int64_t theta_rows, int f,
 #undef ALSK_TC_CASE
     return false;
 }
+
 
 }  // namespace
 
