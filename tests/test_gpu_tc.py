@@ -150,3 +150,20 @@ def test_tc_engines_agree_on_many_rows(A, orc, gpu):
         with A.use_fp32_engine(eng):
             x = A.update_x(r, th, A.SolverConfig(f=f, lambda_=0.05, accumulate_double=False))
         assert normwise_gap(x.entries, xo) <= 1e-4, eng
+
+
+def test_tc_long_rows_segmented_accumulation(A, orc, gpu):
+    """Hugewiki-like item degrees (~78K ratings per item, the Theta-half at 3.1e9 ratings over
+    39,781 items): rows of 20K-80K ratings span many 512-rating TMEM segments, each drained
+    with round-to-nearest adds, so the tensor core's truncating FP32 accumulation cannot
+    build up a bias. The factors must stay at FP32-level agreement with the FP64 oracle."""
+    f = 100
+    lengths = [20000, 40001, 78123, 511, 512, 513]
+    n = 200000
+    r = rows_with_lengths(A, lengths, n, 2026)
+    th = A.random_factor(n, f, 11)
+    st, xo = orc.update_x(ocsr(r), th.entries, n, f, 0.05, acc_double=1)
+    assert st == 0
+    x = tc_update(A, r, th, f, 0.05)
+    gap = normwise_gap(x.entries, xo)
+    assert gap <= 5e-5, gap
