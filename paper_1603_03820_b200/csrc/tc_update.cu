@@ -15,16 +15,16 @@
 // SEG_CHUNKS x 32 ratings are therefore accumulated in segments, each drained from TMEM and
 // added into shared memory with round-to-nearest FP32 adds.
 //
-// Warp roles (448 threads, 1 CTA per SM, rows j = blockIdx.x + t*gridDim.x):
+// Warp roles (672 threads, 1 CTA per SM, rows j = blockIdx.x + t*gridDim.x):
 //   warps 0-7  : two epilogue groups of 4 warps (group g takes rows with t%2 == g). TMEM ->
 //                registers -> shared memory (segment sums, symmetrisation, lambda n_u) ->
 //                8x8 tiles in registers -> blocked right-looking Cholesky -> back
 //                substitution -> x_u.
-//   warps 8-11 : split warps: read the staged rating-major rows, split tf32 hi/lo and
+//   warps 8-15 : split warps: read the staged rating-major rows, split tf32 hi/lo and
 //                write them transposed into the K-major operand tile (lane = rating), with
 //                zero padding of partial k-groups.
-//   warp 12    : MMA issuer (one thread), owns the TMEM allocation (2 buffers x 256 columns).
-//   warps 13-14: loaders: the only readers of the CSR arrays (4-chunk register prefetch queue);
+//   warp 16    : MMA issuer (one thread), owns the TMEM allocation (2 buffers x 256 columns).
+//   warps 17-20: loaders: the only readers of the CSR arrays (4-chunk register prefetch queue);
 //                copies each gathered factor row with cp.async (one coalesced row per
 //                instruction) into a rating-major staging ring, completion counted per lane
 //                on the stage mbarrier (cp.async.mbarrier.arrive.noinc).
@@ -49,9 +49,15 @@ using namespace tc;
 
 constexpr int KC = 32;                   // ratings per stage (four k-groups of 8)
 constexpr int HL_BYTES = 256 * KC * 4;      // 32 KB: H rows [0,NF) then 2L rows [NF,2NF), K-major
-constexpr int HL_STAGES = 2;
+constexpr int HL_STAGES_MAX = 3;           // operand-ring depth: 3 where shared memory allows, else 2
 constexpr int SEG_CHUNKS = 16;              // TMEM accumulation segment: 16 x 32 ratings
-constexpr int NTHREADS = 480;  // 8 epilogue + 4 split + MMA + 2 loader warps
+constexpr int NSPLIT = 8;                 // split warps
+constexpr int NG = 2;                     // epilogue groups (one alone falls behind the MMA on
+                                          // short X-half rows: measured 61 vs 54.5 ms)
+constexpr int W_SPLIT = 4 * NG, W_MMA = W_SPLIT + NSPLIT, W_LOAD = W_MMA + 1;
+constexpr int NLOAD = 4;                  // loader warps
+constexpr int NWARPS = W_LOAD + NLOAD;
+constexpr int NTHREADS = 32 * NWARPS;     // 4*NG epilogue + NSPLIT split + MMA + NLOAD loader warps
 constexpr int TMEM_COLS = 512;           // two buffers x 256 columns (D0 @ +0, D1 @ +NF)
 
 // ---- shared-memory plan (host and device agree) ----
@@ -61,22 +67,24 @@ constexpr int TMEM_COLS = 512;           // two buffers x 256 columns (D0 @ +0, 
 __host__ __device__ inline int staging_stride(int ldt) { return (ldt % 8 == 4) ? ldt : ldt + 4; }
 
 struct TcPlan {
-    int f, sld, stages, nb, rs, raw_bytes;
+    int f, sld, stages, nb, hls, rs, raw_bytes;
     int s_floats, grp_floats;
     size_t hl_off, ring_bytes, grp_bytes, bar_off, info_off, total;
-    __host__ __device__ TcPlan(int f_, int nb_, int stages_, int ldt) : f(f_), stages(stages_), nb(nb_) {
+    // solve_scratch: the fused-solve epilogue also needs panel/diag/flags per group
+    __host__ __device__ TcPlan(int f_, int nb_, int stages_, int ldt, bool solve_scratch, int hls_)
+        : f(f_), stages(stages_), nb(nb_), hls(hls_) {
         rs = staging_stride(ldt);
         raw_bytes = (KC * rs * 4 + 127) & ~127;
         sld = (f + 1) | 1;  // >= f+1 columns (A and B); odd: row writes and column reads conflict-free
         s_floats = ((f + 1) * sld + 3) & ~3;  // keep the float4 panel 16-byte aligned
         const int fp = 8 * nb;
-        grp_floats = (s_floats + 8 * fp + 64 + fp + 8 + 3) & ~3;
+        grp_floats = solve_scratch ? ((s_floats + 8 * fp + 64 + fp + 8 + 3) & ~3) : s_floats;
         hl_off = (static_cast<size_t>(stages) * raw_bytes + 1023) & ~static_cast<size_t>(1023);  // UMMA atoms: 1 KB
-        ring_bytes = hl_off + static_cast<size_t>(HL_STAGES) * HL_BYTES;
+        ring_bytes = hl_off + static_cast<size_t>(hls) * HL_BYTES;
         grp_bytes = static_cast<size_t>(grp_floats) * 4;
-        bar_off = (ring_bytes + 2 * grp_bytes + 15) & ~static_cast<size_t>(15);
-        info_off = bar_off + static_cast<size_t>(2 * stages + 2 * HL_STAGES + 6) * 8 + 16;
-        total = info_off + static_cast<size_t>(stages) * (KC * 4 + 16) + HL_STAGES * 16 + 1024;  // + align slack
+        bar_off = (ring_bytes + NG * grp_bytes + 15) & ~static_cast<size_t>(15);
+        info_off = bar_off + static_cast<size_t>(2 * stages + 2 * hls + 6) * 8 + 16;
+        total = info_off + static_cast<size_t>(stages) * (KC * 4 + 16) + hls * 16 + 1024;  // + align slack
     }
 };
 
@@ -180,7 +188,7 @@ struct ChunkWalker {
         ci.cnt = left < KC ? static_cast<int>(left) : KC;
         const int64_t ch = c0 / KC;
         ci.flags = ((ch % SEG_CHUNKS) == 0 ? CH_FIRST : 0u) |
-                   ((c0 + KC >= n || (ch % SEG_CHUNKS) == SEG_CHUNKS - 1) ? CH_LAST : 0u) | ((t & 1) ? CH_OWNER1 : 0u);
+                   ((c0 + KC >= n || (ch % SEG_CHUNKS) == SEG_CHUNKS - 1) ? CH_LAST : 0u) | ((t % NG) ? CH_OWNER1 : 0u);
         return ci;
     }
     __device__ void advance() {
@@ -371,7 +379,7 @@ tc_update_kernel(const float* __restrict__ theta, int ldt, const int64_t* __rest
                  float lambda, int64_t rb, int64_t nrows, int stages, float* __restrict__ out_x,
                  float* __restrict__ out_a, float* __restrict__ out_b, unsigned long long* __restrict__ min_row,
                  int32_t* __restrict__ column, double* __restrict__ pivot, int64_t status_base,
-                 long long* __restrict__ prof) {
+                 long long* __restrict__ prof, int hls) {
     constexpr int FP = 8 * NB;
     constexpr int NTILES = NB * (NB + 1) / 2;
     static_assert(NTILES <= 128, "tile set must fit one 128-thread epilogue group");
@@ -384,8 +392,9 @@ tc_update_kernel(const float* __restrict__ theta, int ldt, const int64_t* __rest
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw_addr = smem_u32(smem_raw);
     uint8_t* base = smem_raw + (((raw_addr + 1023u) & ~1023u) - raw_addr);
-    const TcPlan P(f, NB, stages, ldt);
+    const TcPlan P(f, NB, stages, ldt, MODE == MODE_SOLVE, hls);
     const int RAW = P.raw_bytes;
+    const int HL_STAGES = hls;
     // augmented features per operand half; a multiple of 16 keeps every 16-column TMEM load of
     // the second half aligned
     const int NF = (f + 1 + 15) & ~15;
@@ -410,11 +419,11 @@ tc_update_kernel(const float* __restrict__ theta, int ldt, const int64_t* __rest
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
         for (int s = 0; s < stages; ++s) {
-            mbar_init(&raw_full[s], 65);  // 2 x 32 cp.async arrivals + the publishing lane
-            mbar_init(&raw_empty[s], 4);
+            mbar_init(&raw_full[s], 32 * NLOAD + 1);  // NLOAD x 32 cp.async arrivals + the publishing lane
+            mbar_init(&raw_empty[s], NSPLIT);
         }
         for (int s = 0; s < HL_STAGES; ++s) {
-            mbar_init(&hl_full[s], 4);
+            mbar_init(&hl_full[s], NSPLIT);
             mbar_init(&hl_empty[s], 1);
         }
         for (int b = 0; b < 4; ++b) mbar_init(&tfull[b], 1);
@@ -423,7 +432,7 @@ tc_update_kernel(const float* __restrict__ theta, int ldt, const int64_t* __rest
     }
     for (int i = threadIdx.x; i < static_cast<int>(P.ring_bytes / 16); i += NTHREADS)
         reinterpret_cast<float4*>(ring)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (warp == 12) tmem_alloc<TMEM_COLS>(tmem_slot);
+    if (warp == W_MMA) tmem_alloc<TMEM_COLS>(tmem_slot);
     fence_proxy_async_smem();
     tc_fence_before();
     __syncthreads();
@@ -431,16 +440,16 @@ tc_update_kernel(const float* __restrict__ theta, int ldt, const int64_t* __rest
     const uint32_t tmem = *tmem_slot;
     if (prof) tp0 = clock64();
 
-    if (warp >= 13) {
+    if (warp >= W_LOAD) {
         // ---------------- loaders (the only readers of the CSR arrays) ----------------
-        // Two warps walk the same chunk sequence; loader ld copies the 16-byte pieces
-        // ld, ld+2, ... of every gathered row, loader 0 also publishes ratings and metadata.
+        // NLOAD warps walk the same chunk sequence; loader ld copies the 16-byte pieces
+        // ld, ld+NLOAD, ... of every gathered row, loader 0 also publishes ratings and metadata.
         // A 4-deep register queue holds the column indices and ratings of upcoming chunks, so
         // their global loads are in flight long before the chunk is staged. Each factor row
         // is copied by cp.async (LDGSTS, 16 bytes per lane, one coalesced row per
         // instruction) and completion is counted on the stage's mbarrier per lane.
         constexpr int D = 4;
-        const int ldr = warp - 13;
+        const int ldr = warp - W_LOAD;
         const int n16 = ldt >> 2;  // 16-byte pieces per factor row
         const int rs4 = P.rs * 4;
         ChunkWalker w(row_ptr, rb, nrows);
@@ -483,8 +492,7 @@ tc_update_kernel(const float* __restrict__ theta, int ldt, const int64_t* __rest
                 const uint32_t ph = (ctr / stages) & 1u;
                 {
                     TP(t0);
-                    if (lane == 0) mbar_wait(&raw_empty[s], ph ^ 1u);
-                    __syncwarp();
+                    mbar_wait(&raw_empty[s], ph ^ 1u);
                     TA(t0, 0);
                 }
                 uint8_t* stage = ring + s * RAW;
@@ -500,9 +508,9 @@ tc_update_kernel(const float* __restrict__ theta, int ldt, const int64_t* __rest
                     if (lane < ci.cnt) {
                         const float* src = theta + static_cast<int64_t>(v) * ldt;
                         const uint32_t dst = smem_u32(my);
-                        for (int c = ldr; c < n16; c += 2) cp_async16(dst + c * 16, src + 4 * c);
+                        for (int c = ldr; c < n16; c += NLOAD) cp_async16(dst + c * 16, src + 4 * c);
                     } else if (lane < kend) {
-                        for (int c = ldr; c < n16; c += 2)
+                        for (int c = ldr; c < n16; c += NLOAD)
                             *reinterpret_cast<float4*>(my + c * 16) = make_float4(0.f, 0.f, 0.f, 0.f);
                     }
                 }
@@ -512,11 +520,11 @@ tc_update_kernel(const float* __restrict__ theta, int ldt, const int64_t* __rest
                 if (ci.cnt < 0) done = true;
             }
         }
-    } else if (warp >= 8 && warp < 12) {
+    } else if (warp >= W_SPLIT && warp < W_MMA) {
         // ---------------- split warps ----------------
-        // lane = rating slot k of the chunk; warp pw handles feature chunks c16 = pw + 4t.
+        // lane = rating slot k of the chunk; warp pw handles feature chunks c16 = pw + NSPLIT*t.
         // Every offset below is a per-thread constant plus a multiple of t.
-        const int pw = warp - 8;
+        const int pw = warp - W_SPLIT;
         const int k = lane;
         const uint32_t raw_k = static_cast<uint32_t>(k * P.rs * 4 + pw * 16);
         uint32_t kq[4];
@@ -526,13 +534,14 @@ tc_update_kernel(const float* __restrict__ theta, int ldt, const int64_t* __rest
             kq[q] = static_cast<uint32_t>((pw >> 1) * 1024 + r8 * 128 + ((((k >> 2) ^ r8)) << 4) + (k & 3) * 4);
         }
         const uint32_t l_off = static_cast<uint32_t>(NF * 128);
-        // the rating slot (feature f) lives in chunk f>>2: warp (f>>2)&3, step f>>4, element f&3
-        const bool owns_r = pw == ((f >> 2) & 3);
+        // the rating slot (feature f) lives in chunk f>>2: warp (f>>2)%NSPLIT, step
+        // (f>>2)/NSPLIT, element f&3
+        const bool owns_r = pw == ((f >> 2) % NSPLIT);
         const int r8f = 4 * (pw & 1) + (f & 3);
         const uint32_t r_off = static_cast<uint32_t>((pw >> 1) * 1024 + r8f * 128 + ((((k >> 2) ^ r8f)) << 4) +
-                                                     (k & 3) * 4 + (f >> 4) * 2048);
+                                                     (k & 3) * 4 + ((f >> 2) / NSPLIT) * (NSPLIT * 512));
         constexpr int NC16 = 2 * NB;              // 16-byte feature chunks below 8*NB
-        constexpr int TPW = (NC16 + 3) / 4;       // chunks per split warp (upper bound)
+        constexpr int TPW = (NC16 + NSPLIT - 1) / NSPLIT;  // chunks per split warp (upper bound)
         const int nc16 = NC16 < (NF >> 2) ? NC16 : (NF >> 2);  // never spill H rows into the L half
         for (uint32_t ctr = 0;; ++ctr) {
             const int s = ctr % stages;
@@ -548,19 +557,20 @@ tc_update_kernel(const float* __restrict__ theta, int ldt, const int64_t* __rest
             if (ci.cnt >= 0) {
                 // Padding slots of the k-group were zeroed by the loader, so the split is
                 // branch-free: h = rna_tf32(x), 2l = 2 rna_tf32(x - h) by bit ops.
-                const uint8_t* raw = ring + s * RAW + raw_k;
-                uint8_t* H = hl + hs * HL_BYTES;
+                const uint8_t* __restrict__ raw = ring + s * RAW + raw_k;  // staging and operand
+                uint8_t* __restrict__ H = hl + hs * HL_BYTES;                // tiles never alias
 #pragma unroll
                 for (int t = 0; t < TPW; ++t) {
-                    if (pw + 4 * t < nc16) {  // uniform per warp
-                        const float4 x = *reinterpret_cast<const float4*>(__builtin_assume_aligned(raw + t * 64, 16));
+                    if (pw + NSPLIT * t < nc16) {  // uniform per warp
+                        const float4 x =
+                            *reinterpret_cast<const float4*>(__builtin_assume_aligned(raw + t * (NSPLIT * 16), 16));
                         const float xv[4] = {x.x, x.y, x.z, x.w};
 #pragma unroll
                         for (int q = 0; q < 4; ++q) {
                             const float h = __uint_as_float((__float_as_uint(xv[q]) + 0x1000u) & 0xFFFFE000u);
                             const float l = xv[q] - h;
                             const float l2 = 2.f * __uint_as_float((__float_as_uint(l) + 0x1000u) & 0xFFFFE000u);
-                            uint8_t* dst = H + kq[q] + t * 2048;
+                            uint8_t* dst = H + kq[q] + t * (NSPLIT * 512);
                             *reinterpret_cast<float*>(dst) = h;
                             *reinterpret_cast<float*>(dst + l_off) = l2;
                         }
@@ -585,39 +595,38 @@ tc_update_kernel(const float* __restrict__ theta, int ldt, const int64_t* __rest
             }
             if (ci.cnt < 0) break;
         }
-    } else if (warp == 12) {
+    } else if (warp == W_MMA) {
         // ---------------- MMA issuer ----------------
         const uint32_t idesc = idesc_tf32(128, 2 * NF);
         uint32_t job = 0;
         for (uint32_t ctr = 0;; ++ctr) {
             const int hs = ctr % HL_STAGES;
-            ChunkInfo ci;
-            {
-                TP(t0);
-                if (lane == 0) {
-                    mbar_wait(&hl_full[hs], (ctr / HL_STAGES) & 1u);
-                    ci = hl_info[hs];
-                }
-                TA(t0, 0);
-            }
-            ci.cnt = __shfl_sync(0xffffffffu, ci.cnt, 0);
-            ci.flags = __shfl_sync(0xffffffffu, ci.flags, 0);
+            // every lane waits (a lane-0-only wait followed by a warp shuffle measured ~700
+            // cycles of reconvergence per chunk)
+            TP(t0);
+            mbar_wait(&hl_full[hs], (ctr / HL_STAGES) & 1u);
+            TA(t0, 0);
+            const ChunkInfo ci = hl_info[hs];
             if (ci.cnt < 0) break;
             const uint32_t b = job & 1u;
             const uint32_t dcol = tmem + b * 256u;
+            TP(t1);
+            if (ci.flags & CH_FIRST) mbar_wait(&tempty[b], ((job >> 1) & 1u) ^ 1u);
+            TA(t1, 1);
+            tc_fence_after();
             if (lane == 0) {
-                TP(t1);
-                if (ci.flags & CH_FIRST) mbar_wait(&tempty[b], ((job >> 1) & 1u) ^ 1u);
-                TA(t1, 1);
-                tc_fence_after();
                 const uint32_t hb = smem_u32(hl + hs * HL_BYTES);
                 const int ksteps = (ci.cnt + 7) >> 3;
+                TP(t2);
                 for (int kb = 0; kb < ksteps; ++kb) {
                     const uint64_t d = sdesc_sw128(hb + kb * 32, 16, 1024);
                     mma_tf32(dcol, d, d, idesc, (!(ci.flags & CH_FIRST) || kb > 0) ? 1u : 0u);
                 }
+                TA(t2, 2);
+                TP(t3);
                 mma_commit(&hl_empty[hs]);
                 if (ci.flags & CH_LAST) mma_commit(&tfull[2 * ((ci.flags & CH_OWNER1) ? 1 : 0) + b]);
+                TA(t3, 3);
             }
             __syncwarp();
             if (ci.flags & CH_LAST) ++job;
@@ -639,7 +648,7 @@ tc_update_kernel(const float* __restrict__ theta, int ldt, const int64_t* __rest
         int bi = 0, bj = 0;
         if (active) tile_coords_colmajor(e, NB, bi, bj);
         const int ia = 8 * bi, jb = 8 * bj;
-        if (e == 0) flags[0] = flags[1] = flags[2] = 0;
+        if (MODE == MODE_SOLVE && e == 0) flags[0] = flags[1] = flags[2] = 0;  // scratch only in solve mode
         float* Srow = S + e * sld;
         uint32_t job = 0, use[2] = {0u, 0u};
         int t = 0;
@@ -647,7 +656,7 @@ tc_update_kernel(const float* __restrict__ theta, int ldt, const int64_t* __rest
             const int64_t u = rb + it.j;
             const int64_t n = row_ptr[u + 1] - row_ptr[u];
             const uint32_t nseg = static_cast<uint32_t>(row_segments(n));
-            if ((t & 1) != g) {
+            if ((t % NG) != g) {
                 job += nseg;
                 continue;
             }
@@ -687,37 +696,47 @@ tc_update_kernel(const float* __restrict__ theta, int ldt, const int64_t* __rest
                 }
                 TP(t2);
                 named_barrier(bar_id, 128);
-                // symmetrise in place: lower A (+ lambda n_u on the diagonal, float arithmetic as
-                // solver.hpp:141,152) and B in row f
-                if (e < f) {
-                    for (int j = 0; j < e; ++j) Srow[j] = 0.5f * (Srow[j] + S[j * sld + e]);
-                    Srow[e] += lambda * static_cast<float>(n);
-                } else if (e == f) {
-                    for (int j = 0; j < f; ++j) Srow[j] = 0.5f * (Srow[j] + S[j * sld + f]);
-                }
-                named_barrier(bar_id, 128);
+                const float reg = lambda * static_cast<float>(n);  // float arithmetic as solver.hpp:141,152
                 if constexpr (MODE == MODE_FULL) {
+                    // A = sym(S) (+ lambda n_u on the diagonal) written full and B = row f; the
+                    // symmetrisation 0.5 (S_ij + S_ji) is commutative, so A mirrors bit-exactly
                     float* a_out = out_a + row * static_cast<int64_t>(f) * f;
                     float* b_out = out_b + row * static_cast<int64_t>(f);
                     for (int idx = e; idx < f * f; idx += 128) {
                         const int i = idx / f, j = idx - i * f;
-                        a_out[idx] = j <= i ? S[i * sld + j] : S[j * sld + i];
+                        float v = 0.5f * (S[i * sld + j] + S[j * sld + i]);
+                        if (i == j) v += reg;
+                        a_out[idx] = v;
                     }
-                    for (int j = e; j < f; j += 128) b_out[j] = S[f * sld + j];
+                    for (int j = e; j < f; j += 128) b_out[j] = 0.5f * (S[f * sld + j] + S[j * sld + f]);
                     named_barrier(bar_id, 128);
                     continue;
                 } else if constexpr (MODE == MODE_PACKED) {
-                    // warp-cooperative rows: row i (lower part, then B as row f) is contiguous
+                    // one pass, warp-cooperative rows: lower row i of sym(S) (row f = B) is
+                    // contiguous in the packed output; S_ij reads are contiguous across lanes and
+                    // the transposed S_ji reads are conflict-free (odd row stride)
                     float* pk = out_a + row * packed_stride(f);
                     const int wq = e >> 5, ln = e & 31;
                     for (int i = wq; i <= f; i += 4) {
                         const int len = i < f ? i + 1 : f;
                         float* dst = pk + i * (i + 1) / 2;  // row f starts at f(f+1)/2
-                        for (int j = ln; j < len; j += 32) dst[j] = S[i * sld + j];
+                        for (int j = ln; j < len; j += 32) {
+                            float v = 0.5f * (S[i * sld + j] + S[j * sld + i]);
+                            if (j == i) v += reg;
+                            dst[j] = v;
+                        }
                     }
                     named_barrier(bar_id, 128);
                     continue;
                 }
+                // fused solve: symmetrise in place, lower A (+ lambda n_u) and B in row f
+                if (e < f) {
+                    for (int j = 0; j < e; ++j) Srow[j] = 0.5f * (Srow[j] + S[j * sld + e]);
+                    Srow[e] += reg;
+                } else if (e == f) {
+                    for (int j = 0; j < f; ++j) Srow[j] = 0.5f * (Srow[j] + S[j * sld + f]);
+                }
+                named_barrier(bar_id, 128);
 #pragma unroll
                 for (int ii = 0; ii < 8; ++ii)
 #pragma unroll
@@ -746,13 +765,13 @@ tc_update_kernel(const float* __restrict__ theta, int ldt, const int64_t* __rest
     if (prof) {
         pc[5] = clock64() - tp0;
         if (lane == 0)
-            for (int i = 0; i < 6; ++i) prof[(static_cast<int64_t>(blockIdx.x) * 15 + warp) * 6 + i] = pc[i];
+            for (int i = 0; i < 6; ++i) prof[(static_cast<int64_t>(blockIdx.x) * NWARPS + warp) * 6 + i] = pc[i];
     }
 #undef TP
 #undef TA
     tc_fence_before();
     __syncthreads();
-    if (warp == 12) {
+    if (warp == W_MMA) {
         tc_fence_after();
         tmem_dealloc<TMEM_COLS>(tmem);
     }
@@ -762,9 +781,15 @@ tc_update_kernel(const float* __restrict__ theta, int ldt, const int64_t* __rest
 template <int NB, int MODE>
 void launch_tc(const DevCsr& r, const float* theta, int64_t theta_rows, int f, int ldt, float lambda, int64_t rb,
                int64_t re, float* x, float* a, float* b, const SolveStatus* st, cudaStream_t s) {
-    int stages = 6;
-    while (stages > 2 && TcPlan(f, NB, stages, ldt).total > 227 * 1024) --stages;
-    const TcPlan P(f, NB, stages, ldt);
+    // deepest operand ring first (the MMA is fed by the split through it), then the staging ring
+    int hls = HL_STAGES_MAX, stages = 6;
+    for (;;) {
+        while (stages > 2 && TcPlan(f, NB, stages, ldt, MODE == MODE_SOLVE, hls).total > 227 * 1024) --stages;
+        if (stages >= 3 || hls == 2) break;
+        --hls;
+        stages = 6;
+    }
+    const TcPlan P(f, NB, stages, ldt, MODE == MODE_SOLVE, hls);
     auto k = tc_update_kernel<NB, MODE>;
     ALSK_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(P.total)));
     const int64_t nrows = re - rb;
@@ -772,26 +797,26 @@ void launch_tc(const DevCsr& r, const float* theta, int64_t theta_rows, int f, i
     static const bool want_prof = std::getenv("ALSK_TC_PROF") != nullptr;
     DevBuf prof;
     if (want_prof) {
-        prof.alloc(sizeof(long long) * grid * 15 * 6, s);
-        ALSK_CUDA(cudaMemsetAsync(prof.as<void>(), 0, sizeof(long long) * grid * 15 * 6, s));
+        prof.alloc(sizeof(long long) * grid * NWARPS * 6, s);
+        ALSK_CUDA(cudaMemsetAsync(prof.as<void>(), 0, sizeof(long long) * grid * NWARPS * 6, s));
     }
     k<<<grid, NTHREADS, P.total, s>>>(theta, ldt, r.row_ptr, r.col_idx, r.values, r.col_offset, f, lambda, rb, nrows, stages,
                                        x, a, b, st ? st->min_row : nullptr, st ? st->column : nullptr,
-                                       st ? st->pivot : nullptr, 0, want_prof ? prof.as<long long>() : nullptr);
+                                       st ? st->pivot : nullptr, 0, want_prof ? prof.as<long long>() : nullptr, hls);
     ALSK_LAUNCHED();
     if (want_prof) {
-        std::vector<long long> h(static_cast<size_t>(grid) * 15 * 6);
+        std::vector<long long> h(static_cast<size_t>(grid) * NWARPS * 6);
         ALSK_CUDA(cudaMemcpyAsync(h.data(), prof.as<void>(), h.size() * sizeof(long long), cudaMemcpyDeviceToHost, s));
         ALSK_CUDA(cudaStreamSynchronize(s));
         // per-role mean over CTAs (Mcycles): epilogue = warp 0, split = warp 8, mma = 12, tma = 13
         const char* names[4] = {"epi(w0): diag,panel,trail,backsub,pre,total",
-                                "split(w8): raw_full,hl_empty,work,fence,-,total",
-                                "mma(w12): hl_full,tempty,-,-,-,total", "load(w13): raw_empty,-,-,-,-,total"};
-        const int ws[4] = {0, 8, 12, 13};
+                                "split: raw_full,hl_empty,work,fence,-,total",
+                                "mma: hl_full,tempty,issue,commit,-,total", "load: raw_empty,-,-,-,-,total"};
+        const int ws[4] = {0, W_SPLIT, W_MMA, W_LOAD};
         for (int r = 0; r < 4; ++r) {
             double acc[6] = {0, 0, 0, 0, 0, 0};
             for (unsigned c = 0; c < grid; ++c)
-                for (int i = 0; i < 6; ++i) acc[i] += static_cast<double>(h[(static_cast<size_t>(c) * 15 + ws[r]) * 6 + i]);
+                for (int i = 0; i < 6; ++i) acc[i] += static_cast<double>(h[(static_cast<size_t>(c) * NWARPS + ws[r]) * 6 + i]);
             std::fprintf(stderr, "[tc-prof f=%d rows=%lld] %-46s", f, static_cast<long long>(nrows), names[r]);
             for (int i = 0; i < 6; ++i) std::fprintf(stderr, " %9.3f", acc[i] / grid / 1e6);
             std::fprintf(stderr, "\n");
