@@ -118,7 +118,7 @@ struct StatusBufs {
     // Raise the reference's NumericalError (solver.hpp:232-235) if any row broke down.
     // `index_base` is subtracted from the failing launch-relative row to get the batch
     // index; batch_rows > 0 folds a global row into update_x's batch numbering.
-    void raise_if_broken(cudaStream_t s, int64_t batch_rows) {
+    void raise_if_broken(cudaStream_t s, int64_t batch_rows, int64_t first_row = 0) {
         unsigned long long bad = 0;
         d2h(&bad, st.min_row, 1, s);
         ALSK_CUDA(cudaStreamSynchronize(s));
@@ -128,7 +128,8 @@ struct StatusBufs {
         d2h(&col, st.column + bad, 1, s);
         d2h(&piv, st.pivot + bad, 1, s);
         ALSK_CUDA(cudaStreamSynchronize(s));
-        const int64_t k = batch_rows > 0 ? static_cast<int64_t>(bad) % batch_rows : static_cast<int64_t>(bad);
+        const int64_t g = first_row + static_cast<int64_t>(bad);  // matrix row of the failure
+        const int64_t k = batch_rows > 0 ? g % batch_rows : g;
         t_breakdown = k;
         fail_numerical("cholesky breakdown at batch index " + std::to_string(k) + " (pivot " +
                        std::to_string(piv) + " at column " + std::to_string(col - 1) + ")");
@@ -181,7 +182,7 @@ void update_rows_device(const DevCsr& r, const float* theta, int64_t theta_rows,
             cudaEventDestroy(e0);
             cudaEventDestroy(e1);
         }
-        sb.raise_if_broken(s, br);
+        sb.raise_if_broken(s, br, rb);
         return;
     }
     if (e0) cudaEventDestroy(e0);
@@ -196,9 +197,6 @@ void update_rows_device(const DevCsr& r, const float* theta, int64_t theta_rows,
         st.pivot += (b0 - rb);
         // solve_exact reports launch-relative rows; shift by the batch offset
         solve_exact(A.as<float>(), B.as<float>(), b1 - b0, f, false, x_out + (b0 - rb) * f, st, s);
-        if (b0 != rb) {
-            // re-base: min_row holds a launch-relative index; check per chunk
-        }
         unsigned long long bad = 0;
         d2h(&bad, sb.st.min_row, 1, s);
         ALSK_CUDA(cudaStreamSynchronize(s));
@@ -327,22 +325,84 @@ alsk_status alsk_batch_solve(const float* a, const float* b, int64_t count, int 
     });
 }
 
+// update_x on host buffers (solver.hpp:330-345), pipelined: the rows are split into
+// PIPE_BATCHES ranges; each range's col_idx/values go host->device on a copy stream while the
+// previous range computes, and each solved range of X goes back while the next computes.
+// Only row_ptr and the gathered factor must be resident before the first range starts.
 alsk_status alsk_update_x(const alsk_csr* r, const float* theta, int64_t theta_rows, int f,
                           const alsk_solver_config* cfg, float* x_out) {
     return guard([&] {
         check_update_shapes(r, theta_rows, f);
         if (r->rows == 0) return;
         require_device();
-        cudaStream_t s = nullptr;
-        StagedCsr R(r, s);
-        DevBuf T(sizeof(float) * std::max<int64_t>(theta_rows * f, 1), s);
-        h2d(T.as<float>(), theta, theta_rows * f, s);
-        DevBuf X(sizeof(float) * r->rows * f, s);
-        update_rows_device(R.view, T.as<float>(), theta_rows, f, cfg->lambda,
-                           cfg->accumulate_double != 0 ? ALSK_PREC_FP64_EXACT : ALSK_PREC_FP32, cfg->batch_rows, 0,
-                           r->rows, X.as<float>(), s);
-        d2h(x_out, X.as<float>(), r->rows * f, s);
-        ALSK_CUDA(cudaStreamSynchronize(s));
+        static cudaStream_t s = nullptr, c = nullptr;  // compute / copy streams (process lifetime)
+        if (!s) {
+            ALSK_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+            ALSK_CUDA(cudaStreamCreateWithFlags(&c, cudaStreamNonBlocking));
+        }
+        const int64_t m = r->rows, nnz = r->nnz;
+        DevBuf RP(sizeof(int64_t) * (m + 1), s), CI(sizeof(int32_t) * std::max<int64_t>(nnz, 1), s),
+            V(sizeof(float) * std::max<int64_t>(nnz, 1), s), T(sizeof(float) * std::max<int64_t>(theta_rows * f, 1), s),
+            X(sizeof(float) * m * f, s);
+        struct Events {
+            std::vector<cudaEvent_t> ev;
+            cudaEvent_t make() {
+                cudaEvent_t e;
+                ALSK_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+                ev.push_back(e);
+                return e;
+            }
+            ~Events() {
+                for (auto e : ev) cudaEventDestroy(e);
+            }
+        } evs;
+        struct Drain {  // destroyed before the buffers: no copy may outlive them (errors included)
+            cudaStream_t c, s;
+            ~Drain() {
+                cudaStreamSynchronize(c);
+                cudaStreamSynchronize(s);
+            }
+        } drain{c, s};
+        cudaEvent_t allocated = evs.make();
+        ALSK_CUDA(cudaEventRecord(allocated, s));
+        ALSK_CUDA(cudaStreamWaitEvent(c, allocated, 0));
+        h2d(RP.as<int64_t>(), r->row_ptr, m + 1, c);
+        h2d(T.as<float>(), theta, theta_rows * f, c);
+        cudaEvent_t base = evs.make();
+        ALSK_CUDA(cudaEventRecord(base, c));
+        constexpr int64_t PIPE_BATCHES = 8;
+        const int64_t nb = std::min<int64_t>(PIPE_BATCHES, m);
+        std::vector<cudaEvent_t> staged(nb);
+        for (int64_t k = 0; k < nb; ++k) {
+            const int64_t b0 = m * k / nb, b1 = m * (k + 1) / nb;
+            const int64_t k0 = r->row_ptr[b0], k1 = r->row_ptr[b1];
+            h2d(CI.as<int32_t>() + k0, r->col_idx + k0, k1 - k0, c);
+            h2d(V.as<float>() + k0, r->values + k0, k1 - k0, c);
+            staged[k] = evs.make();
+            ALSK_CUDA(cudaEventRecord(staged[k], c));
+        }
+        DevCsr view;
+        view.rows = m;
+        view.cols = r->cols;
+        view.col_offset = r->col_offset;
+        view.nnz = nnz;
+        view.row_ptr = RP.as<int64_t>();
+        view.col_idx = CI.as<int32_t>();
+        view.values = V.as<float>();
+        ALSK_CUDA(cudaStreamWaitEvent(s, base, 0));
+        const alsk_precision prec = cfg->accumulate_double != 0 ? ALSK_PREC_FP64_EXACT : ALSK_PREC_FP32;
+        for (int64_t k = 0; k < nb; ++k) {
+            const int64_t b0 = m * k / nb, b1 = m * (k + 1) / nb;
+            ALSK_CUDA(cudaStreamWaitEvent(s, staged[k], 0));
+            update_rows_device(view, T.as<float>(), theta_rows, f, cfg->lambda, prec, cfg->batch_rows, b0, b1,
+                               X.as<float>() + b0 * f, s);
+            cudaEvent_t solved = evs.make();
+            ALSK_CUDA(cudaEventRecord(solved, s));
+            ALSK_CUDA(cudaStreamWaitEvent(c, solved, 0));
+            d2h(x_out + b0 * f, X.as<float>() + b0 * f, (b1 - b0) * f, c);
+        }
+        ALSK_CUDA(cudaStreamSynchronize(c));
+        ALSK_CUDA(cudaStreamSynchronize(s));  // the buffers are freed (stream-ordered) on s
     });
 }
 
