@@ -159,16 +159,16 @@ tc_solve_kernel(const float* __restrict__ packed, int64_t count, int f, float* _
     const uint32_t prow = static_cast<uint32_t>((i >> 3) * 1024 + (i & 7) * 128);
     const uint32_t pc0 = prow + ((0u ^ (i & 7)) << 4), pc1 = prow + ((1u ^ (i & 7)) << 4);
 
-    for (; g < ngroups; g += gridDim.x) {
-        const int64_t row0 = g * RPC;
+    // fill TMEM with my row of each system of group gg (lower part; row f = b); nz[r] flags a
+    // nonzero A entry in my row
+    auto fill = [&](int64_t gg, int (&nz)[RPC]) {
         mbar_wait(load_bar, load_phase);
         load_phase ^= 1u;
-        bool active[RPC];
-        // ---- fill TMEM with my row of each system (lower part; row f = b) ----
+        const int64_t rr0 = gg * RPC;
 #pragma unroll
         for (int r = 0; r < RPC; ++r) {
-            const bool exists = row0 + r < count;
-            int nz = 0;
+            const bool exists = rr0 + r < count;
+            nz[r] = 0;
             for (int c0 = 0; c0 < N; c0 += 8) {
                 float v[8];
 #pragma unroll
@@ -178,7 +178,7 @@ tc_solve_kernel(const float* __restrict__ packed, int64_t count, int f, float* _
                     if (exists) {
                         if (i < f && j <= i) {
                             t = rowbuf[r][i * (i + 1) / 2 + j];
-                            nz |= t != 0.f;
+                            nz[r] |= t != 0.f;
                         } else if (i == f && j < f) {
                             t = rowbuf[r][f * (f + 1) / 2 + j];
                         }
@@ -187,13 +187,22 @@ tc_solve_kernel(const float* __restrict__ packed, int64_t count, int f, float* _
                 }
                 tmem_st8(tlane + r * 128 + c0, v);
             }
-            active[r] = __syncthreads_or(nz) != 0;  // all-zero A: x = 0 (solver.hpp:215-220)
-            if (exists && !active[r]) {
+        }
+        tmem_st_wait();
+    };
+    int nzr[RPC];
+    if (g < ngroups) fill(g, nzr);
+    for (; g < ngroups; g += gridDim.x) {
+        const int64_t row0 = g * RPC;
+        bool active[RPC];
+#pragma unroll
+        for (int r = 0; r < RPC; ++r) {
+            active[r] = __syncthreads_or(nzr[r]) != 0;  // all-zero A: x = 0 (solver.hpp:215-220)
+            if (row0 + r < count && !active[r]) {
                 if (i < f) out_x[(row0 + r) * f + i] = 0.f;
                 if (i == 0) column[row0 + r] = 0;
             }
         }
-        tmem_st_wait();
         tc_fence_before();
         __syncthreads();
         if (i == 0 && g + gridDim.x < ngroups) issue_load(g + gridDim.x);  // rowbufs are free
@@ -374,6 +383,9 @@ tc_solve_kernel(const float* __restrict__ packed, int64_t count, int f, float* _
             }
         }
         __syncthreads();
+        // back substitution of system r by warp r, overlapped with the next group's TMEM fill
+        // by the other warps (each warp fills its own lanes once it is free); the barrier at
+        // the top of the next iteration orders the tiles' reuse
 #pragma unroll
         for (int r = 0; r < RPC; ++r) {
             if (warp != r || !active[r]) continue;
@@ -410,8 +422,10 @@ tc_solve_kernel(const float* __restrict__ packed, int64_t count, int f, float* _
             }
             if (lane == 0) column[row0 + r] = 0;
         }
-        tc_fence_before();
-        __syncthreads();  // TMEM, tiles and scratch are reused by the next group
+        if (g + gridDim.x < ngroups) {
+            tc_fence_after();
+            fill(g + gridDim.x, nzr);
+        }
     }
     tc_fence_before();
     __syncthreads();
