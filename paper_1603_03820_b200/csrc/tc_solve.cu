@@ -218,8 +218,10 @@ tc_solve_kernel(const float* __restrict__ packed, int64_t count, int f, float* _
 #pragma unroll
             for (int r = 0; r < RPC; ++r) tmem_ld8(tlane + r * 128 + r0, a[r]);
             tmem_ld_wait();
-            // (1) diagonal rows -> shared memory; system r's block is factored by thread 32*r'
-            //     of a distinct warp so the RPC factorizations run concurrently
+            // (1) diagonal rows -> shared memory; the block is factored by a lane of the warp
+            //     that holds those rows (a warp sync suffices: the rest of the CTA waits at the
+            //     barrier after the factorization)
+            const int dwarp = r0 >> 5;
             if (i >= r0 && i < r0 + 8) {
 #pragma unroll
                 for (int r = 0; r < RPC; ++r) {
@@ -227,10 +229,10 @@ tc_solve_kernel(const float* __restrict__ packed, int64_t count, int f, float* _
                     *reinterpret_cast<float4*>(&ss[r].blk[(i - r0) * 8 + 4]) = make_float4(a[r][4], a[r][5], a[r][6], a[r][7]);
                 }
             }
-            __syncthreads();
+            if (warp == dwarp) __syncwarp();
 #pragma unroll
             for (int r = 0; r < RPC; ++r) {
-                if (i != 32 * ((r + 1) & 3) || !active[r]) continue;
+                if (i != 32 * dwarp + ((r0 & 31) + 8 * r) % 32 || !active[r]) continue;
                 float* blk = ss[r].blk;
                 float l[8][8];
 #pragma unroll
