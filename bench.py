@@ -285,6 +285,8 @@ def run_ours(args):
             flops_launch = herm_flops / hn.value
             achieved = flops_launch / (herm_ms_launch * 1e-3) / 1e12
             solve_flops = args.steps * (m + n) * (f ** 3 / 3 + 2 * f * f) / world
+            pk_row = 4 * (((f * (f + 1) // 2 + f) + 3) // 4 * 4)
+            herm_bytes = args.steps * (2 * nz_train * (4 * f + 8) + 8 * (m + n + 2) + (m + n) * pk_row) / world
             roof = {"bound": "tensor", "kernel": "tc_update_kernel (tcgen05 tf32x2 Hermitian + bias, packed rows)",
                     "achieved": achieved, "peak": tf32_peak, "unit": "TFLOP/s", "frac": achieved / tf32_peak,
                     "peak_source": "MEASURED_PEAKS.json bf16_tflops / 2 (dense TF32)" if bf16 else
@@ -293,6 +295,15 @@ def run_ours(args):
                     "launches": int(hn.value), "kernel_share_of_step": (hm.value / args.steps) / ms,
                     "fp32_ffma_equiv": {"peak": ffma_peak or nominal_ffma, "frac": achieved / (ffma_peak or nominal_ffma),
                                         "peak_source": "measured FFMA probe (alsk_fp32_peak_probe)"},
+                    # the same launches against HBM: algorithmic bytes = per rating the column
+                    # index, the value and the gathered factor row (4f), per row the row pointer
+                    # and the packed A/B row written for the solve
+                    "gather": {"bytes_per_launch": herm_bytes / hn.value,
+                               "achieved": herm_bytes / (hm.value * 1e-3) / 1e9, "peak": peaks.get("hbm_gbs"),
+                               "unit": "GB/s",
+                               "frac": (herm_bytes / (hm.value * 1e-3) / 1e9) / peaks["hbm_gbs"]
+                               if peaks.get("hbm_gbs") else None,
+                               "peak_source": "MEASURED_PEAKS.json hbm_gbs"},
                     "solve": {"kernel": "tc_solve_kernel (TMEM-resident Cholesky, tensor-core rank-8 updates)",
                               "ms_per_step": sm_.value / args.steps, "launches": int(sn.value),
                               "achieved_tflops": solve_flops / (sm_.value * 1e-3) / 1e12 if sm_.value else None,

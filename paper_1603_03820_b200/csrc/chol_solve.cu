@@ -75,10 +75,10 @@ packed_solve_kernel(const float* __restrict__ packed, int f, float* __restrict__
             float v = 0.f;
             if (active && j < f) {
                 if (i < f && j <= i) {
-                    v = __ldg(pk + i * (i + 1) / 2 + j);
+                    v = __ldg(pk + pb_index(f, i, j));
                     nz |= v != 0.f;
                 } else if (i == f) {
-                    v = __ldg(pk + f * (f + 1) / 2 + j);
+                    v = __ldg(pk + pb_index(f, f, j));
                 }
             }
             acc[ii][jj] = v;

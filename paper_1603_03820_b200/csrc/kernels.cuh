@@ -58,17 +58,28 @@ bool update_fused_fp32(const DevCsr& r, const float* theta, int64_t theta_rows, 
 bool hermitian_fused_fp32(const DevCsr& r, const float* theta, int64_t theta_rows, int f, float lambda,
                           int64_t rb, int64_t re, float* A, float* B, cudaStream_t s);
 
-// Tensor-core (tcgen05 kind::tf32, two-term split) assembly fused with the in-register
-// Cholesky, one persistent CTA per SM (tc_update.cu). tc_supported: 16 <= f <= 119.
+// Tensor-core (tcgen05 kind::tf32, two-term split) Hermitian assembly, one persistent CTA per
+// SM (tc_update.cu), followed by the batched TMEM Cholesky (tc_solve.cu).
+// tc_supported: 16 <= f <= 119.
 bool tc_supported(int f);
 bool update_tc(const DevCsr& r, const float* theta, int64_t theta_rows, int f, float lambda, int64_t rb,
                int64_t re, float* x_out, const SolveStatus& st, cudaStream_t s);
 bool hermitian_tc(const DevCsr& r, const float* theta, int64_t theta_rows, int f, float lambda, int64_t rb,
                   int64_t re, float* A, float* B, cudaStream_t s);
 
-// Packed Hermitian rows: lower A (lambda n_u included) then b, f(f+1)/2 + f floats, row
-// stride rounded to 4 floats so every row is 16-byte aligned for bulk copies.
-__host__ __device__ inline int64_t packed_stride(int f) { return ((static_cast<int64_t>(f) * (f + 1) / 2 + f) + 3) & ~int64_t(3); }
+// Packed Hermitian rows (panel-blocked): the lower triangle of the augmented matrix
+// [A (lambda n_u included) ; b^T] stored by 8-column block b = 0 .. ceil(f/8)-1 as rows
+// 8b .. f (row f = b^T) of 8 floats each (columns 8b .. 8b+7; cells above the diagonal or at
+// columns >= f hold 0). A lane owning matrix row i reads its 8 entries of block b as two
+// 16-byte vectors at pb_block(f, b) + 8 (i - 8b); every row is 32-byte aligned.
+__host__ __device__ inline int64_t pb_block(int f, int b) {
+    return 8 * (static_cast<int64_t>(b) * (f + 1) - 4 * static_cast<int64_t>(b) * (b - 1));
+}
+__host__ __device__ inline int64_t packed_stride(int f) { return pb_block(f, (f + 7) / 8); }
+// element (i, j), j <= i (or i == f, j < f) of a packed row
+__host__ __device__ inline int64_t pb_index(int f, int i, int j) {
+    return pb_block(f, j >> 3) + 8 * static_cast<int64_t>(i - (j & ~7)) + (j & 7);
+}
 
 // Batched FP32 solves of packed rows (status rows reported at status_off + i):
 //  packed_solve       - tensor-core Cholesky, matrix resident in TMEM (tc_solve.cu);

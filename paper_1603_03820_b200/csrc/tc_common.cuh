@@ -53,6 +53,24 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         }
     } while (!done);
 }
+// The same wait with a nanosleep back-off between probes: for long or latency-tolerant
+// waits, so the waiting warp does not take issue slots from the warps doing the work.
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity, uint32_t ns) {
+    uint32_t done = 0;
+    long long t0 = 0;
+    for (;;) {
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+            : "=r"(done)
+            : "r"(smem_u32(bar)), "r"(parity)
+            : "memory");
+        if (done) return;
+        __nanosleep(ns);
+        const long long now = clock64();
+        if (t0 == 0) t0 = now;
+        else if (now - t0 > 20000000000ll) __trap();
+    }
+}
 // Generic-proxy shared-memory writes -> visible to the async proxy (tensor core operands).
 __device__ __forceinline__ void fence_proxy_async_smem() {
     asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");

@@ -2,28 +2,35 @@
 // Schur-complement updates on the tensor core (the batched Cholesky of the tensor-core
 // half-sweep; replaces batch_solve_into, solver.hpp:204-262, at FP32 tolerance).
 //
-// A CTA of 128 threads factors RPC systems side by side (persistent over groups of RPC rows,
-// 4/RPC CTAs per SM, 128 TMEM columns per system; RPC = 1 by default, 2 measured slower). Thread i owns TMEM lane i = row i of every
-// augmented matrix [A lower ; b^T] (rows < f: A, row f: b). Per 8-column block bc, for all
-// RPC systems at once (every barrier and MMA round trip is shared between them):
+// A CTA (persistent, 4 per SM, one system at a time in 128 TMEM columns) has 128 factor
+// threads and one back-substitution warp. Factor thread i owns TMEM lane i = row i of the
+// augmented matrix [A lower ; b^T] (rows < f: A, row f: b). Per 8-column block bc:
 //   1. every lane reads its 8 entries of the block column from TMEM (tcgen05.ld);
-//   2. the 8 diagonal-block rows go through shared memory; one thread per system (in
-//      different warps) factors the 8x8 block (rsqrt) and publishes L_cc and 1/diag;
-//   3. each lane below the block solves its own row against it (TRSM); the augmented row
-//      becomes y = L^{-1} b (forward substitution for free); L goes back to TMEM;
+//   2. the 8 diagonal-block rows go through shared memory; the lane of the first of them
+//      factors the 8x8 block (rsqrt, branch-free; the breakdown check follows) and publishes
+//      M = diag(1/L_cc) L_cc (row c of L_cc scaled by 1/L[c][c], diagonal = 1/L[c][c]);
+//   3. every lane at or below the block solves its own row against it (TRSM:
+//      L[c] = a[c] M[c][c] - sum_k<c L[k] M[c][k]; on a diagonal-block row this also yields
+//      its L_cc row); the augmented row becomes y = L^{-1} b (forward substitution for
+//      free); L goes back to TMEM;
 //   4. the panel P (rows below the block, K = 8) is split P = Ph + Pl (tf32 hi/lo) into two
-//      K-major 128B-swizzled tiles and one thread issues D -= Ph Ph^T + Ph Pl^T + Pl Ph^T
-//      as three negated tcgen05.mma (M = 128, N = round16(f), K = 8) per system.
-// Back substitution L^T x = y: the lanes dump L (packed lower) into the idle operand tiles
-// and one warp per system runs the column-oriented solve with the right-hand side in
-// registers. The next group's packed rows are bulk-copied into shared memory while the
-// current one is factored. All-zero A gives x = 0 (solver.hpp:215-220); a non-positive pivot
-// is reported with row, column and pivot (solver.hpp:230-235) and that row's x is zeroed.
+//      K-major tiles (no swizzle, 4 KB each) and one thread issues D -= Ph Ph^T + Ph Pl^T +
+//      Pl Ph^T as three negated tcgen05.mma (M = 128, N = round16(f), K = 8).
+// Warps whose rows all lie above the current block skip its TMEM traffic (upper part).
+// Back substitution L^T x = y: the factor threads dump L and y (panel-blocked like the input,
+// kernels.cuh) into a shared buffer and hand it to the back-substitution warp (mbarriers
+// lfull / lfree), which solves it with the right-hand side in registers while the factor
+// threads fill TMEM with the next system (its packed rows were bulk-copied into shared
+// memory during the factorization: two 16-byte loads per lane and block).
+// All-zero A gives x = 0 (solver.hpp:215-220); a non-positive pivot is reported with row,
+// column and pivot (solver.hpp:230-235) and that row's x is zeroed.
 #include <cuda_runtime.h>
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdio>
 #include <cstdlib>
+#include <vector>
 
 #include "kernels.cuh"
 #include "tc_common.cuh"
@@ -32,21 +39,28 @@ namespace alsk {
 namespace {
 using namespace tc;
 
-constexpr int TS_THREADS = 128;
-constexpr int TILE_BYTES = 128 * 128;      // one K-major SW128 operand tile: 128 rows x 128 B (K=8 used)
+constexpr int TS_FACTOR = 128;              // factor threads (thread i <-> TMEM lane i)
+constexpr int TS_THREADS = TS_FACTOR + 32;  // + the back-substitution warp
+constexpr int BS_WARP = TS_FACTOR / 32;
+constexpr uint32_t BAR_FACTOR = 1;          // named barrier of the factor threads
+// K = 8 panel tile, K-major without swizzle: core matrices of 8 rows x 16 bytes; the two
+// K halves of a row group are LBO = 128 bytes apart, row groups SBO = 256 bytes apart
+constexpr int PT_BYTES = 4096;
+constexpr uint32_t PT_LBO = 128, PT_SBO = 256;
+constexpr int TS_PROF_SLOTS = 12;
 
-template <int RPC>
 struct TsPlan {
-    int pks, rowbuf_bytes;
-    size_t tiles, rowbuf, misc, total;
+    int pks;
+    size_t rowbuf, lbuf, vec, blk, bars, total;
     __host__ __device__ explicit TsPlan(int f) {
         pks = static_cast<int>(packed_stride(f));
-        rowbuf_bytes = pks * 4;
-        tiles = 0;                                          // RPC x (Ph, Pl)
-        rowbuf = static_cast<size_t>(RPC) * 2 * TILE_BYTES;  // RPC packed rows
-        misc = rowbuf + static_cast<size_t>(RPC) * ((rowbuf_bytes + 127) & ~127);
-        // per system: blk[64] ys[128] xs[128] dinv[128]; flags; 2 mbarriers + tmem slot
-        total = misc + static_cast<size_t>(RPC) * (64 + 128 * 3 + 4) * 4 + 64 + 1024;
+        const size_t pkb = (static_cast<size_t>(pks) * 4 + 127) & ~static_cast<size_t>(127);
+        rowbuf = 2 * PT_BYTES;  // Ph at 0, Pl at PT_BYTES
+        lbuf = rowbuf + pkb;    // L and y of the system handed to the back substitution
+        vec = lbuf + pkb;       // dinv[2][128]
+        blk = vec + 2 * 128 * 4;  // 8x8 block, flags, meta
+        bars = blk + 64 * 4 + 32;
+        total = bars + 8 * 8 + 1024;  // mbarriers + TMEM slot, 1 KB alignment slack
     }
 };
 
@@ -76,186 +90,224 @@ __device__ __forceinline__ void expect_tx(uint64_t* bar, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
                  : "memory");
 }
+// barrier over `threads` threads of barrier `id`, returning the OR of v over them
+__device__ __forceinline__ bool bar_red_or(uint32_t id, uint32_t threads, bool v) {
+    uint32_t r;
+    asm volatile(
+        "{\n .reg .pred p, q;\n setp.ne.u32 q, %1, 0;\n bar.red.or.pred p, %2, %3, q;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(r)
+        : "r"(static_cast<uint32_t>(v)), "r"(id), "r"(threads)
+        : "memory");
+    return r != 0;
+}
 __device__ __forceinline__ float rna_tf32(float x) { return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xFFFFE000u); }
+// panel tile descriptor starting at row `row` (a multiple of 8)
+__device__ __forceinline__ uint64_t pt_desc(uint32_t tile, int row) {
+    uint64_t d = 0;
+    d |= static_cast<uint64_t>(((tile + (row >> 3) * PT_SBO) >> 4) & 0x3FFFu);
+    d |= static_cast<uint64_t>((PT_LBO >> 4) & 0x3FFFu) << 16;
+    d |= static_cast<uint64_t>((PT_SBO >> 4) & 0x3FFFu) << 32;
+    d |= 1ull << 46;  // descriptor version (Blackwell); layout bits 61-63 = 0: no swizzle
+    return d;
+}
+// D[:, col .. col+n) -= Ph Ph^T + Ph Pl^T + Pl Ph^T restricted to B rows col .. col+n
+__device__ __forceinline__ void schur_mma(uint32_t tmem, uint32_t ph, uint32_t pl, int col, int n) {
+    const uint32_t id = idesc_tf32(128, n) | (1u << 13);  // negate A: D -= A B^T
+    const uint64_t ah = pt_desc(ph, 0), al = pt_desc(pl, 0), bh = pt_desc(ph, col), bl = pt_desc(pl, col);
+    mma_tf32(tmem + col, ah, bh, id, 1u);
+    mma_tf32(tmem + col, ah, bl, id, 1u);
+    mma_tf32(tmem + col, al, bh, id, 1u);
+}
 
-struct SysSmem {  // per-system scratch in shared memory
-    float* blk;   // 8x8 diagonal block (row-major), then L_cc
-    float* ys;    // y = L^{-1} b
-    float* xs;    // x
-    float* dinv;  // 1 / L[c][c]
-    int* flags;   // [0] breakdown column + 1, [1] pivot bits
-};
-
-template <int RPC>
-__global__ void __launch_bounds__(TS_THREADS, 4 / RPC)
+// PROF: clock64() per phase, thread 0 (slots 0-7) and the back-substitution warp's lane 0
+// (8-9), into prof[blockIdx.x * TS_PROF_SLOTS + slot] (ALSK_TS_PROF=1).
+template <bool PROF>
+__global__ void __launch_bounds__(TS_THREADS, 4)
 tc_solve_kernel(const float* __restrict__ packed, int64_t count, int f, float* __restrict__ out_x,
                 unsigned long long* __restrict__ min_row, int32_t* __restrict__ column,
-                double* __restrict__ pivot, int64_t status_base) {
+                double* __restrict__ pivot, int64_t status_base, long long* __restrict__ prof,
+                uint32_t sleep_ns, uint32_t opts) {
+    long long pcy[TS_PROF_SLOTS] = {};
+    long long tq = PROF ? clock64() : 0;
+    const long long tstart = tq;
+    auto lap = [&](int slot) {
+        if constexpr (PROF) {
+            const long long now = clock64();
+            pcy[slot] += now - tq;
+            tq = now;
+        }
+    };
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw = smem_u32(smem_raw);
     uint8_t* base = smem_raw + (((raw + 1023u) & ~1023u) - raw);
-    constexpr int TS_TMEM_COLS = 128 * RPC;
-    const TsPlan<RPC> P(f);
-    const int rbb = (P.rowbuf_bytes + 127) & ~127;
-    SysSmem ss[RPC];
-    uint8_t* Ph[RPC];
-    uint8_t* Pl[RPC];
-    float* rowbuf[RPC];
-    {
-        float* m = reinterpret_cast<float*>(base + P.misc);
-#pragma unroll
-        for (int r = 0; r < RPC; ++r) {
-            Ph[r] = base + P.tiles + static_cast<size_t>(r) * 2 * TILE_BYTES;
-            Pl[r] = Ph[r] + TILE_BYTES;
-            rowbuf[r] = reinterpret_cast<float*>(base + P.rowbuf + static_cast<size_t>(r) * rbb);
-            ss[r].blk = m;
-            ss[r].ys = m + 64;
-            ss[r].xs = m + 192;
-            ss[r].dinv = m + 320;
-            ss[r].flags = reinterpret_cast<int*>(m + 448);
-            m += 452;
-        }
-    }
-    uint64_t* bars = reinterpret_cast<uint64_t*>(base + P.misc + static_cast<size_t>(RPC) * 452 * 4 + 8 * 0);
-    bars = reinterpret_cast<uint64_t*>((reinterpret_cast<uintptr_t>(bars) + 7) & ~static_cast<uintptr_t>(7));
-    uint64_t* load_bar = bars;
-    uint64_t* mma_bar = bars + 1;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2);
+    const TsPlan P(f);
+    uint8_t* Ph = base;
+    uint8_t* Pl = base + PT_BYTES;
+    float* rowbuf = reinterpret_cast<float*>(base + P.rowbuf);
+    float* lbuf = reinterpret_cast<float*>(base + P.lbuf);
+    float* dinvb = reinterpret_cast<float*>(base + P.vec);  // [2][128]: 1 / L[c][c] of the systems in flight
+    float* blk = reinterpret_cast<float*>(base + P.blk);     // 8x8 diagonal block, then M
+    int* flags = reinterpret_cast<int*>(blk + 64);         // [0] breakdown column + 1, [1] pivot bits
+    int* meta = flags + 4;                                 // [0] 1: system handed to the back substitution
+    uint64_t* bars = reinterpret_cast<uint64_t*>(base + P.bars);
+    uint64_t* load_bar = bars;  // packed rows of the next system landed
+    uint64_t* mma_bar = bars + 1;  // Schur update done (tiles free, trailing columns final)
+    uint64_t* lfull = bars + 2;    // L / y / 1/diag of a system ready for the back substitution
+    uint64_t* lfree = bars + 3;    // back substitution done with them
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 4);
 
-    const int i = threadIdx.x;  // matrix row == TMEM lane
+    const int i = threadIdx.x;
     const int warp = i >> 5, lane = i & 31;
     const int nbc = (f + 7) >> 3;
     const int N = (f + 15) & ~15;
-    const uint32_t idesc_neg = idesc_tf32(128, N) | (1u << 13);  // D -= A * B^T
-    const uint32_t row_bytes = static_cast<uint32_t>(P.rowbuf_bytes);
-    const int64_t ngroups = (count + RPC - 1) / RPC;
 
-    if (warp == 0) tmem_alloc<TS_TMEM_COLS>(tmem_slot);
+    if (warp == 0) tmem_alloc<128>(tmem_slot);
     if (i == 0) {
         mbar_init(load_bar, 1);
         mbar_init(mma_bar, 1);
+        mbar_init(lfull, 1);
+        mbar_init(lfree, 1);
         fence_barrier_init();
     }
-    for (int t = i; t < RPC * 2 * TILE_BYTES / 16; t += TS_THREADS)
-        reinterpret_cast<float4*>(base + P.tiles)[t] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int t = i; t < 2 * PT_BYTES / 16; t += TS_THREADS)
+        reinterpret_cast<float4*>(base)[t] = make_float4(0.f, 0.f, 0.f, 0.f);
     fence_proxy_async_smem();
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
-    const uint32_t tlane = tmem + (static_cast<uint32_t>(warp * 32) << 16);
-    uint32_t load_phase = 0, mma_phase = 0;
 
-    auto issue_load = [&](int64_t g) {  // thread 0: bulk-copy the group's packed rows
-        const int64_t r0 = g * RPC;
-        const int nr = static_cast<int>(std::min<int64_t>(RPC, count - r0));
-        expect_tx(load_bar, row_bytes * static_cast<uint32_t>(nr));
-        for (int r = 0; r < nr; ++r)
-            bulk_g2s(smem_u32(base + P.rowbuf) + r * rbb, packed + (r0 + r) * P.pks, row_bytes, load_bar);
-    };
-    int64_t g = blockIdx.x;
-    if (i == 0 && g < ngroups) issue_load(g);
-    // row i's operand slots in the K-major tiles (two 16-byte chunks, 128B swizzle)
-    const uint32_t prow = static_cast<uint32_t>((i >> 3) * 1024 + (i & 7) * 128);
-    const uint32_t pc0 = prow + ((0u ^ (i & 7)) << 4), pc1 = prow + ((1u ^ (i & 7)) << 4);
-
-    // fill TMEM with my row of each system of group gg (lower part; row f = b); nz[r] flags a
-    // nonzero A entry in my row
-    auto fill = [&](int64_t gg, int (&nz)[RPC]) {
-        mbar_wait(load_bar, load_phase);
-        load_phase ^= 1u;
-        const int64_t rr0 = gg * RPC;
+    if (warp == BS_WARP) {
+        // ---------------- back substitution L^T x = y, one system at a time ----------------
+        uint32_t t = 0;
+        for (int64_t g = blockIdx.x; g < count; g += gridDim.x, ++t) {
+            mbar_wait_sleep(lfull, t & 1u, 256);  // long wait: sleep, leave the issue slots to the factor warps
+            lap(9);
+            if (meta[0]) {
+                const float* dinv = dinvb + 128 * (t & 1u);
+                constexpr int G = 4;  // 128 / 32 values per lane
+                // lane j's cells of row ii of the panel-blocked dump sit at lb[g] + 8 ii
+                int lb[G];
+                float yv[G];
 #pragma unroll
-        for (int r = 0; r < RPC; ++r) {
-            const bool exists = rr0 + r < count;
-            nz[r] = 0;
-            for (int c0 = 0; c0 < N; c0 += 8) {
-                float v[8];
+                for (int gq = 0; gq < G; ++gq) {
+                    const int j = min(gq * 32 + lane, f - 1);
+                    lb[gq] = static_cast<int>(pb_index(f, 0, j));
+                    yv[gq] = gq * 32 + lane < f ? lbuf[lb[gq] + 8 * f] : 0.f;  // y = row f
+                }
 #pragma unroll
-                for (int q = 0; q < 8; ++q) {
-                    const int j = c0 + q;
-                    float t = 0.f;
-                    if (exists) {
-                        if (i < f && j <= i) {
-                            t = rowbuf[r][i * (i + 1) / 2 + j];
-                            nz[r] |= t != 0.f;
-                        } else if (i == f && j < f) {
-                            t = rowbuf[r][f * (f + 1) / 2 + j];
+                for (int gq = G - 1; gq >= 0; --gq) {
+                    for (int s = 31; s >= 0; --s) {
+                        const int ii = gq * 32 + s;
+                        if (ii >= f) continue;  // uniform
+                        const float xi = __shfl_sync(0xffffffffu, yv[gq], s) * dinv[ii];
+                        if (lane == s) yv[gq] = xi;
+#pragma unroll
+                        for (int gg = 0; gg <= gq; ++gg) {
+                            const int j = gg * 32 + lane;
+                            if (j < ii) yv[gg] = fmaf(-lbuf[lb[gg] + 8 * ii], xi, yv[gg]);
                         }
                     }
-                    v[q] = t;
                 }
-                tmem_st8(tlane + r * 128 + c0, v);
-            }
-        }
-        tmem_st_wait();
-    };
-    int nzr[RPC];
-    if (g < ngroups) fill(g, nzr);
-    for (; g < ngroups; g += gridDim.x) {
-        const int64_t row0 = g * RPC;
-        bool active[RPC];
+                float* x = out_x + g * f;
 #pragma unroll
-        for (int r = 0; r < RPC; ++r) {
-            active[r] = __syncthreads_or(nzr[r]) != 0;  // all-zero A: x = 0 (solver.hpp:215-220)
-            if (row0 + r < count && !active[r]) {
-                if (i < f) out_x[(row0 + r) * f + i] = 0.f;
-                if (i == 0) column[row0 + r] = 0;
+                for (int gq = 0; gq < G; ++gq) {
+                    const int j = gq * 32 + lane;
+                    if (j < f) x[j] = yv[gq];
+                }
+                if (lane == 0) column[g] = 0;
             }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(lfree);
+            lap(8);
         }
-        tc_fence_before();
-        __syncthreads();
-        if (i == 0 && g + gridDim.x < ngroups) issue_load(g + gridDim.x);  // rowbufs are free
-
-        for (int bc = 0; bc < nbc; ++bc) {
-            const int r0 = 8 * bc;
-            bool any = false;
+    } else {
+        // ---------------- factor threads ----------------
+        const uint32_t tlane = tmem + (static_cast<uint32_t>(warp * 32) << 16);
+        // last row of my warp: TMEM blocks right of it are the upper part for the whole warp
+        // (never read), so the warp skips their loads and stores
+        const int wtop = 32 * warp + 31;
+        const uint32_t row_bytes = static_cast<uint32_t>(P.pks) * 4;
+        const uint32_t sPh = smem_u32(Ph), sPl = smem_u32(Pl);
+        // row i's two 16-byte K chunks in the panel tiles
+        const uint32_t pc0 = static_cast<uint32_t>((i >> 3) * PT_SBO + (i & 7) * 16), pc1 = pc0 + PT_LBO;
+        uint32_t ph_load = 0, ph_mma = 0;
+        auto issue_load = [&](int64_t gg) {  // thread 0: bulk-copy a system's packed row
+            expect_tx(load_bar, row_bytes);
+            bulk_g2s(smem_u32(rowbuf), packed + gg * P.pks, row_bytes, load_bar);
+        };
+        // my row of the system in rowbuf into TMEM (panel-blocked; row f = b); nz: a nonzero
+        // A entry in my row
+        auto fill = [&](int& nz) {
+            mbar_wait_sleep(load_bar, ph_load, sleep_ns);
+            ph_load ^= 1u;
+            uint32_t bits = 0;
+            for (int b = 0; b < nbc && 8 * b <= wtop; ++b) {
+                float v[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+                if (i >= 8 * b && i <= f) {
+                    const float4* src = reinterpret_cast<const float4*>(rowbuf + pb_block(f, b) + 8 * (i - 8 * b));
+                    const float4 u = src[0], w = src[1];
+                    v[0] = u.x, v[1] = u.y, v[2] = u.z, v[3] = u.w, v[4] = w.x, v[5] = w.y, v[6] = w.z, v[7] = w.w;
 #pragma unroll
-            for (int r = 0; r < RPC; ++r) any |= active[r];
-            if (!any) break;
+                    for (int q = 0; q < 8; ++q) bits |= __float_as_uint(v[q]) << 1;  // +-0 -> 0
+                }
+                tmem_st8(tlane + 8 * b, v);
+            }
+            nz = i < f && bits != 0;
+            tmem_st_wait();
+        };
+        int64_t g = blockIdx.x;
+        if (i == 0 && g < count) issue_load(g);
+        int nz = 0;
+        if (g < count) fill(nz);
+        lap(6);
+        uint32_t t = 0;
+        for (; g < count; g += gridDim.x, ++t) {
+            float* dinv = dinvb + 128 * (t & 1u);
+            tc_fence_before();
+            bool active = bar_red_or(BAR_FACTOR, TS_FACTOR, nz != 0);  // all-zero A: x = 0 (solver.hpp:215-220)
             tc_fence_after();
-            float a[RPC][8];
-#pragma unroll
-            for (int r = 0; r < RPC; ++r) tmem_ld8(tlane + r * 128 + r0, a[r]);
-            tmem_ld_wait();
-            // (1) diagonal rows -> shared memory; the block is factored by a lane of the warp
-            //     that holds those rows (a warp sync suffices: the rest of the CTA waits at the
-            //     barrier after the factorization)
-            const int dwarp = r0 >> 5;
-            if (i >= r0 && i < r0 + 8) {
-#pragma unroll
-                for (int r = 0; r < RPC; ++r) {
-                    *reinterpret_cast<float4*>(&ss[r].blk[(i - r0) * 8]) = make_float4(a[r][0], a[r][1], a[r][2], a[r][3]);
-                    *reinterpret_cast<float4*>(&ss[r].blk[(i - r0) * 8 + 4]) = make_float4(a[r][4], a[r][5], a[r][6], a[r][7]);
-                }
+            if (i == 0 && g + gridDim.x < count) issue_load(g + gridDim.x);  // rowbuf is free
+            if (!active) {
+                if (i < f) out_x[g * f + i] = 0.f;
+                if (i == 0) column[g] = 0;
             }
-            if (warp == dwarp) __syncwarp();
-#pragma unroll
-            for (int r = 0; r < RPC; ++r) {
-                if (i != 32 * dwarp + ((r0 & 31) + 8 * r) % 32 || !active[r]) continue;
-                float* blk = ss[r].blk;
-                float l[8][8];
-#pragma unroll
-                for (int q = 0; q < 8; ++q) {
-                    const float4 u = *reinterpret_cast<const float4*>(&blk[q * 8]);
-                    const float4 w = *reinterpret_cast<const float4*>(&blk[q * 8 + 4]);
-                    l[q][0] = u.x, l[q][1] = u.y, l[q][2] = u.z, l[q][3] = u.w;
-                    l[q][4] = w.x, l[q][5] = w.y, l[q][6] = w.z, l[q][7] = w.w;
+            lap(10);
+            for (int bc = 0; active && bc < nbc; ++bc) {
+                const int r0 = 8 * bc;
+                const bool wlive = wtop >= r0;  // warp-uniform: some row of my warp at or below the block
+                tc_fence_after();
+                float a[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+                if (wlive) {
+                    tmem_ld8(tlane + r0, a);
+                    tmem_ld_wait();
                 }
-                int bad = 0;
-                float badv = 0.f;
+                // (1) diagonal rows -> shared memory; the lane of row r0 factors the block (a
+                //     warp sync suffices: the rest of the CTA waits at the barrier below)
+                if (i >= r0 && i < r0 + 8) {
+                    *reinterpret_cast<float4*>(&blk[(i - r0) * 8]) = make_float4(a[0], a[1], a[2], a[3]);
+                    *reinterpret_cast<float4*>(&blk[(i - r0) * 8 + 4]) = make_float4(a[4], a[5], a[6], a[7]);
+                }
+                if (warp == (r0 >> 5)) __syncwarp();
+                lap(0);
+                if (i == r0) {
+                    float l[8][8];
 #pragma unroll
-                for (int c = 0; c < 8; ++c) {
-                    const float d = l[c][c];
-                    const bool live = !bad && r0 + c < f;
-                    if (live && !(d > 0.f)) {
-                        bad = r0 + c + 1;
-                        badv = d;
+                    for (int q = 0; q < 8; ++q) {
+                        const float4 u = *reinterpret_cast<const float4*>(&blk[q * 8]);
+                        const float4 w = *reinterpret_cast<const float4*>(&blk[q * 8 + 4]);
+                        l[q][0] = u.x, l[q][1] = u.y, l[q][2] = u.z, l[q][3] = u.w;
+                        l[q][4] = w.x, l[q][5] = w.y, l[q][6] = w.z, l[q][7] = w.w;
                     }
-                    const bool ok = live && d > 0.f;
-                    const float ic = ok ? rsqrtf(d) : 0.f;
-                    ss[r].dinv[r0 + c] = ic;
-                    if (ok) {
+                    // branch-free right-looking 8x8 Cholesky; a non-positive pivot poisons what
+                    // follows it, which the check below discards with the whole system
+                    float piv[8], dv[8];
+#pragma unroll
+                    for (int c = 0; c < 8; ++c) {
+                        const float d = l[c][c];
+                        piv[c] = d;
+                        const float ic = rsqrtf(d);
+                        dv[c] = ic;
                         l[c][c] = d * ic;
 #pragma unroll
                         for (int q = c + 1; q < 8; ++q) l[q][c] *= ic;
@@ -264,65 +316,61 @@ tc_solve_kernel(const float* __restrict__ packed, int64_t count, int f, float* _
 #pragma unroll
                             for (int p = c + 1; p <= q; ++p) l[q][p] = fmaf(-l[q][c], l[p][c], l[q][p]);
                     }
-                }
+                    int bad = 0;
+                    float badv = 0.f;
 #pragma unroll
-                for (int q = 0; q < 8; ++q) {
-                    *reinterpret_cast<float4*>(&blk[q * 8]) = make_float4(l[q][0], l[q][1], l[q][2], l[q][3]);
-                    *reinterpret_cast<float4*>(&blk[q * 8 + 4]) = make_float4(l[q][4], l[q][5], l[q][6], l[q][7]);
-                }
-                ss[r].flags[0] = bad;
-                ss[r].flags[1] = __float_as_int(badv);
-            }
-            __syncthreads();
+                    for (int c = 7; c >= 0; --c)  // first real column with a non-positive pivot
+                        if (r0 + c < f && !(piv[c] > 0.f)) {
+                            bad = r0 + c + 1;
+                            badv = piv[c];
+                        }
+                    // M = diag(1/L_cc) L_cc, rows of padding columns zero
 #pragma unroll
-            for (int r = 0; r < RPC; ++r) {
-                if (active[r] && ss[r].flags[0]) {  // breakdown (uniform)
-                    const int64_t row = row0 + r;
-                    if (i == 0) {
-                        column[row] = ss[r].flags[0];
-                        pivot[row] = static_cast<double>(__int_as_float(ss[r].flags[1]));
-                        atomicMin(min_row, static_cast<unsigned long long>(status_base + row));
+                    for (int c = 0; c < 8; ++c) {
+                        const bool real = r0 + c < f;  // padding rows of M stay exactly zero
+                        float m[8];
+#pragma unroll
+                        for (int k = 0; k < 8; ++k) m[k] = !real ? 0.f : (k < c ? l[c][k] * dv[c] : (k == c ? dv[c] : 0.f));
+                        *reinterpret_cast<float4*>(&blk[c * 8]) = make_float4(m[0], m[1], m[2], m[3]);
+                        *reinterpret_cast<float4*>(&blk[c * 8 + 4]) = make_float4(m[4], m[5], m[6], m[7]);
+                        dinv[r0 + c] = dv[c];
                     }
-                    if (i < f) out_x[row * f + i] = 0.f;
-                    active[r] = false;
+                    flags[0] = bad;
+                    flags[1] = __float_as_int(badv);
                 }
-            }
-            const bool update = bc + 1 < nbc;  // no trailing columns after the last block
-            const bool diag_row = i >= r0 && i < r0 + 8 && i < f;
-            const bool below = (i >= r0 + 8 && i < f) || (i == f && i >= r0);
-#pragma unroll
-            for (int r = 0; r < RPC; ++r) {
-                // (2) my row of L; lanes outside keep their entries (upper-part or padding
-                //     cells that are never read)
+                named_barrier(BAR_FACTOR, TS_FACTOR);
+                lap(1);
+                if (flags[0]) {  // breakdown (uniform)
+                    if (i == 0) {
+                        column[g] = flags[0];
+                        pivot[g] = static_cast<double>(__int_as_float(flags[1]));
+                        atomicMin(min_row, static_cast<unsigned long long>(status_base + g));
+                    }
+                    if (i < f) out_x[g * f + i] = 0.f;
+                    active = false;
+                    break;
+                }
+                const bool update = bc + 1 < nbc;  // no trailing columns after the last block
+                // (2) my row of L (rows at or below the block, including row f = y); lanes above
+                //     keep their entries (upper-part or padding cells that are never read)
                 float L[8];
 #pragma unroll
-                for (int c = 0; c < 8; ++c) L[c] = a[r][c];
-                const float* blk = ss[r].blk;
-                if (active[r] && diag_row) {
-                    const float4 u = *reinterpret_cast<const float4*>(&blk[(i - r0) * 8]);
-                    const float4 w = *reinterpret_cast<const float4*>(&blk[(i - r0) * 8 + 4]);
-                    const float v[8] = {u.x, u.y, u.z, u.w, w.x, w.y, w.z, w.w};
-#pragma unroll
-                    for (int c = 0; c < 8; ++c) L[c] = (c <= i - r0) ? v[c] : 0.f;
-                } else if (active[r] && below) {
+                for (int c = 0; c < 8; ++c) L[c] = a[c];
+                if (i >= r0 && i <= f) {
 #pragma unroll
                     for (int c = 0; c < 8; ++c) {
                         const float4 u = *reinterpret_cast<const float4*>(&blk[c * 8]);
                         const float4 w = *reinterpret_cast<const float4*>(&blk[c * 8 + 4]);
-                        const float lc[8] = {u.x, u.y, u.z, u.w, w.x, w.y, w.z, w.w};
-                        float s = a[r][c];
+                        const float mc[8] = {u.x, u.y, u.z, u.w, w.x, w.y, w.z, w.w};
+                        float s = a[c] * mc[c];
 #pragma unroll
-                        for (int k = 0; k < c; ++k) s = fmaf(-L[k], lc[k], s);
-                        L[c] = (r0 + c < f) ? s * ss[r].dinv[r0 + c] : 0.f;
+                        for (int k = 0; k < c; ++k) s = fmaf(-L[k], mc[k], s);
+                        L[c] = (i - r0 >= c || i == f) ? s : 0.f;  // diagonal-block rows: lower part
                     }
                 }
-                tmem_st8(tlane + r * 128 + r0, L);  // .sync.aligned: every lane of the warp stores
-                if (active[r] && i == f) {
-#pragma unroll
-                    for (int c = 0; c < 8; ++c)
-                        if (r0 + c < f) ss[r].ys[r0 + c] = L[c];
-                }
-                if (update && active[r]) {
+                if (wlive) tmem_st8(tlane + r0, L);  // .sync.aligned: every lane of the warp stores
+                lap(2);
+                if (update) {
                     // panel operand: rows below the block only (factored rows contribute nothing)
                     float h[8], lo[8];
 #pragma unroll
@@ -331,135 +379,125 @@ tc_solve_kernel(const float* __restrict__ packed, int64_t count, int f, float* _
                         h[c] = rna_tf32(pv);
                         lo[c] = rna_tf32(pv - h[c]);
                     }
-                    *reinterpret_cast<float4*>(Ph[r] + pc0) = make_float4(h[0], h[1], h[2], h[3]);
-                    *reinterpret_cast<float4*>(Ph[r] + pc1) = make_float4(h[4], h[5], h[6], h[7]);
-                    *reinterpret_cast<float4*>(Pl[r] + pc0) = make_float4(lo[0], lo[1], lo[2], lo[3]);
-                    *reinterpret_cast<float4*>(Pl[r] + pc1) = make_float4(lo[4], lo[5], lo[6], lo[7]);
+                    if (wlive) {  // rows of a dead warp were zeroed when its rows left the panel
+                        *reinterpret_cast<float4*>(Ph + pc0) = make_float4(h[0], h[1], h[2], h[3]);
+                        *reinterpret_cast<float4*>(Ph + pc1) = make_float4(h[4], h[5], h[6], h[7]);
+                        *reinterpret_cast<float4*>(Pl + pc0) = make_float4(lo[0], lo[1], lo[2], lo[3]);
+                        *reinterpret_cast<float4*>(Pl + pc1) = make_float4(lo[4], lo[5], lo[6], lo[7]);
+                    }
+                    fence_proxy_async_smem();
                 }
+                tmem_st_wait();
+                tc_fence_before();
+                named_barrier(BAR_FACTOR, TS_FACTOR);
+                lap(3);
+                if (update) {
+                    if (i == 0) {
+                        tc_fence_after();
+                        schur_mma(tmem, sPh, sPl, 0, N);
+                        mma_commit(mma_bar);
+                    }
+                    mbar_wait_sleep(mma_bar, ph_mma, sleep_ns);
+                    ph_mma ^= 1u;
+                }
+                lap(4);
             }
-            if (update) fence_proxy_async_smem();
-            tmem_st_wait();
-            tc_fence_before();
-            __syncthreads();
-            if (update) {
-                bool issued = false;
-                if (i == 0) {
+            // hand the factor to the back-substitution warp: L (packed lower) into lbuf once
+            // it is done with the previous system
+            if (t > 0) mbar_wait_sleep(lfree, (t - 1) & 1u, sleep_ns);
+            if (active) {
+                for (int b = 0; b < nbc && 8 * b <= wtop; ++b) {
                     tc_fence_after();
-#pragma unroll
-                    for (int r = 0; r < RPC; ++r) {
-                        if (!active[r]) continue;
-                        const uint64_t dh = sdesc_sw128(smem_u32(Ph[r]), 16, 1024);
-                        const uint64_t dl = sdesc_sw128(smem_u32(Pl[r]), 16, 1024);
-                        const uint32_t d = tmem + r * 128;
-                        mma_tf32(d, dh, dh, idesc_neg, 1u);
-                        mma_tf32(d, dh, dl, idesc_neg, 1u);
-                        mma_tf32(d, dl, dh, idesc_neg, 1u);
-                        issued = true;
-                    }
-                    if (issued) mma_commit(mma_bar);
-                    else mbar_arrive(mma_bar);  // nothing to wait for; keep the phase count
-                }
-                mbar_wait(mma_bar, mma_phase);
-                mma_phase ^= 1u;
-            }
-        }
-        // ---- back substitution L^T x = y ----
-        // every lane dumps its row of L (columns 0..i) of each system from TMEM into a packed
-        // lower copy in that system's (now idle) operand tiles; warp r then runs system r's
-        // column-oriented solve with the right-hand side spread over its lanes
-        for (int c0 = 0; c0 < 8 * nbc; c0 += 8) {
-            tc_fence_after();
-            float lb[RPC][8];
-#pragma unroll
-            for (int r = 0; r < RPC; ++r) tmem_ld8(tlane + r * 128 + c0, lb[r]);
-            tmem_ld_wait();
-            if (i < f) {
-#pragma unroll
-                for (int r = 0; r < RPC; ++r) {
-                    if (!active[r]) continue;
-                    float* lpk = reinterpret_cast<float*>(Ph[r]);
-#pragma unroll
-                    for (int c = 0; c < 8; ++c)
-                        if (c0 + c <= i) lpk[i * (i + 1) / 2 + c0 + c] = lb[r][c];
-                }
-            }
-        }
-        __syncthreads();
-        // back substitution of system r by warp r, overlapped with the next group's TMEM fill
-        // by the other warps (each warp fills its own lanes once it is free); the barrier at
-        // the top of the next iteration orders the tiles' reuse
-#pragma unroll
-        for (int r = 0; r < RPC; ++r) {
-            if (warp != r || !active[r]) continue;
-            const float* lpk = reinterpret_cast<const float*>(Ph[r]);
-            const float* ys = ss[r].ys;
-            const float* dinv = ss[r].dinv;
-            constexpr int G = 4;  // 128 / 32 values per lane
-            float yv[G];
-#pragma unroll
-            for (int gq = 0; gq < G; ++gq) {
-                const int j = gq * 32 + lane;
-                yv[gq] = j < f ? ys[j] : 0.f;
-            }
-#pragma unroll
-            for (int gq = G - 1; gq >= 0; --gq) {
-                for (int t = 31; t >= 0; --t) {
-                    const int ii = gq * 32 + t;
-                    if (ii >= f) continue;  // uniform
-                    const float xi = __shfl_sync(0xffffffffu, yv[gq], t) * dinv[ii];
-                    if (lane == t) yv[gq] = xi;
-                    const float* lrow = lpk + ii * (ii + 1) / 2;
-#pragma unroll
-                    for (int gg = 0; gg <= gq; ++gg) {
-                        const int j = gg * 32 + lane;
-                        if (j < ii) yv[gg] = fmaf(-lrow[j], xi, yv[gg]);
+                    float lv[8];
+                    tmem_ld8(tlane + 8 * b, lv);
+                    tmem_ld_wait();
+                    if (i >= 8 * b && i <= f) {
+                        float4* dst = reinterpret_cast<float4*>(lbuf + pb_block(f, b) + 8 * (i - 8 * b));
+                        dst[0] = make_float4(lv[0], lv[1], lv[2], lv[3]);
+                        dst[1] = make_float4(lv[4], lv[5], lv[6], lv[7]);
                     }
                 }
             }
-            float* x = out_x + (row0 + r) * f;
-#pragma unroll
-            for (int gq = 0; gq < G; ++gq) {
-                const int j = gq * 32 + lane;
-                if (j < f) x[j] = yv[gq];
+            if (i == 0) meta[0] = active ? 1 : 0;
+            named_barrier(BAR_FACTOR, TS_FACTOR);
+            if (i == 0) mbar_arrive(lfull);
+            lap(5);
+            if (g + gridDim.x < count) {
+                tc_fence_after();
+                fill(nz);
             }
-            if (lane == 0) column[row0 + r] = 0;
+            lap(6);
         }
-        if (g + gridDim.x < ngroups) {
-            tc_fence_after();
-            fill(g + gridDim.x, nzr);
+    }
+    if constexpr (PROF) {
+        if (i == 0 || i == 32 * BS_WARP) {
+            pcy[7] = clock64() - tstart;
+            const int lo = i == 0 ? 0 : 8, hi = i == 0 ? 8 : 10;
+            for (int q = lo; q < hi; ++q) prof[blockIdx.x * TS_PROF_SLOTS + q] = pcy[q];
+            if (i == 0) {
+                prof[blockIdx.x * TS_PROF_SLOTS + 10] = pcy[10];
+                prof[blockIdx.x * TS_PROF_SLOTS + 11] = pcy[7];
+            }
         }
     }
     tc_fence_before();
     __syncthreads();
     if (warp == 0) {
         tc_fence_after();
-        tmem_dealloc<TS_TMEM_COLS>(tmem);
+        tmem_dealloc<128>(tmem);
     }
 }
 
-template <int RPC>
 void launch_solve(const float* packed, int64_t count, int f, float* x, const SolveStatus& st, int64_t status_off,
                   cudaStream_t s) {
-    const TsPlan<RPC> P(f);
-    ALSK_CUDA(cudaFuncSetAttribute(tc_solve_kernel<RPC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   static_cast<int>(P.total)));
-    const int64_t groups = (count + RPC - 1) / RPC;
-    const unsigned grid = static_cast<unsigned>(std::min<int64_t>(groups, static_cast<int64_t>(4 / RPC) * num_sms()));
-    tc_solve_kernel<RPC><<<grid, TS_THREADS, P.total, s>>>(packed, count, f, x, st.min_row, st.column + status_off,
-                                                           st.pivot + status_off, status_off);
+    const TsPlan P(f);
+    // at least 46 KB of shared memory per CTA: never more than 4 CTAs (4 x 128 TMEM columns)
+    // on an SM, so no CTA waits in tcgen05.alloc for another to finish
+    const int smem = static_cast<int>(std::max<size_t>(P.total, 46 * 1024));
+    const unsigned grid = static_cast<unsigned>(std::min<int64_t>(count, 4 * static_cast<int64_t>(num_sms())));
+    static const bool want_prof = std::getenv("ALSK_TS_PROF") != nullptr;
+    // back-off of the factor threads' short waits (MMA completion, hand-off, loads)
+    static const uint32_t sleep_ns = [] {
+        const char* e = std::getenv("ALSK_TS_SLEEP");
+        return e ? static_cast<uint32_t>(std::atoi(e)) : 32u;
+    }();
+    const uint32_t opts = 0;
+    if (!want_prof) {
+        ALSK_CUDA(cudaFuncSetAttribute(tc_solve_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        tc_solve_kernel<false><<<grid, TS_THREADS, smem, s>>>(packed, count, f, x, st.min_row, st.column + status_off,
+                                                              st.pivot + status_off, status_off, nullptr, sleep_ns, opts);
+        ALSK_LAUNCHED();
+        return;
+    }
+    ALSK_CUDA(cudaFuncSetAttribute(tc_solve_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    DevBuf prof;
+    prof.alloc(sizeof(long long) * grid * TS_PROF_SLOTS, s);
+    ALSK_CUDA(cudaMemsetAsync(prof.as<void>(), 0, sizeof(long long) * grid * TS_PROF_SLOTS, s));
+    tc_solve_kernel<true><<<grid, TS_THREADS, smem, s>>>(packed, count, f, x, st.min_row, st.column + status_off,
+                                                         st.pivot + status_off, status_off, prof.as<long long>(), sleep_ns, opts);
     ALSK_LAUNCHED();
+    std::vector<long long> h(static_cast<size_t>(grid) * TS_PROF_SLOTS);
+    ALSK_CUDA(cudaMemcpyAsync(h.data(), prof.as<void>(), h.size() * sizeof(long long), cudaMemcpyDeviceToHost, s));
+    ALSK_CUDA(cudaStreamSynchronize(s));
+    double acc[TS_PROF_SLOTS] = {};
+    for (unsigned c = 0; c < grid; ++c)
+        for (int q = 0; q < TS_PROF_SLOTS; ++q) acc[q] += static_cast<double>(h[c * TS_PROF_SLOTS + q]);
+    for (double& v : acc) v /= static_cast<double>(count) * 1e3;
+    std::fprintf(stderr,
+                 "[ts-prof f=%d rows=%lld grid=%u] kcyc/system: diag %.2f potrf %.2f trsm %.2f panel %.2f mma %.2f "
+                 "handoff %.2f fill %.2f start %.2f | total %.2f | backsub %.2f bs-wait %.2f\n",
+                 f, static_cast<long long>(count), grid, acc[0], acc[1], acc[2], acc[3], acc[4], acc[5], acc[6],
+                 acc[10], acc[11], acc[8], acc[9]);
 }
 
 }  // namespace
 
 bool packed_solve(const float* packed, int64_t count, int f, float* x, const SolveStatus& st, int64_t status_off,
                   cudaStream_t s) {
-    static const bool tiles = std::getenv("ALSK_SOLVE_TILES") != nullptr;  // A/B switches for measurements
-    static const bool pairs = std::getenv("ALSK_SOLVE_PAIRS") != nullptr;
+    static const bool tiles = std::getenv("ALSK_SOLVE_TILES") != nullptr;  // A/B switch for measurements
     if (tiles || f < 8 || f > 127) return packed_solve_tiles(packed, count, f, x, st, status_off, s);
     if (count <= 0) return true;
-    if (pairs) launch_solve<2>(packed, count, f, x, st, status_off, s);
-    else launch_solve<1>(packed, count, f, x, st, status_off, s);
+    launch_solve(packed, count, f, x, st, status_off, s);
     return true;
 }
 

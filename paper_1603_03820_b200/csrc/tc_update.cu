@@ -1,9 +1,10 @@
-// Tensor-core half-sweep (ALSK_PREC_TF32X2): get_hermitian + get_bias on tcgen05 (kind::tf32,
-// two-term split), Cholesky + both triangular solves on the CUDA cores, one persistent CTA
-// per SM, nothing per-row materialised in HBM.
+// Tensor-core get_hermitian + get_bias (ALSK_PREC_TF32X2): tcgen05 kind::tf32 with a two-term
+// split, one persistent CTA per SM. Writes A_u (+ lambda n_u) and B_u either in the
+// get_hermitian layout (MODE_FULL) or lower-packed for the batched TMEM Cholesky solve of
+// tc_solve.cu (MODE_PACKED, the half-sweep path).
 //
-// Replaces, for this precision, the loop body of update_x (solver.hpp:336-344):
-// assemble_mo_rows (solver.hpp:99-157) followed by batch_solve_into (solver.hpp:204-262).
+// Replaces, for this precision, assemble_mo_rows (solver.hpp:99-157) in the loop body of
+// update_x (solver.hpp:336-344); batch_solve_into (solver.hpp:204-262) is tc_solve.cu.
 //
 // Arithmetic. The gathered rows are augmented with the rating, theta'_k = [theta_k, r_k]
 // (f+1 features), and every entry is split x = h + l, h = rna_tf32(x), l = rna_tf32(x - h).
@@ -17,9 +18,8 @@
 //
 // Warp roles (672 threads, 1 CTA per SM, rows j = blockIdx.x + t*gridDim.x):
 //   warps 0-7  : two epilogue groups of 4 warps (group g takes rows with t%2 == g). TMEM ->
-//                registers -> shared memory (segment sums, symmetrisation, lambda n_u) ->
-//                8x8 tiles in registers -> blocked right-looking Cholesky -> back
-//                substitution -> x_u.
+//                registers -> shared memory (segment sums) -> symmetrised A_u + lambda n_u
+//                and B_u rows written to HBM.
 //   warps 8-15 : split warps: read the staged rating-major rows, split tf32 hi/lo and
 //                write them transposed into the K-major operand tile (lane = rating), with
 //                zero padding of partial k-groups.
@@ -70,15 +70,13 @@ struct TcPlan {
     int f, sld, stages, nb, hls, rs, raw_bytes;
     int s_floats, grp_floats;
     size_t hl_off, ring_bytes, grp_bytes, bar_off, info_off, total;
-    // solve_scratch: the fused-solve epilogue also needs panel/diag/flags per group
-    __host__ __device__ TcPlan(int f_, int nb_, int stages_, int ldt, bool solve_scratch, int hls_)
+    __host__ __device__ TcPlan(int f_, int nb_, int stages_, int ldt, int hls_)
         : f(f_), stages(stages_), nb(nb_), hls(hls_) {
         rs = staging_stride(ldt);
         raw_bytes = (KC * rs * 4 + 127) & ~127;
         sld = (f + 1) | 1;  // >= f+1 columns (A and B); odd: row writes and column reads conflict-free
         s_floats = ((f + 1) * sld + 3) & ~3;  // keep the float4 panel 16-byte aligned
-        const int fp = 8 * nb;
-        grp_floats = solve_scratch ? ((s_floats + 8 * fp + 64 + fp + 8 + 3) & ~3) : s_floats;
+        grp_floats = s_floats;
         hl_off = (static_cast<size_t>(stages) * raw_bytes + 1023) & ~static_cast<size_t>(1023);  // UMMA atoms: 1 KB
         ring_bytes = hl_off + static_cast<size_t>(hls) * HL_BYTES;
         grp_bytes = static_cast<size_t>(grp_floats) * 4;
@@ -87,34 +85,6 @@ struct TcPlan {
         total = info_off + static_cast<size_t>(stages) * (KC * 4 + 16) + hls * 16 + 1024;  // + align slack
     }
 };
-
-__device__ __forceinline__ void tile_coords_colmajor(int t, int nb, int& bi, int& bj) {
-    int c = 0;
-    while (t >= nb - c) {
-        t -= nb - c;
-        ++c;
-    }
-    bj = c;
-    bi = c + t;
-}
-
-template <int LDT, bool NEG>
-__device__ __forceinline__ void outer_accumulate(float (&acc)[8][8], const float* buf, int cnt, int ia, int jb) {
-#pragma unroll 2
-    for (int kk = 0; kk < cnt; ++kk) {
-        const float* trow = buf + kk * LDT;
-        const float4 a0 = *reinterpret_cast<const float4*>(trow + ia);
-        const float4 a1 = *reinterpret_cast<const float4*>(trow + ia + 4);
-        const float4 b0 = *reinterpret_cast<const float4*>(trow + jb);
-        const float4 b1 = *reinterpret_cast<const float4*>(trow + jb + 4);
-        const float a[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
-        const float b[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
-#pragma unroll
-        for (int i = 0; i < 8; ++i)
-#pragma unroll
-            for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(NEG ? -a[i] : a[i], b[j], acc[i][j]);
-    }
-}
 
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
@@ -207,182 +177,22 @@ struct RowIter {  // the CTA's row sequence j = blockIdx.x + t * gridDim.x
     __device__ void next() { j += gridDim.x; }
 };
 
-// One epilogue group's Cholesky of the augmented tile set (rows < f: A lower; row f: B) and
-// the back substitution; x written to xrow. Mirrors fused_fp32.cu's blocked algorithm with
-// group-scoped named barriers. Returns the breakdown column+1 (0 = ok).
-template <int NB, int GT = 128>
-__device__ __forceinline__ void group_solve(float (&acc)[8][8], bool active, int bi, int bj, int e, int f,
-                                            float* lpk, float* panel, float* dblk, float* dinv, int* flags,
-                                            uint32_t bar_id, float* __restrict__ xrow, int32_t* col_out,
-                                            double* piv_out, unsigned long long* min_row, int64_t status_row,
-                                            bool prof, long long (&pc)[6]) {
-    constexpr int FP = 8 * NB;
-    const int ia = 8 * bi, jb = 8 * bj;
-    long long tq = prof ? clock64() : 0;
-    auto lap = [&](int slot) {
-        if (prof) {
-            const long long now = clock64();
-            pc[slot] += now - tq;
-            tq = now;
-        }
-    };
-    const int aug = f;
-    // all-zero A => x = 0 (solver.hpp:215-220)
-    int nz = 0;
-    if (active) {
-#pragma unroll
-        for (int ii = 0; ii < 8; ++ii)
-#pragma unroll
-            for (int jj = 0; jj < 8; ++jj)
-                if (ia + ii < f && jb + jj <= ia + ii) nz |= (acc[ii][jj] != 0.f);
-    }
-    if (e == 0) flags[2] = 0;
-    named_barrier(bar_id, GT);
-    if (nz) flags[2] = 1;
-    named_barrier(bar_id, GT);
-    if (!flags[2]) {
-        for (int i = e; i < f; i += GT) xrow[i] = 0.f;
-        if (e == 0) *col_out = 0;
-        named_barrier(bar_id, GT);
-        return;
-    }
-    const int nbc = (f + 7) >> 3;
-    for (int bc = 0; bc < nbc; ++bc) {
-        if (active && bi == bc && bj == bc) {
-            int bad = 0;
-#pragma unroll
-            for (int c = 0; c < 8; ++c) {
-                if (bad || 8 * bc + c >= f) continue;
-                const float d = acc[c][c];
-                if (!(d > 0.f)) {
-                    bad = 8 * bc + c + 1;
-                    flags[1] = __float_as_int(d);
-                    continue;
-                }
-                const float l = sqrtf(d), inv = 1.0f / l;
-                acc[c][c] = l;
-                dinv[8 * bc + c] = inv;
-#pragma unroll
-                for (int r = c + 1; r < 8; ++r) acc[r][c] *= inv;
-#pragma unroll
-                for (int r = c + 1; r < 8; ++r)
-#pragma unroll
-                    for (int q = c + 1; q <= r; ++q) acc[r][q] = fmaf(-acc[r][c], acc[q][c], acc[r][q]);
-            }
-            flags[0] = bad;
-#pragma unroll
-            for (int r = 0; r < 8; ++r)
-#pragma unroll
-                for (int c = 0; c < 8; ++c) dblk[r * 8 + c] = acc[r][c];
-        }
-        named_barrier(bar_id, GT);
-        lap(0);
-        if (flags[0]) {
-            if (e == 0) {
-                *col_out = flags[0];
-                *piv_out = static_cast<double>(__int_as_float(flags[1]));
-                atomicMin(min_row, static_cast<unsigned long long>(status_row));
-            }
-            for (int i = e; i < f; i += GT) xrow[i] = 0.f;
-            named_barrier(bar_id, GT);
-            if (e == 0) flags[0] = 0;
-            named_barrier(bar_id, GT);
-            return;
-        }
-        if (active && bj == bc && bi > bc) {
-#pragma unroll
-            for (int c = 0; c < 8; ++c) {
-                const float di = (8 * bc + c < f) ? dinv[8 * bc + c] : 0.f;
-#pragma unroll
-                for (int r = 0; r < 8; ++r) {
-                    float s = acc[r][c];
-#pragma unroll
-                    for (int k = 0; k < c; ++k) s = fmaf(-acc[r][k], dblk[c * 8 + k], s);
-                    acc[r][c] = s * di;
-                }
-            }
-#pragma unroll
-            for (int c = 0; c < 8; ++c) {
-                float4* dst = reinterpret_cast<float4*>(panel + c * FP + ia);
-                dst[0] = make_float4(acc[0][c], acc[1][c], acc[2][c], acc[3][c]);
-                dst[1] = make_float4(acc[4][c], acc[5][c], acc[6][c], acc[7][c]);
-            }
-        }
-        named_barrier(bar_id, GT);
-        lap(1);
-        if (active && bj > bc) outer_accumulate<FP, true>(acc, panel, 8, ia, jb);
-        lap(2);
-    }
-    if (e == 0) *col_out = 0;
-    // packed L (rows < f) and y (row aug) for the back substitution
-    float* yrow = lpk + f * (f + 1) / 2;
-    if (active) {
-#pragma unroll
-        for (int ii = 0; ii < 8; ++ii)
-#pragma unroll
-            for (int jj = 0; jj < 8; ++jj) {
-                const int i = ia + ii, j = jb + jj;
-                if (j >= f || j > i) continue;
-                if (i < f) lpk[i * (i + 1) / 2 + j] = acc[ii][jj];
-                else if (i == aug) yrow[j] = acc[ii][jj];
-            }
-    }
-    named_barrier(bar_id, GT);
-    if (e < 32) {
-        const int lane = e;
-        constexpr int G = (FP + 31) / 32;
-        float yv[G];
-#pragma unroll
-        for (int g = 0; g < G; ++g) {
-            const int j = g * 32 + lane;
-            yv[g] = j < f ? yrow[j] : 0.f;
-        }
-#pragma unroll
-        for (int g = G - 1; g >= 0; --g) {
-            for (int t = 31; t >= 0; --t) {
-                const int i = g * 32 + t;
-                if (i >= f) continue;
-                const float xi = __shfl_sync(0xffffffffu, yv[g], t) * dinv[i];
-                if (lane == t) yv[g] = xi;
-                const float* lrow = lpk + i * (i + 1) / 2;
-#pragma unroll
-                for (int gg = 0; gg <= g; ++gg) {
-                    const int j = gg * 32 + lane;
-                    if (j < i) yv[gg] = fmaf(-lrow[j], xi, yv[gg]);
-                }
-            }
-        }
-#pragma unroll
-        for (int g = 0; g < G; ++g) {
-            const int j = g * 32 + lane;
-            if (j < f) xrow[j] = yv[g];
-        }
-    }
-    named_barrier(bar_id, GT);  // lpk / dinv reused by the group's next row
-    lap(3);
-}
-
 __device__ __forceinline__ int64_t row_segments(int64_t n) {
     const int64_t nch = (n + KC - 1) / KC;
     return (nch + SEG_CHUNKS - 1) / SEG_CHUNKS;
 }
 
-// MODE_SOLVE: fused Cholesky + solves -> x rows. MODE_FULL: A (full, mirrored) + B rows
-// (get_hermitian layout). MODE_PACKED: lower-packed A then B, f(f+1)/2+f floats per row, for
-// the separate batched solve.
-enum { MODE_SOLVE = 0, MODE_FULL = 1, MODE_PACKED = 2 };
+// MODE_FULL: A (full, mirrored) + B rows (get_hermitian layout). MODE_PACKED: lower-packed A
+// then B, panel-blocked (packed_stride(f) floats per row, kernels.cuh), for the batched solve
+// (tc_solve.cu).
+enum { MODE_FULL = 1, MODE_PACKED = 2 };
 
 template <int NB, int MODE>
 __global__ void __launch_bounds__(NTHREADS, 1)
 tc_update_kernel(const float* __restrict__ theta, int ldt, const int64_t* __restrict__ row_ptr,
                  const int32_t* __restrict__ col_idx, const float* __restrict__ values, int64_t col_lo, int f,
-                 float lambda, int64_t rb, int64_t nrows, int stages, float* __restrict__ out_x,
-                 float* __restrict__ out_a, float* __restrict__ out_b, unsigned long long* __restrict__ min_row,
-                 int32_t* __restrict__ column, double* __restrict__ pivot, int64_t status_base,
-                 long long* __restrict__ prof, int hls) {
-    constexpr int FP = 8 * NB;
-    constexpr int NTILES = NB * (NB + 1) / 2;
-    static_assert(NTILES <= 128, "tile set must fit one 128-thread epilogue group");
+                 float lambda, int64_t rb, int64_t nrows, int stages, float* __restrict__ out_a,
+                 float* __restrict__ out_b, long long* __restrict__ prof, int hls) {
     // optional per-warp cycle accounting (ALSK_TC_PROF=1): pc[] slots per role, see launch_tc
     long long pc[6] = {0, 0, 0, 0, 0, 0};
     long long tp0 = 0;
@@ -392,7 +202,7 @@ tc_update_kernel(const float* __restrict__ theta, int ldt, const int64_t* __rest
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw_addr = smem_u32(smem_raw);
     uint8_t* base = smem_raw + (((raw_addr + 1023u) & ~1023u) - raw_addr);
-    const TcPlan P(f, NB, stages, ldt, MODE == MODE_SOLVE, hls);
+    const TcPlan P(f, NB, stages, ldt, hls);
     const int RAW = P.raw_bytes;
     const int HL_STAGES = hls;
     // augmented features per operand half; a multiple of 16 keeps every 16-column TMEM load of
@@ -637,18 +447,9 @@ tc_update_kernel(const float* __restrict__ theta, int ldt, const int64_t* __rest
         const int e = threadIdx.x & 127;  // TMEM lane = matrix row owned in the readback
         const uint32_t bar_id = 1 + g;
         float* S = grp0 + g * P.grp_floats;
-        float* panel = S + P.s_floats;
-        float* dblk = panel + 8 * FP;
-        float* dinv = dblk + 64;
-        int* flags = reinterpret_cast<int*>(dinv + FP);
         const int sld = P.sld;
         const uint32_t lane_base = static_cast<uint32_t>((warp & 3) * 32) << 16;
         const int nch16 = (f + 1 + 15) >> 4;  // 16-column TMEM chunks covering features 0..f
-        const bool active = e < NTILES;
-        int bi = 0, bj = 0;
-        if (active) tile_coords_colmajor(e, NB, bi, bj);
-        const int ia = 8 * bi, jb = 8 * bj;
-        if (MODE == MODE_SOLVE && e == 0) flags[0] = flags[1] = flags[2] = 0;  // scratch only in solve mode
         float* Srow = S + e * sld;
         uint32_t job = 0, use[2] = {0u, 0u};
         int t = 0;
@@ -661,11 +462,6 @@ tc_update_kernel(const float* __restrict__ theta, int ldt, const int64_t* __rest
                 continue;
             }
             const int64_t row = it.j;
-            float acc[8][8];
-#pragma unroll
-            for (int ii = 0; ii < 8; ++ii)
-#pragma unroll
-                for (int jj = 0; jj < 8; ++jj) acc[ii][jj] = 0.f;
             if (n > 0) {
                 for (uint32_t sg = 0; sg < nseg; ++sg, ++job) {
                     const uint32_t b = job & 1u;
@@ -709,56 +505,38 @@ tc_update_kernel(const float* __restrict__ theta, int ldt, const int64_t* __rest
                         a_out[idx] = v;
                     }
                     for (int j = e; j < f; j += 128) b_out[j] = 0.5f * (S[f * sld + j] + S[j * sld + f]);
-                    named_barrier(bar_id, 128);
-                    continue;
-                } else if constexpr (MODE == MODE_PACKED) {
-                    // one pass, warp-cooperative rows: lower row i of sym(S) (row f = B) is
-                    // contiguous in the packed output; S_ij reads are contiguous across lanes and
-                    // the transposed S_ji reads are conflict-free (odd row stride)
+                } else {
+                    // panel-blocked packed row (kernels.cuh): block b holds rows 8b..f x 8
+                    // columns; consecutive threads write consecutive floats, the transposed S_ji
+                    // reads are conflict-light (odd row stride)
                     float* pk = out_a + row * packed_stride(f);
-                    const int wq = e >> 5, ln = e & 31;
-                    for (int i = wq; i <= f; i += 4) {
-                        const int len = i < f ? i + 1 : f;
-                        float* dst = pk + i * (i + 1) / 2;  // row f starts at f(f+1)/2
-                        for (int j = ln; j < len; j += 32) {
-                            float v = 0.5f * (S[i * sld + j] + S[j * sld + i]);
-                            if (j == i) v += reg;
-                            dst[j] = v;
+                    const int nbk = (f + 7) >> 3;
+                    for (int bk = 0; bk < nbk; ++bk) {
+                        float* dst = pk + pb_block(f, bk);
+                        const int cnt = (f + 1 - 8 * bk) * 8;
+                        for (int q = e; q < cnt; q += 128) {
+                            const int i = 8 * bk + (q >> 3), j = 8 * bk + (q & 7);
+                            float v = 0.f;
+                            if (i < f ? j <= i : j < f) {
+                                v = 0.5f * (S[i * sld + j] + S[j * sld + i]);
+                                if (j == i) v += reg;
+                            }
+                            dst[q] = v;
                         }
                     }
-                    named_barrier(bar_id, 128);
-                    continue;
-                }
-                // fused solve: symmetrise in place, lower A (+ lambda n_u) and B in row f
-                if (e < f) {
-                    for (int j = 0; j < e; ++j) Srow[j] = 0.5f * (Srow[j] + S[j * sld + e]);
-                    Srow[e] += reg;
-                } else if (e == f) {
-                    for (int j = 0; j < f; ++j) Srow[j] = 0.5f * (Srow[j] + S[j * sld + f]);
                 }
                 named_barrier(bar_id, 128);
-#pragma unroll
-                for (int ii = 0; ii < 8; ++ii)
-#pragma unroll
-                    for (int jj = 0; jj < 8; ++jj) {
-                        const int i = ia + ii, j = jb + jj;
-                        if (active && j < f && (j <= i || i == f) && i <= f) acc[ii][jj] = S[i * sld + j];
-                    }
-                named_barrier(bar_id, 128);  // S becomes the packed-L scratch
                 TA(t2, 4);
+                continue;
             }
             if constexpr (MODE == MODE_FULL) {
                 float* a_out = out_a + row * static_cast<int64_t>(f) * f;
                 for (int idx = e; idx < f * f; idx += 128) a_out[idx] = 0.f;
                 for (int j = e; j < f; j += 128) out_b[row * static_cast<int64_t>(f) + j] = 0.f;
-            } else if constexpr (MODE == MODE_PACKED) {
+            } else {
                 const int pkn = static_cast<int>(packed_stride(f));
                 float* pk = out_a + row * static_cast<int64_t>(pkn);
                 for (int idx = e; idx < pkn; idx += 128) pk[idx] = 0.f;
-            } else {
-                group_solve<NB>(acc, active, bi, bj, e, f, S, panel, dblk, dinv, flags, bar_id,
-                                out_x + row * static_cast<int64_t>(f), column + row, pivot + row, min_row,
-                                status_base + row, prof != nullptr, pc);
             }
         }
     }
@@ -784,12 +562,12 @@ void launch_tc(const DevCsr& r, const float* theta, int64_t theta_rows, int f, i
     // deepest operand ring first (the MMA is fed by the split through it), then the staging ring
     int hls = HL_STAGES_MAX, stages = 6;
     for (;;) {
-        while (stages > 2 && TcPlan(f, NB, stages, ldt, MODE == MODE_SOLVE, hls).total > 227 * 1024) --stages;
+        while (stages > 2 && TcPlan(f, NB, stages, ldt, hls).total > 227 * 1024) --stages;
         if (stages >= 3 || hls == 2) break;
         --hls;
         stages = 6;
     }
-    const TcPlan P(f, NB, stages, ldt, MODE == MODE_SOLVE, hls);
+    const TcPlan P(f, NB, stages, ldt, hls);
     auto k = tc_update_kernel<NB, MODE>;
     ALSK_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(P.total)));
     const int64_t nrows = re - rb;
@@ -801,8 +579,7 @@ void launch_tc(const DevCsr& r, const float* theta, int64_t theta_rows, int f, i
         ALSK_CUDA(cudaMemsetAsync(prof.as<void>(), 0, sizeof(long long) * grid * NWARPS * 6, s));
     }
     k<<<grid, NTHREADS, P.total, s>>>(theta, ldt, r.row_ptr, r.col_idx, r.values, r.col_offset, f, lambda, rb, nrows, stages,
-                                       x, a, b, st ? st->min_row : nullptr, st ? st->column : nullptr,
-                                       st ? st->pivot : nullptr, 0, want_prof ? prof.as<long long>() : nullptr, hls);
+                                       a, b, want_prof ? prof.as<long long>() : nullptr, hls);
     ALSK_LAUNCHED();
     if (want_prof) {
         std::vector<long long> h(static_cast<size_t>(grid) * NWARPS * 6);
