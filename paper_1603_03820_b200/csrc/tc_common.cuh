@@ -71,6 +71,21 @@ __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity, 
         else if (now - t0 > 20000000000ll) __trap();
     }
 }
+// The same wait with a suspend-time hint: a waiting thread is parked in try_wait until the
+// phase completes (or the hint expires), so the wait costs a handful of instructions.
+__device__ __forceinline__ void mbar_wait_park(uint64_t* bar, uint32_t parity) {
+    uint32_t done = 0;
+    uint32_t rounds = 0;
+    for (;;) {
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n selp.u32 %0, 1, 0, p;\n}\n"
+            : "=r"(done)
+            : "r"(smem_u32(bar)), "r"(parity), "r"(1000000u)
+            : "memory");
+        if (done) return;
+        if (++rounds > 20000u) __trap();  // > 20 s parked: deadlock
+    }
+}
 // Generic-proxy shared-memory writes -> visible to the async proxy (tensor core operands).
 __device__ __forceinline__ void fence_proxy_async_smem() {
     asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");

@@ -47,7 +47,7 @@ constexpr uint32_t BAR_FACTOR = 1;          // named barrier of the factor threa
 // K halves of a row group are LBO = 128 bytes apart, row groups SBO = 256 bytes apart
 constexpr int PT_BYTES = 4096;
 constexpr uint32_t PT_LBO = 128, PT_SBO = 256;
-constexpr int TS_PROF_SLOTS = 12;
+constexpr int TS_PROF_SLOTS = 16;
 
 struct TsPlan {
     int pks;
@@ -100,6 +100,11 @@ __device__ __forceinline__ bool bar_red_or(uint32_t id, uint32_t threads, bool v
         : "memory");
     return r != 0;
 }
+// waits of the factor threads: parked in try_wait (ns == 0) or nanosleep back-off
+__device__ __forceinline__ void ts_wait(uint64_t* bar, uint32_t parity, uint32_t ns) {
+    if (ns == 0) mbar_wait_park(bar, parity);
+    else mbar_wait_sleep(bar, parity, ns);
+}
 __device__ __forceinline__ float rna_tf32(float x) { return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xFFFFE000u); }
 // panel tile descriptor starting at row `row` (a multiple of 8)
 __device__ __forceinline__ uint64_t pt_desc(uint32_t tile, int row) {
@@ -119,20 +124,20 @@ __device__ __forceinline__ void schur_mma(uint32_t tmem, uint32_t ph, uint32_t p
     mma_tf32(tmem + col, al, bh, id, 1u);
 }
 
-// PROF: clock64() per phase, thread 0 (slots 0-7) and the back-substitution warp's lane 0
-// (8-9), into prof[blockIdx.x * TS_PROF_SLOTS + slot] (ALSK_TS_PROF=1).
+// PROF: clock64() per phase, factor thread `opts` (slots 0-7) and the back-substitution warp's lane 0
+// (8-9), into prof[blockIdx.x * TS_PROF_SLOTS + slot] (ALSK_TS_PROF=<thread>).
 template <bool PROF>
 __global__ void __launch_bounds__(TS_THREADS, 4)
 tc_solve_kernel(const float* __restrict__ packed, int64_t count, int f, float* __restrict__ out_x,
                 unsigned long long* __restrict__ min_row, int32_t* __restrict__ column,
                 double* __restrict__ pivot, int64_t status_base, long long* __restrict__ prof,
                 uint32_t sleep_ns, uint32_t opts) {
-    long long pcy[TS_PROF_SLOTS] = {};
-    long long tq = PROF ? clock64() : 0;
-    const long long tstart = tq;
+    uint32_t pcy[TS_PROF_SLOTS] = {};  // 32-bit: one launch of one CTA stays far below 2^32 cycles
+    uint32_t tq = PROF ? static_cast<uint32_t>(clock()) : 0u;
+    const uint32_t tstart = tq;
     auto lap = [&](int slot) {
         if constexpr (PROF) {
-            const long long now = clock64();
+            const uint32_t now = static_cast<uint32_t>(clock());
             pcy[slot] += now - tq;
             tq = now;
         }
@@ -181,7 +186,7 @@ tc_solve_kernel(const float* __restrict__ packed, int64_t count, int f, float* _
         // ---------------- back substitution L^T x = y, one system at a time ----------------
         uint32_t t = 0;
         for (int64_t g = blockIdx.x; g < count; g += gridDim.x, ++t) {
-            mbar_wait_sleep(lfull, t & 1u, 256);  // long wait: sleep, leave the issue slots to the factor warps
+            ts_wait(lfull, t & 1u, sleep_ns ? 256u : 0u);  // long wait: leave the issue slots to the factor warps
             lap(9);
             if (meta[0]) {
                 const float* dinv = dinvb + 128 * (t & 1u);
@@ -239,7 +244,7 @@ tc_solve_kernel(const float* __restrict__ packed, int64_t count, int f, float* _
         // my row of the system in rowbuf into TMEM (panel-blocked; row f = b); nz: a nonzero
         // A entry in my row
         auto fill = [&](int& nz) {
-            mbar_wait_sleep(load_bar, ph_load, sleep_ns);
+            ts_wait(load_bar, ph_load, sleep_ns);
             ph_load ^= 1u;
             uint32_t bits = 0;
             for (int b = 0; b < nbc && 8 * b <= wtop; ++b) {
@@ -350,6 +355,7 @@ tc_solve_kernel(const float* __restrict__ packed, int64_t count, int f, float* _
                     active = false;
                     break;
                 }
+                lap(12);
                 const bool update = bc + 1 < nbc;  // no trailing columns after the last block
                 // (2) my row of L (rows at or below the block, including row f = y); lanes above
                 //     keep their entries (upper-part or padding cells that are never read)
@@ -368,6 +374,7 @@ tc_solve_kernel(const float* __restrict__ packed, int64_t count, int f, float* _
                         L[c] = (i - r0 >= c || i == f) ? s : 0.f;  // diagonal-block rows: lower part
                     }
                 }
+                lap(13);
                 if (wlive) tmem_st8(tlane + r0, L);  // .sync.aligned: every lane of the warp stores
                 lap(2);
                 if (update) {
@@ -377,7 +384,7 @@ tc_solve_kernel(const float* __restrict__ packed, int64_t count, int f, float* _
                     for (int c = 0; c < 8; ++c) {
                         const float pv = (i >= r0 + 8 && i <= f) ? L[c] : 0.f;
                         h[c] = rna_tf32(pv);
-                        lo[c] = rna_tf32(pv - h[c]);
+                        lo[c] = pv - h[c];  // exact; the MMA reads its leading tf32 bits
                     }
                     if (wlive) {  // rows of a dead warp were zeroed when its rows left the panel
                         *reinterpret_cast<float4*>(Ph + pc0) = make_float4(h[0], h[1], h[2], h[3]);
@@ -397,14 +404,14 @@ tc_solve_kernel(const float* __restrict__ packed, int64_t count, int f, float* _
                         schur_mma(tmem, sPh, sPl, 0, N);
                         mma_commit(mma_bar);
                     }
-                    mbar_wait_sleep(mma_bar, ph_mma, sleep_ns);
+                    ts_wait(mma_bar, ph_mma, sleep_ns);
                     ph_mma ^= 1u;
                 }
                 lap(4);
             }
             // hand the factor to the back-substitution warp: L (packed lower) into lbuf once
             // it is done with the previous system
-            if (t > 0) mbar_wait_sleep(lfree, (t - 1) & 1u, sleep_ns);
+            if (t > 0) ts_wait(lfree, (t - 1) & 1u, sleep_ns);
             if (active) {
                 for (int b = 0; b < nbc && 8 * b <= wtop; ++b) {
                     tc_fence_after();
@@ -430,14 +437,14 @@ tc_solve_kernel(const float* __restrict__ packed, int64_t count, int f, float* _
         }
     }
     if constexpr (PROF) {
-        if (i == 0 || i == 32 * BS_WARP) {
-            pcy[7] = clock64() - tstart;
-            const int lo = i == 0 ? 0 : 8, hi = i == 0 ? 8 : 10;
-            for (int q = lo; q < hi; ++q) prof[blockIdx.x * TS_PROF_SLOTS + q] = pcy[q];
-            if (i == 0) {
-                prof[blockIdx.x * TS_PROF_SLOTS + 10] = pcy[10];
-                prof[blockIdx.x * TS_PROF_SLOTS + 11] = pcy[7];
-            }
+        const int pt = static_cast<int>(opts);  // profiled factor thread
+        pcy[7] = static_cast<uint32_t>(clock()) - tstart;
+        pcy[11] = pcy[7];
+        // constant indices only: pcy stays in registers
+#pragma unroll
+        for (int q = 0; q < TS_PROF_SLOTS; ++q) {
+            const bool bs = q == 8 || q == 9;
+            if ((i == pt && !bs) || (i == 32 * BS_WARP && bs)) prof[blockIdx.x * TS_PROF_SLOTS + q] = pcy[q];
         }
     }
     tc_fence_before();
@@ -454,14 +461,19 @@ void launch_solve(const float* packed, int64_t count, int f, float* x, const Sol
     // at least 46 KB of shared memory per CTA: never more than 4 CTAs (4 x 128 TMEM columns)
     // on an SM, so no CTA waits in tcgen05.alloc for another to finish
     const int smem = static_cast<int>(std::max<size_t>(P.total, 46 * 1024));
-    const unsigned grid = static_cast<unsigned>(std::min<int64_t>(count, 4 * static_cast<int64_t>(num_sms())));
+    static const int per_sm = [] {  // CTAs per SM (A/B switch for latency measurements; at most 4)
+        const char* e = std::getenv("ALSK_TS_CTAS");
+        return e ? std::max(1, std::min(4, std::atoi(e))) : 4;
+    }();
+    const unsigned grid = static_cast<unsigned>(std::min<int64_t>(count, per_sm * static_cast<int64_t>(num_sms())));
     static const bool want_prof = std::getenv("ALSK_TS_PROF") != nullptr;
     // back-off of the factor threads' short waits (MMA completion, hand-off, loads)
     static const uint32_t sleep_ns = [] {
         const char* e = std::getenv("ALSK_TS_SLEEP");
-        return e ? static_cast<uint32_t>(std::atoi(e)) : 32u;
+        return e ? static_cast<uint32_t>(std::atoi(e)) : 32u;  // parking (0) measured slower
     }();
-    const uint32_t opts = 0;
+    // ALSK_TS_PROF=<factor thread>: whose phases the profile reports
+    const uint32_t opts = want_prof ? static_cast<uint32_t>(std::atoi(std::getenv("ALSK_TS_PROF")) & 127) : 0u;
     if (!want_prof) {
         ALSK_CUDA(cudaFuncSetAttribute(tc_solve_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         tc_solve_kernel<false><<<grid, TS_THREADS, smem, s>>>(packed, count, f, x, st.min_row, st.column + status_off,
@@ -485,9 +497,9 @@ void launch_solve(const float* packed, int64_t count, int f, float* x, const Sol
     for (double& v : acc) v /= static_cast<double>(count) * 1e3;
     std::fprintf(stderr,
                  "[ts-prof f=%d rows=%lld grid=%u] kcyc/system: diag %.2f potrf %.2f trsm %.2f panel %.2f mma %.2f "
-                 "handoff %.2f fill %.2f start %.2f | total %.2f | backsub %.2f bs-wait %.2f\n",
+                 "handoff %.2f fill %.2f start %.2f | total %.2f | backsub %.2f bs-wait %.2f | flags %.2f trsm-math %.2f\n",
                  f, static_cast<long long>(count), grid, acc[0], acc[1], acc[2], acc[3], acc[4], acc[5], acc[6],
-                 acc[10], acc[11], acc[8], acc[9]);
+                 acc[10], acc[11], acc[8], acc[9], acc[12], acc[13]);
 }
 
 }  // namespace

@@ -36,6 +36,29 @@ __global__ void __launch_bounds__(128) k(int iters, int n, int nmma, int mode, l
     uint32_t ph = 0;
     long long t0 = clock64();
     for (int it = 0; it < iters; ++it) {
+        if (mode == 4) {
+            if (threadIdx.x == 0) {
+                tc_fence_after();
+                for (int q = 0; q < nmma; ++q) mma_tf32(tmem, a, b, id, 1u);
+                mma_commit(&bar);
+            }
+            __syncwarp();
+            const long long s0 = clock64();
+            const uint32_t ta = tmem + ((uint32_t)(warp * 32) << 16) + 120;
+            uint32_t r[8];
+            asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
+                         : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+                         : "r"(ta) : "memory");
+            tmem_ld_wait();
+            const long long s1 = clock64();
+            if (r[0] == 12345u && r[7] == 7u) out[0] = 1;
+            if (threadIdx.x == 32) out[gridDim.x + blockIdx.x] += s1 - s0;
+            mbar_wait(&bar, ph);
+            ph ^= 1u;
+            tc_fence_before();
+            named_barrier(1, 128);
+            continue;
+        }
         if (mode >= 2) {
             const uint32_t ta = tmem + ((uint32_t)(warp * 32) << 16) + (it & 7) * 8;
             uint32_t r[8];
@@ -79,23 +102,25 @@ int main() {
     int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
     long long* d;
-    cudaMalloc(&d, sizeof(long long) * 4 * sms);
-    long long* h = new long long[4 * sms];
+    cudaMalloc(&d, sizeof(long long) * 8 * sms);
+    long long* h = new long long[8 * sms];
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 50000);
     const int ns[] = {16, 112};
     for (int cps : {1, 4})
-        for (int mode : {3, 2, 1, 0})
+        for (int mode : {4, 3, 2, 1, 0})
             for (int n : ns)
                 for (int nmma : {1, 3}) {
-                    if (mode >= 1 && (n != 16 || nmma != 1)) continue;
+                    if (mode >= 1 && mode <= 3 && (n != 16 || nmma != 1)) continue;
                     const int grid = cps * sms;
+                    cudaMemset(d, 0, sizeof(long long) * 8 * sms);
                     k<<<grid, 128, 50000>>>(2000, n, nmma, mode, d);
                     cudaError_t e = cudaDeviceSynchronize();
                     if (e) { printf("err %s\n", cudaGetErrorString(e)); return 1; }
-                    cudaMemcpy(h, d, sizeof(long long) * grid, cudaMemcpyDeviceToHost);
-                    double s = 0;
-                    for (int i = 0; i < grid; ++i) s += h[i];
-                    printf("CTAs/SM %d %-12s N=%3d x%d: %8.1f clk per round trip\n", cps, mode == 3 ? "tmem st8" : mode == 2 ? "tmem ld8" : mode ? "arrive-only" : "mma+commit",
+                    cudaMemcpy(h, d, sizeof(long long) * 2 * grid, cudaMemcpyDeviceToHost);
+                    double s = 0, s2 = 0;
+                    for (int i = 0; i < grid; ++i) s += h[i], s2 += h[grid + i];
+                    if (mode == 4) printf("   (ld8 under a running MMA: %.1f clk)\n", s2 / grid / 2000);
+                    printf("CTAs/SM %d %-12s N=%3d x%d: %8.1f clk per round trip\n", cps,  mode == 4 ? "mma+ld8" : mode == 3 ? "tmem st8" : mode == 2 ? "tmem ld8" : mode ? "arrive-only" : "mma+commit",
                            n, nmma, s / grid);
                 }
     return 0;
