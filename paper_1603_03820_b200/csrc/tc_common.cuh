@@ -58,7 +58,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity, uint32_t ns) {
     uint32_t done = 0;
     long long t0 = 0;
-    for (;;) {
+    for (uint32_t it = 1;; ++it) {
         asm volatile(
             "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
             : "=r"(done)
@@ -66,9 +66,11 @@ __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity, 
             : "memory");
         if (done) return;
         __nanosleep(ns);
-        const long long now = clock64();
-        if (t0 == 0) t0 = now;
-        else if (now - t0 > 20000000000ll) __trap();
+        if ((it & 63u) == 0) {
+            const long long now = clock64();
+            if (t0 == 0) t0 = now;
+            else if (now - t0 > 20000000000ll) __trap();
+        }
     }
 }
 // The same wait with a suspend-time hint: a waiting thread is parked in try_wait until the

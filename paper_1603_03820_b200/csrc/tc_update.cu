@@ -8,18 +8,21 @@
 //
 // Arithmetic. The gathered rows are augmented with the rating, theta'_k = [theta_k, r_k]
 // (f+1 features), and every entry is split x = h + l, h = rna_tf32(x), l = rna_tf32(x - h).
-// One MMA per 8-rating k-step, D += H^T [H | 2L] (M = 128, N = 2*NF, NF = round16(f+1)), so
-// with D = [D0 | D1]:   sym(D0 + D1) = H^T H + H^T L + L^T H = sum_k theta'_k theta'_k^T
-// up to the dropped L^T L term (2^-22 relative). Rows < f of that symmetric matrix are A_u
+// Two MMAs per 8-rating k-step: D += H^T [H | L] (M = 128, N = 2*NF, NF = round16(f+1)) and
+// D1 += L^T H (N = NF, into the second half), so with D = [D0 | D1]:
+//   D0 + D1 = H^T H + H^T L + L^T H = sum_k theta'_k theta'_k^T
+// up to the dropped L^T L term (2^-22 relative), both halves symmetric: the lane owning row
+// i reads its lower-triangle cells directly, no transpose. Rows < f are A_u
 // (solver.hpp:130-140), row f is B_u (the bias rides along, solver.hpp:137).
 // The tensor core's FP32 accumulation truncates, which biases long sums; rows longer than
 // SEG_CHUNKS x 32 ratings are therefore accumulated in segments, each drained from TMEM and
-// added into shared memory with round-to-nearest FP32 adds.
+// added into a per-group shared-memory row (panel-blocked lower triangle) with
+// round-to-nearest FP32 adds.
 //
 // Warp roles (672 threads, 1 CTA per SM, rows j = blockIdx.x + t*gridDim.x):
-//   warps 0-7  : two epilogue groups of 4 warps (group g takes rows with t%2 == g). TMEM ->
-//                registers -> shared memory (segment sums) -> symmetrised A_u + lambda n_u
-//                and B_u rows written to HBM.
+//   warps 0-7  : two epilogue groups of 4 warps (group g takes rows with t%2 == g). Lane i
+//                reads row i's lower cells from TMEM (segment sums in shared memory) and
+//                writes A_u + lambda n_u and B_u to HBM, 32 bytes per lane and 8-column block.
 //   warps 8-15 : split warps: read the staged rating-major rows, split tf32 hi/lo and
 //                write them transposed into the K-major operand tile (lane = rating), with
 //                zero padding of partial k-groups.
@@ -38,6 +41,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <mutex>
+#include <array>
 #include <vector>
 
 #include "kernels.cuh"
@@ -48,8 +52,8 @@ namespace {
 using namespace tc;
 
 constexpr int KC = 32;                   // ratings per stage (four k-groups of 8)
-constexpr int HL_BYTES = 256 * KC * 4;      // 32 KB: H rows [0,NF) then 2L rows [NF,2NF), K-major
-constexpr int HL_STAGES_MAX = 3;           // operand-ring depth: 3 where shared memory allows, else 2
+constexpr int HL_BYTES = 256 * KC * 4;      // 32 KB: H rows [0,NF) then L rows [NF,2NF), K-major
+constexpr int HL_STAGES_MAX = 4;           // operand-ring depth: as deep as shared memory allows
 constexpr int SEG_CHUNKS = 16;              // TMEM accumulation segment: 16 x 32 ratings
 constexpr int NSPLIT = 8;                 // split warps
 constexpr int NG = 2;                     // epilogue groups (one alone falls behind the MMA on
@@ -74,8 +78,8 @@ struct TcPlan {
         : f(f_), stages(stages_), nb(nb_), hls(hls_) {
         rs = staging_stride(ldt);
         raw_bytes = (KC * rs * 4 + 127) & ~127;
-        sld = (f + 1) | 1;  // >= f+1 columns (A and B); odd: row writes and column reads conflict-free
-        s_floats = ((f + 1) * sld + 3) & ~3;  // keep the float4 panel 16-byte aligned
+        sld = 0;
+        s_floats = static_cast<int>(packed_stride(f));  // segment sums, panel-blocked (kernels.cuh)
         grp_floats = s_floats;
         hl_off = (static_cast<size_t>(stages) * raw_bytes + 1023) & ~static_cast<size_t>(1023);  // UMMA atoms: 1 KB
         ring_bytes = hl_off + static_cast<size_t>(hls) * HL_BYTES;
@@ -85,6 +89,12 @@ struct TcPlan {
         total = info_off + static_cast<size_t>(stages) * (KC * 4 + 16) + hls * 16 + 1024;  // + align slack
     }
 };
+
+// spin (ns == 0) or nanosleep back-off
+__device__ __forceinline__ void tc_wait(uint64_t* bar, uint32_t parity, uint32_t ns) {
+    if (ns == 0) mbar_wait(bar, parity);
+    else mbar_wait_sleep(bar, parity, ns);
+}
 
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
@@ -192,7 +202,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 tc_update_kernel(const float* __restrict__ theta, int ldt, const int64_t* __restrict__ row_ptr,
                  const int32_t* __restrict__ col_idx, const float* __restrict__ values, int64_t col_lo, int f,
                  float lambda, int64_t rb, int64_t nrows, int stages, float* __restrict__ out_a,
-                 float* __restrict__ out_b, long long* __restrict__ prof, int hls) {
+                 float* __restrict__ out_b, long long* __restrict__ prof, int hls, uint32_t epi_sleep,
+                 uint32_t load_sleep, uint32_t split_sleep, uint32_t mma_sleep, uint32_t dry) {
     // optional per-warp cycle accounting (ALSK_TC_PROF=1): pc[] slots per role, see launch_tc
     long long pc[6] = {0, 0, 0, 0, 0, 0};
     long long tp0 = 0;
@@ -302,7 +313,7 @@ tc_update_kernel(const float* __restrict__ theta, int ldt, const int64_t* __rest
                 const uint32_t ph = (ctr / stages) & 1u;
                 {
                     TP(t0);
-                    mbar_wait(&raw_empty[s], ph ^ 1u);
+                    mbar_wait_sleep(&raw_empty[s], ph ^ 1u, load_sleep);
                     TA(t0, 0);
                 }
                 uint8_t* stage = ring + s * RAW;
@@ -357,14 +368,14 @@ tc_update_kernel(const float* __restrict__ theta, int ldt, const int64_t* __rest
             const int s = ctr % stages;
             const int hs = ctr % HL_STAGES;
             TP(t0);
-            mbar_wait(&raw_full[s], (ctr / stages) & 1u);
+            tc_wait(&raw_full[s], (ctr / stages) & 1u, split_sleep);
             TA(t0, 0);
             const ChunkInfo ci = raw_info[s];
             TP(t1);
-            mbar_wait(&hl_empty[hs], ((ctr / HL_STAGES) & 1u) ^ 1u);
+            tc_wait(&hl_empty[hs], ((ctr / HL_STAGES) & 1u) ^ 1u, split_sleep);
             TA(t1, 1);
             TP(t2);
-            if (ci.cnt >= 0) {
+            if (ci.cnt >= 0 && !(dry & 1u)) {
                 // Padding slots of the k-group were zeroed by the loader, so the split is
                 // branch-free: h = rna_tf32(x), 2l = 2 rna_tf32(x - h) by bit ops.
                 const uint8_t* __restrict__ raw = ring + s * RAW + raw_k;  // staging and operand
@@ -379,18 +390,18 @@ tc_update_kernel(const float* __restrict__ theta, int ldt, const int64_t* __rest
                         for (int q = 0; q < 4; ++q) {
                             const float h = __uint_as_float((__float_as_uint(xv[q]) + 0x1000u) & 0xFFFFE000u);
                             const float l = xv[q] - h;
-                            const float l2 = 2.f * __uint_as_float((__float_as_uint(l) + 0x1000u) & 0xFFFFE000u);
+                            const float lr = __uint_as_float((__float_as_uint(l) + 0x1000u) & 0xFFFFE000u);
                             uint8_t* dst = H + kq[q] + t * (NSPLIT * 512);
                             *reinterpret_cast<float*>(dst) = h;
-                            *reinterpret_cast<float*>(dst + l_off) = l2;
+                            *reinterpret_cast<float*>(dst + l_off) = lr;
                         }
                     }
                 }
                 if (owns_r) {  // overwrite feature f (zero column) with the rating
                     const float r = raw_vals[s * KC + k];
-                    const float r_hi = tf32_rna(r), r_lo2 = 2.f * tf32_rna(r - r_hi);
+                    const float r_hi = tf32_rna(r), r_lo = tf32_rna(r - r_hi);
                     *reinterpret_cast<float*>(H + r_off) = r_hi;
-                    *reinterpret_cast<float*>(H + r_off + l_off) = r_lo2;
+                    *reinterpret_cast<float*>(H + r_off + l_off) = r_lo;
                 }
                 TA(t2, 2);
                 TP(t3);
@@ -407,30 +418,33 @@ tc_update_kernel(const float* __restrict__ theta, int ldt, const int64_t* __rest
         }
     } else if (warp == W_MMA) {
         // ---------------- MMA issuer ----------------
-        const uint32_t idesc = idesc_tf32(128, 2 * NF);
+        const uint32_t idesc = idesc_tf32(128, 2 * NF), idesc1 = idesc_tf32(128, NF);
         uint32_t job = 0;
         for (uint32_t ctr = 0;; ++ctr) {
             const int hs = ctr % HL_STAGES;
             // every lane waits (a lane-0-only wait followed by a warp shuffle measured ~700
             // cycles of reconvergence per chunk)
             TP(t0);
-            mbar_wait(&hl_full[hs], (ctr / HL_STAGES) & 1u);
+            tc_wait(&hl_full[hs], (ctr / HL_STAGES) & 1u, mma_sleep);
             TA(t0, 0);
             const ChunkInfo ci = hl_info[hs];
             if (ci.cnt < 0) break;
             const uint32_t b = job & 1u;
             const uint32_t dcol = tmem + b * 256u;
             TP(t1);
-            if (ci.flags & CH_FIRST) mbar_wait(&tempty[b], ((job >> 1) & 1u) ^ 1u);
+            if (ci.flags & CH_FIRST) tc_wait(&tempty[b], ((job >> 1) & 1u) ^ 1u, mma_sleep);
             TA(t1, 1);
             tc_fence_after();
             if (lane == 0) {
                 const uint32_t hb = smem_u32(hl + hs * HL_BYTES);
                 const int ksteps = (ci.cnt + 7) >> 3;
                 TP(t2);
-                for (int kb = 0; kb < ksteps; ++kb) {
-                    const uint64_t d = sdesc_sw128(hb + kb * 32, 16, 1024);
-                    mma_tf32(dcol, d, d, idesc, (!(ci.flags & CH_FIRST) || kb > 0) ? 1u : 0u);
+                for (int kb = 0; kb < ((dry & 2u) ? 0 : ksteps); ++kb) {
+                    const uint32_t acc = (!(ci.flags & CH_FIRST) || kb > 0) ? 1u : 0u;
+                    const uint64_t dh = sdesc_sw128(hb + kb * 32, 16, 1024);               // H rows
+                    const uint64_t dl = sdesc_sw128(hb + NF * 128 + kb * 32, 16, 1024);    // L rows
+                    mma_tf32(dcol, dh, dh, idesc, acc);        // [D0 | D1] (+)= H^T [H | L]
+                    mma_tf32(dcol + NF, dl, dh, idesc1, 1u);   // D1 += L^T H
                 }
                 TA(t2, 2);
                 TP(t3);
@@ -443,14 +457,19 @@ tc_update_kernel(const float* __restrict__ theta, int ldt, const int64_t* __rest
         }
     } else {
         // ---------------- epilogue groups ----------------
+        // Lane e of the group owns matrix row e (TMEM lane e): its lower cells j <= e (row f:
+        // j < f) are D0 + D1 of its own lane, so each lane writes its row's 8-column blocks
+        // (panel-blocked, kernels.cuh) straight to HBM, 32 bytes per block, consecutive lanes
+        // at consecutive addresses. Rows of several segments keep the running sums in the
+        // group's shared-memory row (same layout, conflict-free 16-byte accesses).
         const int g = warp >> 2;
-        const int e = threadIdx.x & 127;  // TMEM lane = matrix row owned in the readback
-        const uint32_t bar_id = 1 + g;
-        float* S = grp0 + g * P.grp_floats;
-        const int sld = P.sld;
+        const int e = threadIdx.x & 127;
+        float* acc_row = grp0 + g * P.grp_floats;
         const uint32_t lane_base = static_cast<uint32_t>((warp & 3) * 32) << 16;
-        const int nch16 = (f + 1 + 15) >> 4;  // 16-column TMEM chunks covering features 0..f
-        float* Srow = S + e * sld;
+        const int wtop = 32 * (warp & 3) + 31;                // last row of my warp
+        const int nc16 = (min(wtop, f) >> 4) + 1;             // 16-column chunks holding my warp's lower cells
+        const int nb_mine = e < f ? (e >> 3) + 1 : (e == f ? ((f - 1) >> 3) + 1 : 0);  // my 8-column blocks
+        const int64_t pkn = packed_stride(f);
         uint32_t job = 0, use[2] = {0u, 0u};
         int t = 0;
         for (RowIter it(nrows); it.more(); it.next(), ++t) {
@@ -462,81 +481,84 @@ tc_update_kernel(const float* __restrict__ theta, int ldt, const int64_t* __rest
                 continue;
             }
             const int64_t row = it.j;
-            if (n > 0) {
-                for (uint32_t sg = 0; sg < nseg; ++sg, ++job) {
-                    const uint32_t b = job & 1u;
-                    const uint32_t dcol = tmem + b * 256u + lane_base;
-                    TP(t0);
-                    mbar_wait(&tfull[2 * g + b], use[b] & 1u);
-                    TA(t0, 4);
-                    ++use[b];
-                    tc_fence_after();
-                    TP(t1);
-                    for (int c = 0; c < nch16; ++c) {
-                        float d0[16], d1[16];
-                        tmem_ld16(dcol + c * 16, d0);
-                        tmem_ld16(dcol + NF + c * 16, d1);
-                        tmem_ld_wait();
-                        if (e <= f) {
-#pragma unroll
-                            for (int jj = 0; jj < 16; ++jj) {
-                                const int j = c * 16 + jj;
-                                if (j <= f) Srow[j] = (sg ? Srow[j] : 0.f) + (d0[jj] + d1[jj]);
-                            }
-                        }
-                    }
-                    tc_fence_before();
-                    __syncwarp();
-                    if ((e & 31) == 0) mbar_arrive(&tempty[b]);
-                    TA(t1, 4);
-                }
-                TP(t2);
-                named_barrier(bar_id, 128);
-                const float reg = lambda * static_cast<float>(n);  // float arithmetic as solver.hpp:141,152
+            const float reg = lambda * static_cast<float>(n);  // float arithmetic as solver.hpp:141,152
+            float* pk = out_a + row * pkn;                                   // MODE_PACKED
+            float* a_out = out_a + row * static_cast<int64_t>(f) * f;        // MODE_FULL
+            float* b_out = out_b + row * static_cast<int64_t>(f);
+            if (n == 0) {
                 if constexpr (MODE == MODE_FULL) {
-                    // A = sym(S) (+ lambda n_u on the diagonal) written full and B = row f; the
-                    // symmetrisation 0.5 (S_ij + S_ji) is commutative, so A mirrors bit-exactly
-                    float* a_out = out_a + row * static_cast<int64_t>(f) * f;
-                    float* b_out = out_b + row * static_cast<int64_t>(f);
-                    for (int idx = e; idx < f * f; idx += 128) {
-                        const int i = idx / f, j = idx - i * f;
-                        float v = 0.5f * (S[i * sld + j] + S[j * sld + i]);
-                        if (i == j) v += reg;
-                        a_out[idx] = v;
-                    }
-                    for (int j = e; j < f; j += 128) b_out[j] = 0.5f * (S[f * sld + j] + S[j * sld + f]);
+                    for (int idx = e; idx < f * f; idx += 128) a_out[idx] = 0.f;
+                    for (int j = e; j < f; j += 128) b_out[j] = 0.f;
                 } else {
-                    // panel-blocked packed row (kernels.cuh): block b holds rows 8b..f x 8
-                    // columns; consecutive threads write consecutive floats, the transposed S_ji
-                    // reads are conflict-light (odd row stride)
-                    float* pk = out_a + row * packed_stride(f);
-                    const int nbk = (f + 7) >> 3;
-                    for (int bk = 0; bk < nbk; ++bk) {
-                        float* dst = pk + pb_block(f, bk);
-                        const int cnt = (f + 1 - 8 * bk) * 8;
-                        for (int q = e; q < cnt; q += 128) {
-                            const int i = 8 * bk + (q >> 3), j = 8 * bk + (q & 7);
-                            float v = 0.f;
-                            if (i < f ? j <= i : j < f) {
-                                v = 0.5f * (S[i * sld + j] + S[j * sld + i]);
-                                if (j == i) v += reg;
-                            }
-                            dst[q] = v;
-                        }
-                    }
+                    for (int64_t idx = e; idx < pkn; idx += 128) pk[idx] = 0.f;
                 }
-                named_barrier(bar_id, 128);
-                TA(t2, 4);
                 continue;
             }
-            if constexpr (MODE == MODE_FULL) {
-                float* a_out = out_a + row * static_cast<int64_t>(f) * f;
-                for (int idx = e; idx < f * f; idx += 128) a_out[idx] = 0.f;
-                for (int j = e; j < f; j += 128) out_b[row * static_cast<int64_t>(f) + j] = 0.f;
-            } else {
-                const int pkn = static_cast<int>(packed_stride(f));
-                float* pk = out_a + row * static_cast<int64_t>(pkn);
-                for (int idx = e; idx < pkn; idx += 128) pk[idx] = 0.f;
+            for (uint32_t sg = 0; sg < nseg; ++sg, ++job) {
+                const uint32_t b = job & 1u;
+                const uint32_t dcol = tmem + b * 256u + lane_base;
+                const bool first = sg == 0, last = sg + 1 == nseg;
+                TP(t0);
+                // long, latency-tolerant wait (the group has the other group's row as slack):
+                // back off so the spinning does not take issue slots from the split warps
+                mbar_wait_sleep(&tfull[2 * g + b], use[b] & 1u, epi_sleep);
+                TA(t0, 4);
+                ++use[b];
+                tc_fence_after();
+                TP(t1);
+                for (int c = 0; c < nc16; ++c) {
+                    float d0[16], d1[16];
+                    tmem_ld16(dcol + c * 16, d0);
+                    tmem_ld16(dcol + NF + c * 16, d1);
+                    tmem_ld_wait();
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const int bk = 2 * c + h;  // 8-column block
+                        if (bk >= nb_mine) continue;
+                        float v[8];
+#pragma unroll
+                        for (int q = 0; q < 8; ++q) {
+                            const int j = 8 * bk + q;
+                            const bool cell = e < f ? j <= e : j < f;
+                            v[q] = cell ? d0[8 * h + q] + d1[8 * h + q] : 0.f;
+                        }
+                        const int64_t off = pb_block(f, bk) + 8 * (e - 8 * bk);
+                        float4* accp = reinterpret_cast<float4*>(acc_row + off);
+                        if (!first) {  // running sum of the earlier segments, round-to-nearest adds
+                            const float4 p0 = accp[0], p1 = accp[1];
+                            v[0] += p0.x, v[1] += p0.y, v[2] += p0.z, v[3] += p0.w;
+                            v[4] += p1.x, v[5] += p1.y, v[6] += p1.z, v[7] += p1.w;
+                        }
+                        if (!last) {
+                            accp[0] = make_float4(v[0], v[1], v[2], v[3]);
+                            accp[1] = make_float4(v[4], v[5], v[6], v[7]);
+                            continue;
+                        }
+                        if (e < f && (e >> 3) == bk) v[e & 7] += reg;  // lambda n_u on the diagonal
+                        if constexpr (MODE == MODE_PACKED) {
+                            float4* dst = reinterpret_cast<float4*>(pk + off);
+                            dst[0] = make_float4(v[0], v[1], v[2], v[3]);
+                            dst[1] = make_float4(v[4], v[5], v[6], v[7]);
+                        } else {
+                            // A written full from the lower triangle (row and its mirror), so it
+                            // mirrors bit-exactly; B = row f
+#pragma unroll
+                            for (int q = 0; q < 8; ++q) {
+                                const int j = 8 * bk + q;
+                                if (e < f && j <= e) {
+                                    a_out[static_cast<int64_t>(e) * f + j] = v[q];
+                                    a_out[static_cast<int64_t>(j) * f + e] = v[q];
+                                } else if (e == f && j < f) {
+                                    b_out[j] = v[q];
+                                }
+                            }
+                        }
+                    }
+                }
+                tc_fence_before();
+                __syncwarp();
+                if ((e & 31) == 0) mbar_arrive(&tempty[b]);
+                TA(t1, 4);
             }
         }
     }
@@ -560,14 +582,37 @@ template <int NB, int MODE>
 void launch_tc(const DevCsr& r, const float* theta, int64_t theta_rows, int f, int ldt, float lambda, int64_t rb,
                int64_t re, float* x, float* a, float* b, const SolveStatus* st, cudaStream_t s) {
     // deepest operand ring first (the MMA is fed by the split through it), then the staging ring
-    int hls = HL_STAGES_MAX, stages = 6;
+    static const int max_hls = [] {  // A/B switches for measurements
+        const char* e = std::getenv("ALSK_TC_HLS");
+        return e ? std::max(2, std::min(HL_STAGES_MAX, std::atoi(e))) : HL_STAGES_MAX;
+    }();
+    static const int max_stages = [] {
+        const char* e = std::getenv("ALSK_TC_STAGES");
+        return e ? std::max(2, std::min(8, std::atoi(e))) : 6;
+    }();
+    int hls = max_hls, stages = max_stages;
     for (;;) {
         while (stages > 2 && TcPlan(f, NB, stages, ldt, hls).total > 227 * 1024) --stages;
         if (stages >= 3 || hls == 2) break;
         --hls;
-        stages = 6;
+        stages = max_stages;
     }
     const TcPlan P(f, NB, stages, ldt, hls);
+    // nanosleep back-off (ns, 0 = spin) of the waits of the epilogue, loader, split and MMA
+    // warps (ALSK_TC_SLEEP=epi,load,split,mma)
+    static const std::array<uint32_t, 4> sleeps = [] {
+        std::array<uint32_t, 4> v{128u, 32u, 50u, 20u};
+        if (const char* e = std::getenv("ALSK_TC_SLEEP")) {
+            unsigned a = 0, b = 0, c = 0, d = 0;
+            if (std::sscanf(e, "%u,%u,%u,%u", &a, &b, &c, &d) == 4) v = {a, b, c, d};
+        }
+        return v;
+    }();
+    // ALSK_TC_DRY (measurements only): 1 = split warps skip the split, 2 = no MMAs
+    static const uint32_t dry = [] {
+        const char* e = std::getenv("ALSK_TC_DRY");
+        return e ? static_cast<uint32_t>(std::atoi(e)) : 0u;
+    }();
     auto k = tc_update_kernel<NB, MODE>;
     ALSK_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(P.total)));
     const int64_t nrows = re - rb;
@@ -579,7 +624,8 @@ void launch_tc(const DevCsr& r, const float* theta, int64_t theta_rows, int f, i
         ALSK_CUDA(cudaMemsetAsync(prof.as<void>(), 0, sizeof(long long) * grid * NWARPS * 6, s));
     }
     k<<<grid, NTHREADS, P.total, s>>>(theta, ldt, r.row_ptr, r.col_idx, r.values, r.col_offset, f, lambda, rb, nrows, stages,
-                                       a, b, want_prof ? prof.as<long long>() : nullptr, hls);
+                                       a, b, want_prof ? prof.as<long long>() : nullptr, hls, sleeps[0], sleeps[1],
+                                       sleeps[2], sleeps[3], dry);
     ALSK_LAUNCHED();
     if (want_prof) {
         std::vector<long long> h(static_cast<size_t>(grid) * NWARPS * 6);
