@@ -19,15 +19,15 @@
 // added into a per-group shared-memory row (panel-blocked lower triangle) with
 // round-to-nearest FP32 adds.
 //
-// Warp roles (672 threads, 1 CTA per SM, rows j = blockIdx.x + t*gridDim.x):
+// Warp roles (800 threads, 1 CTA per SM, rows j = blockIdx.x + t*gridDim.x):
 //   warps 0-7  : two epilogue groups of 4 warps (group g takes rows with t%2 == g). Lane i
 //                reads row i's lower cells from TMEM (segment sums in shared memory) and
 //                writes A_u + lambda n_u and B_u to HBM, 32 bytes per lane and 8-column block.
-//   warps 8-15 : split warps: read the staged rating-major rows, split tf32 hi/lo and
+//   warps 8-19 : split warps: read the staged rating-major rows, split tf32 hi/lo and
 //                write them transposed into the K-major operand tile (lane = rating), with
 //                zero padding of partial k-groups.
-//   warp 16    : MMA issuer (one thread), owns the TMEM allocation (2 buffers x 256 columns).
-//   warps 17-20: loaders: the only readers of the CSR arrays (4-chunk register prefetch queue);
+//   warp 20    : MMA issuer (one thread), owns the TMEM allocation (2 buffers x 256 columns).
+//   warps 21-24: loaders: the only readers of the CSR arrays (4-chunk register prefetch queue);
 //                lane = rating slot, each lane copies 16-byte pieces of its gathered factor
 //                row with cp.async into a rating-major staging ring, completion counted per
 //                lane on the stage mbarrier (cp.async.mbarrier.arrive.noinc).
@@ -60,7 +60,7 @@ constexpr int KC = 32;                   // ratings per stage (four k-groups of 
 constexpr int HL_BYTES = 256 * KC * 4;      // 32 KB: H rows [0,NF) then L rows [NF,2NF), K-major
 constexpr int HL_STAGES_MAX = 4;           // operand-ring depth: as deep as shared memory allows
 constexpr int SEG_CHUNKS = 16;              // TMEM accumulation segment: 16 x 32 ratings
-constexpr int NSPLIT = 8;                 // split warps
+constexpr int NSPLIT = 12;                // split warps (8: 1% slower)
 constexpr int NG = 2;                     // epilogue groups (one alone falls behind the MMA on
                                           // short X-half rows: measured 61 vs 54.5 ms)
 constexpr int W_SPLIT = 4 * NG, W_MMA = W_SPLIT + NSPLIT, W_LOAD = W_MMA + 1;
