@@ -295,6 +295,9 @@ def run_ours(args):
                     "launches": int(hn.value), "kernel_share_of_step": (hm.value / args.steps) / ms,
                     "fp32_ffma_equiv": {"peak": ffma_peak or nominal_ffma, "frac": achieved / (ffma_peak or nominal_ffma),
                                         "peak_source": "measured FFMA probe (alsk_fp32_peak_probe)"},
+                    # a split-precision tensor-core kernel is also reported
+                    # against the TF32 peak / 3 (three tf32 products per FP32-accurate product)
+                    "tf32x3_equiv": {"peak": tf32_peak / 3, "frac": achieved / (tf32_peak / 3)},
                     # the same launches against HBM: algorithmic bytes = per rating the column
                     # index, the value and the gathered factor row (4f), per row the row pointer
                     # and the packed A/B row written for the solve
