@@ -27,6 +27,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <array>
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
@@ -101,6 +102,18 @@ __device__ __forceinline__ bool bar_red_or(uint32_t id, uint32_t threads, bool v
     return r != 0;
 }
 // waits of the factor threads: parked in try_wait (ns == 0) or nanosleep back-off
+// a wait known to take at least ~first_ns: one test, one long sleep, then short polls
+__device__ __forceinline__ void ts_wait_first(uint64_t* bar, uint32_t parity, uint32_t first_ns, uint32_t ns) {
+    uint32_t done;
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    if (done) return;
+    __nanosleep(first_ns);
+    mbar_wait_sleep(bar, parity, ns);
+}
 __device__ __forceinline__ void ts_wait(uint64_t* bar, uint32_t parity, uint32_t ns) {
     if (ns == 0) mbar_wait_park(bar, parity);
     else mbar_wait_sleep(bar, parity, ns);
@@ -131,7 +144,7 @@ __global__ void __launch_bounds__(TS_THREADS, 4)
 tc_solve_kernel(const float* __restrict__ packed, int64_t count, int f, float* __restrict__ out_x,
                 unsigned long long* __restrict__ min_row, int32_t* __restrict__ column,
                 double* __restrict__ pivot, int64_t status_base, long long* __restrict__ prof,
-                uint32_t sleep_ns, uint32_t opts) {
+                uint32_t sleep_ns, uint32_t opts, uint32_t mma_first_ns, uint32_t bs_ns) {
     uint32_t pcy[TS_PROF_SLOTS] = {};  // 32-bit: one launch of one CTA stays far below 2^32 cycles
     uint32_t tq = PROF ? static_cast<uint32_t>(clock()) : 0u;
     const uint32_t tstart = tq;
@@ -186,7 +199,7 @@ tc_solve_kernel(const float* __restrict__ packed, int64_t count, int f, float* _
         // ---------------- back substitution L^T x = y, one system at a time ----------------
         uint32_t t = 0;
         for (int64_t g = blockIdx.x; g < count; g += gridDim.x, ++t) {
-            ts_wait(lfull, t & 1u, sleep_ns ? 256u : 0u);  // long wait: leave the issue slots to the factor warps
+            ts_wait(lfull, t & 1u, bs_ns);  // long wait: leave the issue slots to the factor warps
             lap(9);
             if (meta[0]) {
                 const float* dinv = dinvb + 128 * (t & 1u);
@@ -404,7 +417,7 @@ tc_solve_kernel(const float* __restrict__ packed, int64_t count, int f, float* _
                         schur_mma(tmem, sPh, sPl, 0, N);
                         mma_commit(mma_bar);
                     }
-                    ts_wait(mma_bar, ph_mma, sleep_ns);
+                    ts_wait_first(mma_bar, ph_mma, mma_first_ns, sleep_ns);  // MMA round trip >= ~500 cycles
                     ph_mma ^= 1u;
                 }
                 lap(4);
@@ -465,9 +478,25 @@ void launch_solve(const float* packed, int64_t count, int f, float* x, const Sol
         const char* e = std::getenv("ALSK_TS_CTAS");
         return e ? std::max(1, std::min(4, std::atoi(e))) : 4;
     }();
-    const unsigned grid = static_cast<unsigned>(std::min<int64_t>(count, per_sm * static_cast<int64_t>(num_sms())));
     static const bool want_prof = std::getenv("ALSK_TS_PROF") != nullptr;
+    // persistent CTAs with a static system assignment: never launch more than are resident
+    // at once (large f: shared memory allows only 3 or 2 per SM), or the extra CTAs run as a
+    // second wave after the others
+    int resident = 0;
+    ALSK_CUDA(cudaFuncSetAttribute(tc_solve_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    ALSK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&resident, tc_solve_kernel<false>, TS_THREADS, smem));
+    const int ctas_per_sm = std::max(1, std::min(per_sm, resident));
+    const unsigned grid = static_cast<unsigned>(std::min<int64_t>(count, ctas_per_sm * static_cast<int64_t>(num_sms())));
     // back-off of the factor threads' short waits (MMA completion, hand-off, loads)
+    // ALSK_TS_WAITS=mma_first,backsub (ns): first sleep of the MMA wait, back-substitution poll
+    static const std::array<uint32_t, 2> tun = [] {
+        std::array<uint32_t, 2> v{200u, 1000u};
+        if (const char* e = std::getenv("ALSK_TS_WAITS")) {
+            unsigned a = 0, b = 0;
+            if (std::sscanf(e, "%u,%u", &a, &b) == 2) v = {a, b};
+        }
+        return v;
+    }();
     static const uint32_t sleep_ns = [] {
         const char* e = std::getenv("ALSK_TS_SLEEP");
         return e ? static_cast<uint32_t>(std::atoi(e)) : 32u;  // parking (0) measured slower
@@ -477,7 +506,8 @@ void launch_solve(const float* packed, int64_t count, int f, float* x, const Sol
     if (!want_prof) {
         ALSK_CUDA(cudaFuncSetAttribute(tc_solve_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         tc_solve_kernel<false><<<grid, TS_THREADS, smem, s>>>(packed, count, f, x, st.min_row, st.column + status_off,
-                                                              st.pivot + status_off, status_off, nullptr, sleep_ns, opts);
+                                                              st.pivot + status_off, status_off, nullptr, sleep_ns, opts,
+                                                              tun[0], tun[1]);
         ALSK_LAUNCHED();
         return;
     }
@@ -486,7 +516,8 @@ void launch_solve(const float* packed, int64_t count, int f, float* x, const Sol
     prof.alloc(sizeof(long long) * grid * TS_PROF_SLOTS, s);
     ALSK_CUDA(cudaMemsetAsync(prof.as<void>(), 0, sizeof(long long) * grid * TS_PROF_SLOTS, s));
     tc_solve_kernel<true><<<grid, TS_THREADS, smem, s>>>(packed, count, f, x, st.min_row, st.column + status_off,
-                                                         st.pivot + status_off, status_off, prof.as<long long>(), sleep_ns, opts);
+                                                         st.pivot + status_off, status_off, prof.as<long long>(), sleep_ns, opts,
+                                                         tun[0], tun[1]);
     ALSK_LAUNCHED();
     std::vector<long long> h(static_cast<size_t>(grid) * TS_PROF_SLOTS);
     ALSK_CUDA(cudaMemcpyAsync(h.data(), prof.as<void>(), h.size() * sizeof(long long), cudaMemcpyDeviceToHost, s));
