@@ -484,8 +484,16 @@ void launch_solve(const float* packed, int64_t count, int f, float* x, const Sol
     // second wave after the others
     int resident = 0;
     ALSK_CUDA(cudaFuncSetAttribute(tc_solve_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    ALSK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&resident, tc_solve_kernel<false>, TS_THREADS, smem));
+    // CTAs that fit an SM's shared memory (228 KB, 1 KB reserved per CTA + 1 KB static);
+    // cudaOccupancyMaxActiveBlocksPerMultiprocessor reports 1 for this kernel, which is not
+    // what the hardware runs
+    resident = static_cast<int>((228 * 1024) / (smem + 2 * 1024));
     const int ctas_per_sm = std::max(1, std::min(per_sm, resident));
+    static bool said = false;
+    if (!said && std::getenv("ALSK_TS_VERBOSE")) {
+        std::fprintf(stderr, "[tc_solve] f=%d smem=%d resident=%d ctas_per_sm=%d\n", f, smem, resident, ctas_per_sm);
+        said = true;
+    }
     const unsigned grid = static_cast<unsigned>(std::min<int64_t>(count, ctas_per_sm * static_cast<int64_t>(num_sms())));
     // back-off of the factor threads' short waits (MMA completion, hand-off, loads)
     // ALSK_TS_WAITS=mma_first,backsub (ns): first sleep of the MMA wait, back-substitution poll
@@ -540,6 +548,11 @@ bool packed_solve(const float* packed, int64_t count, int f, float* x, const Sol
     static const bool tiles = std::getenv("ALSK_SOLVE_TILES") != nullptr;  // A/B switch for measurements
     if (tiles || f < 8 || f > 127) return packed_solve_tiles(packed, count, f, x, st, status_off, s);
     if (count <= 0) return true;
+    static const int bw = [] {  // column-step width of the TMEM Cholesky (A/B switch)
+        const char* e = std::getenv("ALSK_TS_BW");
+        return e ? std::atoi(e) : 8;
+    }();
+    if (bw == 16 && packed_solve16(packed, count, f, x, st, status_off, s)) return true;
     launch_solve(packed, count, f, x, st, status_off, s);
     return true;
 }
