@@ -19,15 +19,16 @@
 // added into a per-group shared-memory row (panel-blocked lower triangle) with
 // round-to-nearest FP32 adds.
 //
-// Warp roles (800 threads, 1 CTA per SM, rows j = blockIdx.x + t*gridDim.x):
-//   warps 0-7  : two epilogue groups of 4 warps (group g takes rows with t%2 == g). Lane i
-//                reads row i's lower cells from TMEM (segment sums in shared memory) and
-//                writes A_u + lambda n_u and B_u to HBM, 32 bytes per lane and 8-column block.
-//   warps 8-19 : split warps: read the staged rating-major rows, split tf32 hi/lo and
+// Warp roles (672 threads, 1 CTA per SM, rows j = blockIdx.x + t*gridDim.x):
+//   warps 0-3  : the epilogue group (NG = 1; the code supports NG groups taking rows
+//                t % NG). Lane i reads row i's lower cells from TMEM (segment sums in shared
+//                memory) and writes A_u + lambda n_u and B_u to HBM, 32 bytes per lane and
+//                8-column block.
+//   warps 4-15 : split warps: read the staged rating-major rows, split tf32 hi/lo and
 //                write them transposed into the K-major operand tile (lane = rating), with
 //                zero padding of partial k-groups.
-//   warp 20    : MMA issuer (one thread), owns the TMEM allocation (2 buffers x 256 columns).
-//   warps 21-24: loaders: the only readers of the CSR arrays (4-chunk register prefetch queue);
+//   warp 16    : MMA issuer (one thread), owns the TMEM allocation (2 buffers x 256 columns).
+//   warps 17-20: loaders: the only readers of the CSR arrays (4-chunk register prefetch queue);
 //                lane = rating slot, each lane copies 16-byte pieces of its gathered factor
 //                row with cp.async into a rating-major staging ring, completion counted per
 //                lane on the stage mbarrier (cp.async.mbarrier.arrive.noinc).
@@ -60,9 +61,9 @@ constexpr int KC = 32;                   // ratings per stage (four k-groups of 
 constexpr int HL_BYTES = 256 * KC * 4;      // 32 KB: H rows [0,NF) then L rows [NF,2NF), K-major
 constexpr int HL_STAGES_MAX = 4;           // operand-ring depth: as deep as shared memory allows
 constexpr int SEG_CHUNKS = 16;              // TMEM accumulation segment: 16 x 32 ratings
-constexpr int NSPLIT = 12;                // split warps (8: 1% slower)
-constexpr int NG = 2;                     // epilogue groups (one alone falls behind the MMA on
-                                          // short X-half rows: measured 61 vs 54.5 ms)
+constexpr int NSPLIT = 12;                // split warps (8 and 16 measured ~1% slower)
+constexpr int NG = 1;                     // epilogue groups (two measured 1% slower once the epilogue
+                                          // lost its transpose; with it, one was 12% slower)
 constexpr int W_SPLIT = 4 * NG, W_MMA = W_SPLIT + NSPLIT, W_LOAD = W_MMA + 1;
 constexpr int NLOAD = 4;                  // loader warps
 constexpr int NWARPS = W_LOAD + NLOAD;
