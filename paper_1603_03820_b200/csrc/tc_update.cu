@@ -59,7 +59,7 @@ using namespace tc;
 
 constexpr int KC = 32;                   // ratings per stage (four k-groups of 8)
 constexpr int HL_BYTES = 256 * KC * 4;      // 32 KB: H rows [0,NF) then L rows [NF,2NF), K-major
-constexpr int HL_STAGES_MAX = 4;           // operand-ring depth: as deep as shared memory allows
+constexpr int HL_STAGES_MAX = 2;           // operand-ring depth (measured: 2 58.5, 3 59.8, 4 60.2 ms/iter)
 constexpr int SEG_CHUNKS = 16;              // TMEM accumulation segment: 16 x 32 ratings
 constexpr int NSPLIT = 12;                // split warps (8 and 16 measured ~1% slower)
 constexpr int NG = 1;                     // epilogue groups (two measured 1% slower once the epilogue
@@ -598,7 +598,7 @@ void launch_tc(const DevCsr& r, const float* theta, int64_t theta_rows, int f, i
     }();
     static const int max_stages = [] {
         const char* e = std::getenv("ALSK_TC_STAGES");
-        return e ? std::max(2, std::min(8, std::atoi(e))) : 6;
+        return e ? std::max(2, std::min(8, std::atoi(e))) : 5;  // 4-6 within noise, 3 and 2 slower
     }();
     int hls = max_hls, stages = max_stages;
     for (;;) {
