@@ -175,11 +175,12 @@ def run_reference(args):
     v = float(np.median(vals))
     base["value"] = v
     print(json.dumps({
-        "impl": "reference", "metric": "s/ALS-iter (Netflix-shape f=100)", "value": v, "unit": "s/ALS-iter",
+        "impl": "reference", "metric": f"s/ALS-iter ({args.config}-shape f={f})", "value": v, "unit": "s/ALS-iter",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": v * 1e3,
         "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64-accumulate",
-        "data": "synthetic", "config": {"workload": args.config, "m": m, "n": n, "nnz_total": nnz, "f": f,
-                                        "lambda": lam, "holdout": 0.1},
+        "data": "synthetic (planted rank-10 + U[-0.5,0.5) noise; SURVEY \u00a78(d) generator)",
+        "config": {"workload": args.config, "m": m, "n": n, "nnz_total": nnz, "nnz_train": int(train.row_ptr[-1]),
+                   "f": f, "lambda": lam, "holdout": 0.1, "parallelism": "host threads (reference thread pool)"},
         "cpu_baseline": base, "e2e": {"value": v, "unit": "s/ALS-iter", "h2d_bytes_per_step": 0,
                                       "d2h_bytes_per_step": 0}}))
 
