@@ -225,6 +225,21 @@ alsk_status alsk_dev_partial_hermitian(const alsk_csr* r, const float* theta, in
 alsk_status alsk_dev_solve_packed(const double* packed, int64_t count, int f, float* x_out,
                                   void* stream);
 
+/* FP32 variant of the data-parallel split (replaces local_hermitian + the double
+ * reduce_batches, parallel.hpp:412-421, 206-280, at the FP32 tolerance): packed rows of
+ * A_u + lambda n_u I and B_u for rows [row_begin,row_end) from the tensor cores
+ * (16 <= f <= 119), panel-blocked, alsk_packed_stride(f) floats per row (layout in
+ * INTEGRATION.md); partials of several slabs add entry-wise (lambda uses the local n_u,
+ * so the sum carries lambda n_u of the whole row). */
+int64_t alsk_packed_stride(int f);
+alsk_status alsk_dev_partial_hermitian_f32(const alsk_csr* r, const float* theta, int64_t theta_rows,
+                                           int f, double lambda, int64_t row_begin, int64_t row_end,
+                                           float* out_packed, void* stream);
+/* Solve packed FP32 systems (the layout above) with the batched TMEM Cholesky into
+ * x_out[count*f]; a non-positive pivot raises NumericalError naming the row. */
+alsk_status alsk_dev_solve_packed_f32(const float* packed, int64_t count, int f, float* x_out,
+                                      void* stream);
+
 /* Device loss/rmse; result written to *out (host) after a stream sync. */
 alsk_status alsk_dev_loss(const alsk_csr* r, const int64_t* col_nnz, const float* x,
                           const float* theta, int64_t theta_rows, int f, double lambda,

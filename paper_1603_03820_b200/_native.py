@@ -72,6 +72,9 @@ _SIGS = {
     "alsk_dev_hermitian": (C.c_int, [CsrP, vp, i64, C.c_int, C.c_double, C.c_int, i64, i64, vp, vp, vp]),
     "alsk_dev_partial_hermitian": (C.c_int, [CsrP, vp, i64, C.c_int, C.c_double, i64, i64, vp, vp]),
     "alsk_dev_solve_packed": (C.c_int, [vp, i64, C.c_int, vp, vp]),
+    "alsk_packed_stride": (i64, [C.c_int]),
+    "alsk_dev_partial_hermitian_f32": (C.c_int, [CsrP, vp, i64, C.c_int, C.c_double, i64, i64, vp, vp]),
+    "alsk_dev_solve_packed_f32": (C.c_int, [vp, i64, C.c_int, vp, vp]),
     "alsk_dev_loss": (C.c_int, [CsrP, vp, vp, vp, i64, C.c_int, C.c_double, f64p, vp]),
     "alsk_dev_rmse": (C.c_int, [vp, vp, vp, i64, vp, i64, vp, i64, C.c_int, f64p, vp]),
     "alsk_dev_csr_to_csc": (C.c_int, [CsrP, vp, vp, vp, vp]),

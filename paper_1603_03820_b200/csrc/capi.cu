@@ -742,6 +742,34 @@ alsk_status alsk_dev_partial_hermitian(const alsk_csr* r, const float* theta, in
     });
 }
 
+int64_t alsk_packed_stride(int f) { return f < 1 ? 0 : packed_stride(f); }
+
+alsk_status alsk_dev_partial_hermitian_f32(const alsk_csr* r, const float* theta, int64_t theta_rows, int f,
+                                           double lambda, int64_t row_begin, int64_t row_end, float* out_packed,
+                                           void* stream) {
+    return guard([&] {
+        if (!tc_supported(f)) fail_input("FP32 partial Hermitians need 16 <= f <= 119 (tensor-core engine)");
+        require_device();
+        const DevCsr v = dev_view(r);
+        check_columns(v, row_begin, row_end, r->col_offset, r->col_offset + theta_rows, as_stream(stream));
+        if (!hermitian_packed_tc(v, theta, theta_rows, f, static_cast<float>(lambda), row_begin, row_end, out_packed,
+                                 as_stream(stream)))
+            fail_input("tensor-core Hermitian unavailable for this rank");
+    });
+}
+
+alsk_status alsk_dev_solve_packed_f32(const float* packed, int64_t count, int f, float* x_out, void* stream) {
+    return guard([&] {
+        if (count <= 0) return;
+        if (f < 1) fail_input("rank must be >= 1");
+        require_device();
+        cudaStream_t s = as_stream(stream);
+        StatusBufs sb(count, s);
+        packed_solve(packed, count, f, x_out, sb.st, 0, s);
+        sb.raise_if_broken(s, 0);
+    });
+}
+
 alsk_status alsk_dev_solve_packed(const double* packed, int64_t count, int f, float* x_out, void* stream) {
     return guard([&] {
         if (count <= 0) return;

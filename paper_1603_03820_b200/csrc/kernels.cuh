@@ -64,6 +64,10 @@ bool hermitian_fused_fp32(const DevCsr& r, const float* theta, int64_t theta_row
 bool tc_supported(int f);
 bool update_tc(const DevCsr& r, const float* theta, int64_t theta_rows, int f, float lambda, int64_t rb,
                int64_t re, float* x_out, const SolveStatus& st, cudaStream_t s);
+// Packed (panel-blocked) rows [rb, re) of A_u + lambda n_u I and B_u on the tensor cores into
+// out_packed (packed_stride(f) floats per row): the data-parallel split's FP32 partials.
+bool hermitian_packed_tc(const DevCsr& r, const float* theta, int64_t theta_rows, int f, float lambda, int64_t rb,
+                         int64_t re, float* out_packed, cudaStream_t s);
 bool hermitian_tc(const DevCsr& r, const float* theta, int64_t theta_rows, int f, float lambda, int64_t rb,
                   int64_t re, float* A, float* B, cudaStream_t s);
 

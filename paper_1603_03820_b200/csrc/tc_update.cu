@@ -757,6 +757,29 @@ bool update_tc(const DevCsr& r, const float* theta, int64_t theta_rows, int f, f
     return dispatch_tc<MODE_PACKED>(r, theta, theta_rows, f, lambda, rb, re, x_out, nullptr, nullptr, &st, s);
 }
 
+bool hermitian_packed_tc(const DevCsr& r, const float* theta, int64_t theta_rows, int f, float lambda, int64_t rb,
+                         int64_t re, float* out_packed, cudaStream_t s) {
+    if (!tc_supported(f)) return false;
+    if (re <= rb) return true;
+    Strided th;
+    strided(th, theta, theta_rows, f, s);
+    const int nb = (f + 1 + 7) / 8;
+#define ALSK_TC_PK(NBV)                                                                                  \
+    if (nb <= NBV) {                                                                                     \
+        PhaseTimer pt(PHASE_HERMITIAN, s);                                                               \
+        launch_tc<NBV, MODE_PACKED>(r, th.ptr, theta_rows, f, th.ldt, lambda, rb, re, nullptr, out_packed, nullptr, \
+                                    nullptr, s);                                                         \
+        return true;                                                                                     \
+    }
+    ALSK_TC_PK(5)
+    ALSK_TC_PK(7)
+    ALSK_TC_PK(10)
+    ALSK_TC_PK(13)
+    ALSK_TC_PK(15)
+#undef ALSK_TC_PK
+    return false;
+}
+
 bool hermitian_tc(const DevCsr& r, const float* theta, int64_t theta_rows, int f, float lambda, int64_t rb, int64_t re,
                   float* A, float* B, cudaStream_t s) {
     return dispatch_tc<MODE_FULL>(r, theta, theta_rows, f, lambda, rb, re, nullptr, A, B, nullptr, s);

@@ -76,11 +76,31 @@ def cuda_solve_packed(packed: torch.Tensor, count: int, f: int, out: torch.Tenso
     _check(N.LIB.alsk_dev_solve_packed(packed.data_ptr(), count, f, out.data_ptr(), _stream()))
 
 
+def packed_stride(f: int) -> int:
+    """Floats per panel-blocked packed row (kernels.cuh pb_block): for each 8-column block b,
+    rows 8b..f of 8 floats."""
+    nb = (f + 7) // 8
+    return 8 * (nb * (f + 1) - 4 * nb * (nb - 1))
+
+
+def cuda_partial_hermitian_f32(R, theta: torch.Tensor, theta_rows: int, f: int, lam: float, row_begin: int,
+                               row_end: int, out: torch.Tensor) -> None:
+    """Panel-blocked FP32 partial Hermitians (+ B) of rows [row_begin,row_end), tensor cores."""
+    _check(N.LIB.alsk_dev_partial_hermitian_f32(C.byref(R.c), theta.data_ptr(), theta_rows, f, lam, row_begin,
+                                                row_end, out.data_ptr(), _stream()))
+
+
+def cuda_solve_packed_f32(packed: torch.Tensor, count: int, f: int, out: torch.Tensor) -> None:
+    _check(N.LIB.alsk_dev_solve_packed_f32(packed.data_ptr(), count, f, out.data_ptr(), _stream()))
+
+
 @dataclass
 class Compute:
     update_rows: Callable = cuda_update_rows
     partial_hermitian: Callable = cuda_partial_hermitian
     solve_packed: Callable = cuda_solve_packed
+    partial_hermitian_f32: Callable = cuda_partial_hermitian_f32
+    solve_packed_f32: Callable = cuda_solve_packed_f32
 
 
 def _all_gather_inplace(buf: torch.Tensor, chunk_elems: int, rank: int, world: int, group=None) -> None:
@@ -138,26 +158,35 @@ class ModelParallelALS:
 
 class DataParallelThetaHalf:
     """Theta-half with a data-parallel split over users: per-item partial Hermitians from
-    the local user slab, double reduce-scatter (slice i -> rank i), solve, all-gather.
+    the local user slab, reduce-scatter (slice i -> rank i), solve, all-gather.
 
     `RT_local` is the CSR of (R restricted to this rank's users)^T, i.e. items x all users
-    with only local users' ratings; theta rows are solved for all n items."""
+    with only local users' ratings; theta rows are solved for all n items.
 
-    def __init__(self, RT_local, m: int, n: int, f: int, lam: float, group=None, compute: Optional[Compute] = None):
+    fp32=False (default): packed-lower double partials, double reduce-scatter, one rounding
+    to f32 and the reference-order solve (parallel.hpp:487-583). fp32=True: panel-blocked
+    FP32 partials from the tensor cores, FP32 reduce-scatter and the batched TMEM Cholesky
+    (the north star's FP32 tolerance; half the bytes on NVLink)."""
+
+    def __init__(self, RT_local, m: int, n: int, f: int, lam: float, group=None, compute: Optional[Compute] = None,
+                 fp32: bool = False):
         self.RT, self.m, self.n, self.f, self.lam = RT_local, m, n, f, lam
         self.group = group
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
         self.rank = dist.get_rank(group) if dist.is_initialized() else 0
         self.compute = compute or Compute()
-        self.per = f * (f + 1) // 2 + f
+        self.fp32 = fp32
+        self.per = packed_stride(f) if fp32 else f * (f + 1) // 2 + f
         self.ct, self.ts = even_slices(n, self.world)
 
     def half_theta(self, X: torch.Tensor, T_out: torch.Tensor) -> None:
         dev = X.device
-        partial = torch.zeros(self.ct * self.world * self.per, dtype=torch.float64, device=dev)
+        dt = torch.float32 if self.fp32 else torch.float64
+        partial = torch.zeros(self.ct * self.world * self.per, dtype=dt, device=dev)
         if self.n:
-            self.compute.partial_hermitian(self.RT, X, self.m, self.f, self.lam, 0, self.n, partial)
-        mine = torch.empty(self.ct * self.per, dtype=torch.float64, device=dev)
+            herm = self.compute.partial_hermitian_f32 if self.fp32 else self.compute.partial_hermitian
+            herm(self.RT, X, self.m, self.f, self.lam, 0, self.n, partial)
+        mine = torch.empty(self.ct * self.per, dtype=dt, device=dev)
         if self.world > 1:
             if dist.get_backend(self.group) == "nccl":
                 dist.reduce_scatter_tensor(mine, partial, op=dist.ReduceOp.SUM, group=self.group)
@@ -168,5 +197,6 @@ class DataParallelThetaHalf:
             mine.copy_(partial)
         rb, re = self.ts[self.rank]
         if re > rb:
-            self.compute.solve_packed(mine, re - rb, self.f, T_out[rb * self.f:])
+            solve = self.compute.solve_packed_f32 if self.fp32 else self.compute.solve_packed
+            solve(mine, re - rb, self.f, T_out[rb * self.f:])
         _all_gather_inplace(T_out, self.ct * self.f, self.rank, self.world, self.group)

@@ -85,7 +85,63 @@ def _cpu_compute():
         assert st == 0
         out[: count * f].copy_(torch.from_numpy(x))
 
-    return Compute(update_rows, partial_hermitian, solve_packed)
+    def partial_hermitian_f32(R, theta, theta_rows, f, lam, rb, re, out):
+        from paper_1603_03820_b200.distributed import packed_stride
+        X = theta.numpy()[: theta_rows * f].reshape(theta_rows, f).astype(np.float64)
+        per = packed_stride(f)
+        for v in range(rb, re):
+            k0, k1 = int(R.rp[v]), int(R.rp[v + 1])
+            xs = X[R.ci[k0:k1]]
+            a = xs.T @ xs + lam * (k1 - k0) * np.eye(f)
+            b = xs.T @ R.vv[k0:k1].astype(np.float64)
+            out[(v - rb) * per:(v - rb + 1) * per] = torch.from_numpy(pack_panel_blocked(a, b, f))
+
+    def solve_packed_f32(packed, count, f, out):
+        from paper_1603_03820_b200.distributed import packed_stride
+        per = packed_stride(f)
+        p = packed.numpy()[: count * per].reshape(count, per)
+        A = np.zeros((count, f, f), np.float32)
+        B = np.zeros((count, f), np.float32)
+        for v in range(count):
+            A[v], B[v] = unpack_panel_blocked(p[v], f)
+        st, x = orc.batch_solve(np.ascontiguousarray(A.reshape(-1)), np.ascontiguousarray(B.reshape(-1)), count, f)
+        assert st == 0
+        out[: count * f].copy_(torch.from_numpy(x))
+
+    return Compute(update_rows, partial_hermitian, solve_packed, partial_hermitian_f32, solve_packed_f32)
+
+
+def pack_panel_blocked(a, b, f):
+    """The panel-blocked packed row of kernels.cuh: for each 8-column block k, rows 8k..f of
+    8 floats (A lower, then b as row f; zeros above the diagonal and at columns >= f)."""
+    from paper_1603_03820_b200.distributed import packed_stride
+    out = np.zeros(packed_stride(f), np.float32)
+    off = 0
+    for k in range((f + 7) // 8):
+        for i in range(8 * k, f + 1):
+            for j in range(8 * k, 8 * k + 8):
+                if i < f and j <= i:
+                    out[off + 8 * (i - 8 * k) + (j - 8 * k)] = a[i, j]
+                elif i == f and j < f:
+                    out[off + 8 * (i - 8 * k) + (j - 8 * k)] = b[j]
+        off += 8 * (f + 1 - 8 * k)
+    return out
+
+
+def unpack_panel_blocked(row, f):
+    a = np.zeros((f, f), np.float32)
+    b = np.zeros(f, np.float32)
+    off = 0
+    for k in range((f + 7) // 8):
+        for i in range(8 * k, f + 1):
+            for j in range(8 * k, min(8 * k + 8, f)):
+                v = row[off + 8 * (i - 8 * k) + (j - 8 * k)]
+                if i < f and j <= i:
+                    a[i, j] = a[j, i] = v
+                elif i == f:
+                    b[j] = v
+        off += 8 * (f + 1 - 8 * k)
+    return a, b
 
 
 def _worker(rank, world, port, q):
@@ -114,8 +170,11 @@ def _worker(rank, world, port, q):
         ct, _ = even_slices(n, world)
         T_dp = torch.zeros(ct * world * f)
         dp.half_theta(X.clone(), T_dp)
+        dp32 = DataParallelThetaHalf(RTl, m, n, f, lam, compute=comp, fp32=True)
+        T_dp32 = torch.zeros(ct * world * f)
+        dp32.half_theta(X.clone(), T_dp32)
         if rank == 0:
-            q.put((X.numpy().copy(), T.numpy().copy(), T_dp[: n * f].numpy().copy()))
+            q.put((X.numpy().copy(), T.numpy().copy(), T_dp[: n * f].numpy().copy(), T_dp32[: n * f].numpy().copy()))
     finally:
         dist.destroy_process_group()
 
@@ -128,7 +187,7 @@ def test_model_and_data_parallel_gloo_world2():
     procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
     for p in procs:
         p.start()
-    X, T, T_dp = q.get(timeout=240)
+    X, T, T_dp, T_dp32 = q.get(timeout=240)
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
@@ -145,6 +204,23 @@ def test_model_and_data_parallel_gloo_world2():
     st, th_single = orc.update_x(cRT, X, m, f, lam)
     gap = np.abs(T_dp - th_single).max() / np.abs(th_single).max()
     assert gap <= 1e-6, gap
+    # FP32 panel-blocked partials, FP32 reduce-scatter: within the FP32 bar
+    gap32 = np.linalg.norm(T_dp32 - th_single) / np.linalg.norm(th_single)
+    assert gap32 <= 1e-5, gap32
+
+
+def test_panel_blocked_pack_round_trip():
+    from paper_1603_03820_b200.distributed import packed_stride
+    rng = np.random.default_rng(3)
+    for f in (1, 5, 8, 9, 16, 100):
+        m = rng.standard_normal((f, f))
+        a = (m @ m.T).astype(np.float32)
+        b = rng.standard_normal(f).astype(np.float32)
+        row = pack_panel_blocked(a, b, f)
+        assert row.size == packed_stride(f)
+        a2, b2 = unpack_panel_blocked(row, f)
+        il = np.tril_indices(f)
+        assert np.array_equal(a2[il], a[il]) and np.array_equal(b2, b)
 
 
 def test_even_slices_and_slice_cuts():

@@ -419,3 +419,9 @@ def test_distributed_paths_single_device(A, orc, gpu):
     T2 = torch.zeros(120 * 16, dtype=torch.float32, device=dev)
     dp.half_theta(X, T2)
     assert np.array_equal(T2.cpu().numpy(), t1.entries)
+    # FP32 variant: tensor-core panel-blocked partials + TMEM Cholesky, within the FP32 bar
+    dp32 = DataParallelThetaHalf(RT, 300, 120, 16, 0.05, fp32=True)
+    T3 = torch.zeros(120 * 16, dtype=torch.float32, device=dev)
+    dp32.half_theta(X, T3)
+    gap = normwise_gap(T3.cpu().numpy(), t1.entries)
+    assert gap <= FP32_TOL and gap <= 5e-5, gap

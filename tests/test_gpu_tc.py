@@ -167,3 +167,42 @@ def test_tc_long_rows_segmented_accumulation(A, orc, gpu):
     x = tc_update(A, r, th, f, 0.05)
     gap = normwise_gap(x.entries, xo)
     assert gap <= 5e-5, gap
+
+
+@pytest.mark.parametrize("f", [16, 37, 100])
+def test_tc_partial_hermitian_f32_layout(A, orc, gpu, f):
+    """alsk_dev_partial_hermitian_f32 writes the panel-blocked packed rows of kernels.cuh
+    (checked entry-wise against the double oracle through the test's own packer), and
+    alsk_dev_solve_packed_f32 solves them within the FP32 bar."""
+    import sys
+    from pathlib import Path
+    sys.path.insert(0, str(Path(__file__).resolve().parent))
+    from test_distributed import unpack_panel_blocked
+    from paper_1603_03820_b200.distributed import cuda_partial_hermitian_f32, cuda_solve_packed_f32, packed_stride
+    from paper_1603_03820_b200.session import DeviceCsr
+    m, n = 70, 800
+    lengths = [0, 1, 7, 8, 9, 33, 200, 600] * 8 + [5] * 6
+    r = rows_with_lengths(A, lengths, n, 99 + f)
+    th = A.random_factor(n, f, 17)
+    st, ao, bo = orc.hermitian(ocsr(r), th.entries, n, f, 0.05, 1, 0, m)
+    assert st == 0
+    dev = torch.device("cuda")
+    R = DeviceCsr.from_host(r, dev)
+    T = torch.from_numpy(th.entries).to(dev)
+    from paper_1603_03820_b200 import _native as N
+    per = packed_stride(f)
+    assert N.LIB.alsk_packed_stride(f) == per
+    pk = torch.empty(m * per, dtype=torch.float32, device=dev)
+    cuda_partial_hermitian_f32(R, T, n, f, 0.05, 0, m, pk)
+    rows = pk.cpu().numpy().reshape(m, per)
+    ao, bo = ao.reshape(m, f, f), bo.reshape(m, f)
+    for u in range(m):
+        a, b = unpack_panel_blocked(rows[u], f)
+        sa = max(np.abs(ao[u]).max(), 1e-30)
+        assert np.abs(a - ao[u]).max() / sa <= 1e-5, u
+        assert np.abs(b - bo[u]).max() / max(np.abs(bo[u]).max(), 1e-30) <= 1e-5, u
+    x = torch.empty(m * f, dtype=torch.float32, device=dev)
+    cuda_solve_packed_f32(pk, m, f, x)
+    st, xo = orc.update_x(ocsr(r), th.entries, n, f, 0.05, acc_double=1)
+    assert normwise_gap(x.cpu().numpy(), xo) <= 5e-5
+    assert not x.cpu().numpy().reshape(m, f)[[u for u in range(m) if lengths[u] == 0]].any()
