@@ -316,7 +316,8 @@ def run_ours(args):
             # FFMA engine (f outside the tensor-core range): one fused kernel per half
             kernel_ms = kms.value / max(kl.value, 1)
             nbk = (f + 1 + 7) // 8
-            kname = f"fused_update_kernel<{nbk}> (hermitian+bias+cholesky+solve)"
+            kname = (f"small_update_kernel<{f}> (thread or warp per row: hermitian+bias+cholesky+solve in registers)"
+                     if f <= 15 else f"fused_update_kernel<{nbk}> (hermitian+bias+cholesky+solve)")
             if f <= 32:
                 # small f is HBM-bound; algorithmic gather bytes per half
                 bytes_half = (nz_train * (4 + 4 + 4 * f) + 8 * (max(m, n) + 1)) / world

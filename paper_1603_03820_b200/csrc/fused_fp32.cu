@@ -28,6 +28,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "kernels.cuh"
 
@@ -419,6 +420,172 @@ void strided_theta(StridedTheta& t, const float* theta, int64_t theta_rows, int 
     t.ptr = t.owned.as<float>();
 }
 
+// ---- small ranks: one thread (short rows) or one warp (longer rows) per row ------------
+// The f=10 shapes (ML-1M, SparkALS: ~5 ratings per user, ~1,500 per item) are bound by the
+// gather of 4(f+2) bytes per rating from HBM; a CTA per row spends its time in launch and
+// synchronisation instead. Here a thread (WARP = false) or a warp (WARP = true: lanes take
+// every 32nd rating, then a fixed butterfly reduction) accumulates the lower triangle and
+// B in registers (FP32), adds lambda n_u, and runs the Cholesky and both triangular solves
+// in registers. Same results contract as the fused kernel (FP32 tolerance; all-zero A ->
+// x = 0, solver.hpp:215-220; first non-positive pivot reported, solver.hpp:230-235).
+template <int F, bool WARP>
+__global__ void __launch_bounds__(128)
+small_update_kernel(const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col_idx,
+                    const float* __restrict__ values, int64_t col_lo, const float* __restrict__ theta, int ldt,
+                    float lambda, int64_t rb, int64_t count, float* __restrict__ x,
+                    unsigned long long* __restrict__ min_row, int32_t* __restrict__ column,
+                    double* __restrict__ pivot, int64_t status_base) {
+    const int64_t gt = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int64_t t = WARP ? gt >> 5 : gt;
+    const int lane = WARP ? static_cast<int>(threadIdx.x & 31) : 0;
+    if (t >= count) return;  // warp-uniform in the WARP variant
+    const int64_t u = rb + t;
+    constexpr int NA = F * (F + 1) / 2;
+    constexpr int NQ = (F + 3) / 4;
+    float a[NA], b[F];
+#pragma unroll
+    for (int q = 0; q < NA; ++q) a[q] = 0.f;
+#pragma unroll
+    for (int q = 0; q < F; ++q) b[q] = 0.f;
+    const int64_t k0 = row_ptr[u], k1 = row_ptr[u + 1];
+    for (int64_t k = k0 + lane; k < k1; k += (WARP ? 32 : 1)) {
+        const int v = col_idx[k] - static_cast<int>(col_lo);
+        const float r = values[k];
+        const float4* src = reinterpret_cast<const float4*>(theta + static_cast<int64_t>(v) * ldt);
+        float th[4 * NQ];
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) {
+            const float4 w = __ldg(src + q);
+            th[4 * q] = w.x, th[4 * q + 1] = w.y, th[4 * q + 2] = w.z, th[4 * q + 3] = w.w;
+        }
+#pragma unroll
+        for (int i = 0; i < F; ++i) {
+            b[i] = fmaf(r, th[i], b[i]);
+#pragma unroll
+            for (int j = 0; j <= i; ++j) a[i * (i + 1) / 2 + j] = fmaf(th[i], th[j], a[i * (i + 1) / 2 + j]);
+        }
+    }
+    if constexpr (WARP) {  // every lane ends with the same sums (fixed butterfly order)
+#pragma unroll
+        for (int q = 0; q < NA; ++q)
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) a[q] += __shfl_xor_sync(0xffffffffu, a[q], o);
+#pragma unroll
+        for (int q = 0; q < F; ++q)
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) b[q] += __shfl_xor_sync(0xffffffffu, b[q], o);
+    }
+    const bool writer = lane == 0;
+    const float reg = lambda * static_cast<float>(k1 - k0);  // float arithmetic as solver.hpp:141,152
+    bool nz = false;
+#pragma unroll
+    for (int i = 0; i < F; ++i) {
+        a[i * (i + 1) / 2 + i] += reg;
+#pragma unroll
+        for (int j = 0; j <= i; ++j) nz |= a[i * (i + 1) / 2 + j] != 0.f;
+    }
+    float* xr = x + t * F;
+    if (!nz) {
+        if (writer) {
+#pragma unroll
+            for (int i = 0; i < F; ++i) xr[i] = 0.f;
+            column[t] = 0;
+        }
+        return;
+    }
+    // right-looking Cholesky in registers; a non-positive pivot poisons what follows, which
+    // the check below discards
+    float piv[F], dv[F];
+#pragma unroll
+    for (int c = 0; c < F; ++c) {
+        const float d = a[c * (c + 1) / 2 + c];
+        piv[c] = d;
+        const float ic = rsqrtf(d);
+        dv[c] = ic;
+        a[c * (c + 1) / 2 + c] = d * ic;
+#pragma unroll
+        for (int q = c + 1; q < F; ++q) a[q * (q + 1) / 2 + c] *= ic;
+#pragma unroll
+        for (int q = c + 1; q < F; ++q)
+#pragma unroll
+            for (int p = c + 1; p <= q; ++p)
+                a[q * (q + 1) / 2 + p] = fmaf(-a[q * (q + 1) / 2 + c], a[p * (p + 1) / 2 + c], a[q * (q + 1) / 2 + p]);
+    }
+    int bad = 0;
+    float badv = 0.f;
+#pragma unroll
+    for (int c = F - 1; c >= 0; --c)
+        if (!(piv[c] > 0.f)) {
+            bad = c + 1;
+            badv = piv[c];
+        }
+    if (bad) {
+        if (writer) {
+            column[t] = bad;
+            pivot[t] = static_cast<double>(badv);
+            atomicMin(min_row, static_cast<unsigned long long>(status_base + t));
+#pragma unroll
+            for (int i = 0; i < F; ++i) xr[i] = 0.f;
+        }
+        return;
+    }
+    // L y = b, then L^T x = y
+#pragma unroll
+    for (int i = 0; i < F; ++i) {
+        float s = b[i];
+#pragma unroll
+        for (int k = 0; k < i; ++k) s = fmaf(-a[i * (i + 1) / 2 + k], b[k], s);
+        b[i] = s * dv[i];
+    }
+#pragma unroll
+    for (int i = F - 1; i >= 0; --i) {
+        float s = b[i];
+#pragma unroll
+        for (int k = i + 1; k < F; ++k) s = fmaf(-a[k * (k + 1) / 2 + i], b[k], s);
+        b[i] = s * dv[i];
+    }
+    if (writer) {
+#pragma unroll
+        for (int i = 0; i < F; ++i) xr[i] = b[i];
+        column[t] = 0;
+    }
+}
+
+template <bool WARP>
+bool launch_small(const DevCsr& r, const float* theta, int f, int ldt, float lambda, int64_t rb, int64_t re,
+                  float* x, const SolveStatus& st, cudaStream_t s) {
+    const int64_t count = re - rb;
+    const int64_t threads = WARP ? count * 32 : count;
+    const unsigned grid = static_cast<unsigned>((threads + 127) / 128);
+#define ALSK_SMALL_CASE(FV)                                                                                  \
+    case FV:                                                                                                 \
+        small_update_kernel<FV, WARP><<<grid, 128, 0, s>>>(r.row_ptr, r.col_idx, r.values, r.col_offset, theta, \
+                                                           ldt, lambda, rb, count, x, st.min_row, st.column,    \
+                                                           st.pivot, 0);                                        \
+        ALSK_LAUNCHED();                                                                                     \
+        return true;
+    switch (f) {
+        ALSK_SMALL_CASE(1)
+        ALSK_SMALL_CASE(2)
+        ALSK_SMALL_CASE(3)
+        ALSK_SMALL_CASE(4)
+        ALSK_SMALL_CASE(5)
+        ALSK_SMALL_CASE(6)
+        ALSK_SMALL_CASE(7)
+        ALSK_SMALL_CASE(8)
+        ALSK_SMALL_CASE(9)
+        ALSK_SMALL_CASE(10)
+        ALSK_SMALL_CASE(11)
+        ALSK_SMALL_CASE(12)
+        ALSK_SMALL_CASE(13)
+        ALSK_SMALL_CASE(14)
+        ALSK_SMALL_CASE(15)
+        default:
+            return false;
+    }
+#undef ALSK_SMALL_CASE
+}
+
 template <bool SOLVE>
 bool dispatch(const DevCsr& r, const float* theta, int64_t theta_rows, int f, float lambda, int64_t rb,
               int64_t re, float* x, float* a, float* b, const SolveStatus* st, cudaStream_t s) {
@@ -447,6 +614,16 @@ bool dispatch(const DevCsr& r, const float* theta, int64_t theta_rows, int f, fl
 
 bool update_fused_fp32(const DevCsr& r, const float* theta, int64_t theta_rows, int f, float lambda, int64_t rb,
                        int64_t re, float* x_out, const SolveStatus& st, cudaStream_t s) {
+    // small ranks: a thread per row when rows average under 32 ratings, else a warp per row
+    static const bool no_small = std::getenv("ALSK_NO_SMALL_F") != nullptr;  // A/B switch
+    if (!no_small && f <= 15 && r.rows > 0) {
+        if (re <= rb) return true;
+        StridedTheta th;
+        strided_theta(th, theta, theta_rows, f, s);
+        const bool ok = r.nnz < 32 * r.rows ? launch_small<false>(r, th.ptr, f, th.ldt, lambda, rb, re, x_out, st, s)
+                                            : launch_small<true>(r, th.ptr, f, th.ldt, lambda, rb, re, x_out, st, s);
+        if (ok) return true;
+    }
     return dispatch<true>(r, theta, theta_rows, f, lambda, rb, re, x_out, nullptr, nullptr, &st, s);
 }
 
