@@ -342,7 +342,7 @@ def run_ours(args):
             "dtype": "f32", "data": "synthetic (planted rank-10 + U[-0.5,0.5) noise; SURVEY §8(d) generator)",
             "config": {"workload": args.config, "m": m, "n": n, "nnz_total": nnz, "nnz_train": nz_train, "f": f,
                        "lambda": lam, "holdout": 0.1, "parallelism": f"model-parallel rows x{world} + NCCL all-gather"
-                       if world > 1 else "single GPU", "l2": "inputs > L2 (CSR+CSC 1.4 GB), no flush",
+                       if world > 1 else "single GPU", "l2": f"inputs > L2 (CSR+CSC {2 * (8 * (m + n) / 2 + 8 * nz_train) / 1e9:.1f} GB), no flush",
                        "engine": A.fp32_engine()},
             "roofline": roof,
             "gpu_launches": int(launches),
