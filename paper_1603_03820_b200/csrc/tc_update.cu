@@ -32,9 +32,9 @@
 //                lane = rating slot, each lane copies 16-byte pieces of its gathered factor
 //                row with cp.async into a rating-major staging ring, completion counted per
 //                lane on the stage mbarrier (cp.async.mbarrier.arrive.noinc).
-// Pipelines: staging ring (raw_full / raw_empty, as deep as shared memory allows after the
-// operand ring), operand ring (hl_full / hl_empty, up to 4 deep, released by
-// tcgen05.commit) and the TMEM double buffer (tfull / tempty), one TMEM job per row segment.
+// Pipelines: staging ring (raw_full / raw_empty, 5 deep), operand ring (hl_full / hl_empty,
+// 2 deep, released by tcgen05.commit; deeper rings measured slower) and the TMEM double
+// buffer (tfull / tempty), one TMEM job per row segment.
 // The gather is the bound: ~46 cycles per 400-byte row per SM through cp.async into shared
 // memory, L2- or HBM-resident alike (scripts/probes/gather_probe.cu). Gathering into
 // registers with LDG is ~25 cycles per row in isolation, but inside this kernel (gather
