@@ -16,7 +16,8 @@ taken as TF32 = bf16/2 from MEASURED_PEAKS.json, with the FP32-FFMA-equivalent f
 north star quotes beside it, and the batched-Cholesky phase), cpu_baseline
 (the UNMODIFIED reference compiled into oracle/_ref, timed on this host's cores on a bounded
 row sample, extrapolated by nonzeros), e2e (the same metric through the host-buffer C ABI:
-alsk_update_x / alsk_update_theta on pinned host buffers, H2D + D2H inside the timed region).
+alsk_update_x / alsk_update_theta on pinned host buffers, H2D + D2H inside the timed region;
+at N > 1 GPUs each rank's input slices from pinned memory around the model-parallel step).
 """
 from __future__ import annotations
 
