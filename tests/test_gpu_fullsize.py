@@ -26,10 +26,15 @@ pytestmark = pytest.mark.gpu
 
 
 @pytest.fixture(scope="module")
-def netflix(A, gpu):
+def netflix_split(A, gpu):
     import bench
+    return bench.make_data("netflix")
+
+
+@pytest.fixture(scope="module")
+def netflix(A, gpu, netflix_split):
     from paper_1603_03820_b200.session import DeviceCsr
-    train, _ = bench.make_data("netflix")
+    train, _ = netflix_split
     dev = torch.device("cuda")
     R = DeviceCsr.from_host(train, dev)
     return train, R, dev
@@ -88,3 +93,40 @@ def test_fullsize_normal_equations(A, netflix):
         res = np.linalg.norm(Au @ x[u] - bu) / max(np.linalg.norm(bu), 1e-30)
         worst = max(worst, res)
     assert worst <= 1e-4, worst
+
+
+def _rmse(N, test, X, T, m, n, f, dev):
+    import ctypes as C
+    tt = np.ascontiguousarray(test)
+    rows = torch.from_numpy(tt["row"].copy()).to(dev)
+    cols = torch.from_numpy(tt["col"].copy()).to(dev)
+    vals = torch.from_numpy(tt["value"].copy()).to(dev)
+    out = C.c_double()
+    st = N.LIB.alsk_dev_rmse(rows.data_ptr(), cols.data_ptr(), vals.data_ptr(), len(tt), X.data_ptr(), m,
+                             T.data_ptr(), n, f, C.byref(out), torch.cuda.current_stream().cuda_stream)
+    assert st == 0
+    return out.value
+
+
+def test_fullsize_ten_iterations_rmse_parity(A, netflix, netflix_split):
+    """The north star's end-to-end bar at full size: after 10 ALS iterations from the same
+    initial factors, the tensor-core engine's test RMSE is within 1e-4 of the reference-order
+    FP64 mode's (driver.hpp:255-262 iteration order)."""
+    from paper_1603_03820_b200 import _native as N
+    from paper_1603_03820_b200.distributed import ModelParallelALS
+    from paper_1603_03820_b200.session import PREC_FP32, PREC_FP64_EXACT
+    train, R, dev = netflix
+    _, test = netflix_split
+    m, n, f, lam = train.rows, train.cols, 100, 0.05
+    RT = R.transpose()
+    x0 = torch.from_numpy(A.random_factor(m, f, 42).entries).to(dev)
+    t0 = torch.from_numpy(A.random_factor(n, f, A.mix_seed(42, 1)).entries).to(dev)
+    out = {}
+    for name, prec in (("tc", PREC_FP32), ("fp64", PREC_FP64_EXACT)):
+        with A.use_fp32_engine("tensor"):
+            als = ModelParallelALS(R, RT, m, n, f, lam, prec, x0, t0)
+            for _ in range(10):
+                als.step()
+            X, T = als.factors()
+            out[name] = _rmse(N, test, X, T, m, n, f, dev)
+    assert abs(out["tc"] - out["fp64"]) <= 1e-4, out
