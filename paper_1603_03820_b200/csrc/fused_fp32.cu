@@ -451,12 +451,24 @@ small_update_kernel(const int64_t* __restrict__ row_ptr, const int32_t* __restri
     for (int64_t k = k0 + lane; k < k1; k += (WARP ? 32 : 1)) {
         const int v = col_idx[k] - static_cast<int>(col_lo);
         const float r = values[k];
-        const float4* src = reinterpret_cast<const float4*>(theta + static_cast<int64_t>(v) * ldt);
+        // the caller's rows in place (no padded copy): 16-, 8- or 4-byte loads by F's alignment
+        const float* src = theta + static_cast<int64_t>(v) * ldt;
         float th[4 * NQ];
+        if constexpr (F % 4 == 0) {
 #pragma unroll
-        for (int q = 0; q < NQ; ++q) {
-            const float4 w = __ldg(src + q);
-            th[4 * q] = w.x, th[4 * q + 1] = w.y, th[4 * q + 2] = w.z, th[4 * q + 3] = w.w;
+            for (int q = 0; q < NQ; ++q) {
+                const float4 w = __ldg(reinterpret_cast<const float4*>(src) + q);
+                th[4 * q] = w.x, th[4 * q + 1] = w.y, th[4 * q + 2] = w.z, th[4 * q + 3] = w.w;
+            }
+        } else if constexpr (F % 2 == 0) {
+#pragma unroll
+            for (int q = 0; q < F / 2; ++q) {
+                const float2 w = __ldg(reinterpret_cast<const float2*>(src) + q);
+                th[2 * q] = w.x, th[2 * q + 1] = w.y;
+            }
+        } else {
+#pragma unroll
+            for (int q = 0; q < F; ++q) th[q] = __ldg(src + q);
         }
 #pragma unroll
         for (int i = 0; i < F; ++i) {
@@ -618,10 +630,19 @@ bool update_fused_fp32(const DevCsr& r, const float* theta, int64_t theta_rows, 
     static const bool no_small = std::getenv("ALSK_NO_SMALL_F") != nullptr;  // A/B switch
     if (!no_small && f <= 15 && r.rows > 0) {
         if (re <= rb) return true;
+        // rows read in place at stride f (a factor is never copied: at SparkALS scale X is
+        // 26 GB); only an under-aligned base pointer forces the padded copy
+        const uintptr_t need = f % 4 == 0 ? 15 : (f % 2 == 0 ? 7 : 3);
+        const float* tp = theta;
+        int ldt = f;
         StridedTheta th;
-        strided_theta(th, theta, theta_rows, f, s);
-        const bool ok = r.nnz < 32 * r.rows ? launch_small<false>(r, th.ptr, f, th.ldt, lambda, rb, re, x_out, st, s)
-                                            : launch_small<true>(r, th.ptr, f, th.ldt, lambda, rb, re, x_out, st, s);
+        if (reinterpret_cast<uintptr_t>(theta) & need) {
+            strided_theta(th, theta, theta_rows, f, s);
+            tp = th.ptr;
+            ldt = th.ldt;
+        }
+        const bool ok = r.nnz < 32 * r.rows ? launch_small<false>(r, tp, f, ldt, lambda, rb, re, x_out, st, s)
+                                            : launch_small<true>(r, tp, f, ldt, lambda, rb, re, x_out, st, s);
         if (ok) return true;
     }
     return dispatch<true>(r, theta, theta_rows, f, lambda, rb, re, x_out, nullptr, nullptr, &st, s);
