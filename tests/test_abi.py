@@ -59,3 +59,13 @@ def test_synthetic_generator_shape_and_determinism(A):
     for u in range(0, 1000, 97):
         seg = a.col_idx[a.row_ptr[u]:a.row_ptr[u + 1]]
         assert np.all(np.diff(seg) > 0) and seg.min() >= 0 and seg.max() < 300
+
+
+def test_packed_stride_matches_the_python_layout():
+    """alsk_packed_stride (C ABI, no device needed) and distributed.packed_stride agree: the
+    panel-blocked packed row of kernels.cuh, one 8-float row segment per (block, row)."""
+    from paper_1603_03820_b200 import _native as N
+    from paper_1603_03820_b200.distributed import packed_stride
+    for f in range(1, 131):
+        nb = (f + 7) // 8
+        assert N.LIB.alsk_packed_stride(f) == packed_stride(f) == sum(8 * (f + 1 - 8 * b) for b in range(nb))

@@ -206,3 +206,36 @@ def test_tc_partial_hermitian_f32_layout(A, orc, gpu, f):
     st, xo = orc.update_x(ocsr(r), th.entries, n, f, 0.05, acc_double=1)
     assert normwise_gap(x.cpu().numpy(), xo) <= 5e-5
     assert not x.cpu().numpy().reshape(m, f)[[u for u in range(m) if lengths[u] == 0]].any()
+
+
+def test_tc_partial_hermitian_f32_grid_block(A, orc, gpu):
+    """FP32 partials of a grid block (column-global indices, col_offset = its first column):
+    lambda uses the block's own n_u (parallel.hpp:412-421), so the partials of a row's blocks
+    add up to the whole row's A_u + lambda n_u I."""
+    import sys
+    from pathlib import Path
+    sys.path.insert(0, str(Path(__file__).resolve().parent))
+    from test_distributed import unpack_panel_blocked
+    from paper_1603_03820_b200.distributed import cuda_partial_hermitian_f32, packed_stride
+    from paper_1603_03820_b200.session import DeviceCsr
+    f, m, n = 24, 300, 500
+    r = A.synth_csr(m, n, 12000, 314)
+    th_full = A.random_factor(n, f, 2)
+    g = A.grid_partition(r, 2, 1)  # two column slabs, all rows (block (i, 0) at blocks[i])
+    dev = torch.device("cuda")
+    per = packed_stride(f)
+    total = np.zeros((m, per), np.float32)
+    for i in range(2):
+        blk = g.block(i, 0)
+        lo, hi = int(g.col_cuts[i]), int(g.col_cuts[i + 1])
+        assert int(blk.col_offset) == lo
+        T = torch.from_numpy(th_full.entries[lo * f:hi * f].copy()).to(dev)
+        pk = torch.empty(m * per, dtype=torch.float32, device=dev)
+        cuda_partial_hermitian_f32(DeviceCsr.from_host(blk, dev), T, hi - lo, f, 0.05, 0, m, pk)
+        total += pk.cpu().numpy().reshape(m, per)
+    st, ao, bo = orc.hermitian(ocsr(r), th_full.entries, n, f, 0.05, 1, 0, m)
+    ao, bo = ao.reshape(m, f, f), bo.reshape(m, f)
+    for u in range(0, m, 7):
+        a, b = unpack_panel_blocked(total[u], f)
+        assert np.abs(a - ao[u]).max() <= 1e-5 * max(np.abs(ao[u]).max(), 1e-30), u
+        assert np.abs(b - bo[u]).max() <= 1e-5 * max(np.abs(bo[u]).max(), 1e-30), u
