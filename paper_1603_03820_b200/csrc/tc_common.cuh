@@ -179,6 +179,11 @@ __device__ __forceinline__ uint32_t kmajor_offset(int i, int k) {
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(src) : "memory");
 }
+// The same copy allocating in L1 (the other 16-byte half of a 32-byte sector, copied by the
+// next loader warp, then hits L1 instead of requesting the sector from L2 again).
+__device__ __forceinline__ void cp_async16_ca(uint32_t dst, const void* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(src) : "memory");
+}
 // Arrive on `bar` once all cp.async issued so far by this thread have landed; the arrival
 // counts against the barrier's expected count.
 __device__ __forceinline__ void cp_async_arrive_noinc(uint64_t* bar) {

@@ -335,7 +335,11 @@ tc_update_kernel(const float* __restrict__ theta, int ldt, const int64_t* __rest
                     if (lane < ci.cnt) {
                         const float* src = theta + static_cast<int64_t>(v) * ldt;
                         const uint32_t dst = smem_u32(my);
-                        for (int c = ldr; c < n16; c += NLOAD) cp_async16(dst + c * 16, src + 4 * c);
+                        if (dry & 64u) {
+                            for (int c = ldr; c < n16; c += NLOAD) cp_async16(dst + c * 16, src + 4 * c);
+                        } else {
+                            for (int c = ldr; c < n16; c += NLOAD) cp_async16_ca(dst + c * 16, src + 4 * c);
+                        }
                     } else if (lane < kend) {
                         for (int c = ldr; c < n16; c += NLOAD)
                             *reinterpret_cast<float4*>(my + c * 16) = make_float4(0.f, 0.f, 0.f, 0.f);
