@@ -32,7 +32,7 @@
 //                lane = rating slot, each lane copies 16-byte pieces of its gathered factor
 //                row with cp.async into a rating-major staging ring, completion counted per
 //                lane on the stage mbarrier (cp.async.mbarrier.arrive.noinc).
-// Pipelines: staging ring (raw_full / raw_empty, 5 deep), operand ring (hl_full / hl_empty,
+// Pipelines: staging ring (raw_full / raw_empty, 6 deep), operand ring (hl_full / hl_empty,
 // 2 deep, released by tcgen05.commit; deeper rings measured slower) and the TMEM double
 // buffer (tfull / tempty), one TMEM job per row segment.
 // The gather is the bound: ~46 cycles per 400-byte row per SM through cp.async into shared
@@ -602,7 +602,7 @@ void launch_tc(const DevCsr& r, const float* theta, int64_t theta_rows, int f, i
     }();
     static const int max_stages = [] {
         const char* e = std::getenv("ALSK_TC_STAGES");
-        return e ? std::max(2, std::min(8, std::atoi(e))) : 5;  // 4-6 within noise, 3 and 2 slower
+        return e ? std::max(2, std::min(8, std::atoi(e))) : 6;  // 4-6 within noise (6 best with cp.async.ca), 3, 2, 7 slower
     }();
     int hls = max_hls, stages = max_stages;
     for (;;) {
