@@ -240,6 +240,18 @@ alsk_status alsk_dev_partial_hermitian_f32(const alsk_csr* r, const float* theta
 alsk_status alsk_dev_solve_packed_f32(const float* packed, int64_t count, int f, float* x_out,
                                       void* stream);
 
+/* Binary ratings cache (replaces save_binary_cache / load_binary_cache, dataio.hpp:116-163):
+ * header of five little-endian u64 (magic "ALSKCACH", version 1, rows, cols, nnz), then
+ * row_ptr int64[rows+1], col_idx int32[nnz], values f32[nnz]. Loads validate the CSR like
+ * the reference (IoError "<path>: corrupt cache (<validate message>)"). alsk_dev_load_cache
+ * streams the file into device buffers through pinned staging (read overlapped with the
+ * upload). */
+alsk_status alsk_cache_header(const char* path, int64_t* rows, int64_t* cols, int64_t* nnz);
+alsk_status alsk_save_cache(const alsk_csr* r, const char* path);
+alsk_status alsk_load_cache(const char* path, int64_t* row_ptr, int32_t* col_idx, float* values);
+alsk_status alsk_dev_load_cache(const char* path, int64_t* row_ptr, int32_t* col_idx, float* values,
+                                void* stream);
+
 /* Device loss/rmse; result written to *out (host) after a stream sync. */
 alsk_status alsk_dev_loss(const alsk_csr* r, const int64_t* col_nnz, const float* x,
                           const float* theta, int64_t theta_rows, int f, double lambda,

@@ -186,6 +186,18 @@ class Reference(_Lib):
     def hardware_threads(self) -> int:
         return int(self.call("hardware_threads"))
 
+    def save_cache(self, csr, path: str) -> int:
+        return self.call("save_cache", C.byref(csr), str(path).encode())
+
+    def load_cache(self, path: str, cap_rows: int, cap_nnz: int):
+        rows, cols, nnz = C.c_int64(), C.c_int64(), C.c_int64()
+        rp = np.zeros(cap_rows + 1, np.int64)
+        ci = np.zeros(max(cap_nnz, 1), np.int32)
+        vv = np.zeros(max(cap_nnz, 1), np.float32)
+        st = self.call("load_cache", str(path).encode(), C.byref(rows), C.byref(cols), C.byref(nnz), _p(rp), _p(ci),
+                       _p(vv), C.c_int64(cap_rows), C.c_int64(cap_nnz))
+        return st, rows.value, cols.value, rp[: rows.value + 1], ci[: nnz.value], vv[: nnz.value]
+
     def hermitian_mo(self, csr, theta, theta_rows, f, lam, acc_double, rb, re, bin=16):
         A = np.zeros((re - rb) * f * f, np.float32)
         B = np.zeros((re - rb) * f, np.float32)

@@ -264,4 +264,24 @@ alsk_status ref_plan_partition(int64_t m, int64_t n, int64_t nnz, int f, int wor
     });
 }
 
+// binary ratings cache, the reference's own writer/reader (dataio.hpp:116-163), for
+// cross-checking the repo's implementation file for file
+alsk_status ref_save_cache(const alsk_csr* a, const char* path) {
+    return guarded([&] { R::save_binary_cache(to_csr(a), path); });
+}
+alsk_status ref_load_cache(const char* path, int64_t* rows, int64_t* cols, int64_t* nnz, int64_t* row_ptr,
+                           int32_t* col_idx, float* vals, int64_t cap_rows, int64_t cap_nnz) {
+    return guarded([&] {
+        const R::CsrMatrix a = R::load_binary_cache(path);
+        *rows = a.rows;
+        *cols = a.cols;
+        *nnz = a.nnz();
+        if (a.rows <= cap_rows && a.nnz() <= cap_nnz) {
+            std::memcpy(row_ptr, a.row_ptr.data(), sizeof(int64_t) * a.row_ptr.size());
+            std::memcpy(col_idx, a.col_idx.data(), sizeof(int32_t) * a.col_idx.size());
+            std::memcpy(vals, a.values.data(), sizeof(float) * a.values.size());
+        }
+    });
+}
+
 }  // extern "C"

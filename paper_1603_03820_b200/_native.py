@@ -73,6 +73,10 @@ _SIGS = {
     "alsk_dev_partial_hermitian": (C.c_int, [CsrP, vp, i64, C.c_int, C.c_double, i64, i64, vp, vp]),
     "alsk_dev_solve_packed": (C.c_int, [vp, i64, C.c_int, vp, vp]),
     "alsk_packed_stride": (i64, [C.c_int]),
+    "alsk_cache_header": (C.c_int, [C.c_char_p, C.POINTER(i64), C.POINTER(i64), C.POINTER(i64)]),
+    "alsk_save_cache": (C.c_int, [CsrP, C.c_char_p]),
+    "alsk_load_cache": (C.c_int, [C.c_char_p, vp, vp, vp]),
+    "alsk_dev_load_cache": (C.c_int, [C.c_char_p, vp, vp, vp, vp]),
     "alsk_dev_partial_hermitian_f32": (C.c_int, [CsrP, vp, i64, C.c_int, C.c_double, i64, i64, vp, vp]),
     "alsk_dev_solve_packed_f32": (C.c_int, [vp, i64, C.c_int, vp, vp]),
     "alsk_dev_loss": (C.c_int, [CsrP, vp, vp, vp, i64, C.c_int, C.c_double, f64p, vp]),

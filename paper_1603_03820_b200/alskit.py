@@ -9,6 +9,7 @@ from __future__ import annotations
 
 import ctypes as C
 import enum
+import os
 from dataclasses import dataclass, field
 from typing import Callable, Optional, Sequence
 
@@ -492,6 +493,32 @@ def synth_csr(m: int, n: int, nnz: int, seed: int, threads: int = 0) -> CsrMatri
     if st != 0:
         raise InputError("invalid synthetic shape")
     return CsrMatrix(m, n, 0, rp, ci, va)
+
+
+# ---------------------------------------------------------------- binary ratings cache
+def cache_header(path) -> tuple:
+    """(rows, cols, nnz) of a binary ratings cache, after the reference's header checks
+    (dataio.hpp:133-150: magic, version, bounds, exact file size)."""
+    r, c, z = C.c_int64(), C.c_int64(), C.c_int64()
+    _check(LIB.alsk_cache_header(os.fsencode(path), C.byref(r), C.byref(c), C.byref(z)))
+    return r.value, c.value, z.value
+
+
+def save_binary_cache(a: CsrMatrix, path) -> None:
+    """dataio.hpp:116-128. col_offset is not part of the format."""
+    c = a._c()
+    _check(LIB.alsk_save_cache(C.byref(c), os.fsencode(path)))
+
+
+def load_binary_cache(path) -> CsrMatrix:
+    """dataio.hpp:133-163: bit-identical to the saved matrix; truncation, bad magic/version,
+    a size mismatch or CSR invariant violations raise IoError naming the file."""
+    rows, cols, nnz = cache_header(path)
+    rp = np.empty(rows + 1, np.int64)
+    ci = np.empty(nnz, np.int32)
+    va = np.empty(nnz, np.float32)
+    _check(LIB.alsk_load_cache(os.fsencode(path), _p(rp), _p(ci), _p(va)))
+    return CsrMatrix(rows, cols, 0, rp, ci, va)
 
 
 FP32_ENGINES = {"auto": 0, "ffma": 1, "tensor": 2}

@@ -13,6 +13,7 @@
 
 #include "alskit_cuda.h"
 #include "kernels.cuh"
+#include "cache_io.cuh"
 
 namespace alsk {
 
@@ -913,6 +914,102 @@ void alsk_session_destroy(alsk_session* S) {
         cudaDeviceSynchronize();
         cudaStreamDestroy(s);
     }
+}
+
+// ---- binary ratings cache (dataio.hpp:108-163; helpers in cache_io.cuh) ----
+
+alsk_status alsk_cache_header(const char* path, int64_t* rows, int64_t* cols, int64_t* nnz) {
+    return guard([&] {
+        File in(path, "rb");
+        const Header h = read_header(in);
+        *rows = static_cast<int64_t>(h.rows);
+        *cols = static_cast<int64_t>(h.cols);
+        *nnz = static_cast<int64_t>(h.nnz);
+    });
+}
+
+alsk_status alsk_save_cache(const alsk_csr* r, const char* path) {
+    return guard([&] {
+        File out(path, "wb");
+        const uint64_t h[5] = {kMagic, kVersion, static_cast<uint64_t>(r->rows), static_cast<uint64_t>(r->cols),
+                               static_cast<uint64_t>(r->nnz)};
+        out.write(h, sizeof(h));
+        out.write(r->row_ptr, sizeof(int64_t) * (r->rows + 1));
+        out.write(r->col_idx, sizeof(int32_t) * r->nnz);
+        out.write(r->values, sizeof(float) * r->nnz);
+        if (std::fflush(out.f) != 0) fail_io(std::string("write failed for ") + path);
+    });
+}
+
+// Host buffers (sizes from alsk_cache_header).
+alsk_status alsk_load_cache(const char* path, int64_t* row_ptr, int32_t* col_idx, float* values) {
+    return guard([&] {
+        File in(path, "rb");
+        const Header h = read_header(in);
+        const int64_t rows = static_cast<int64_t>(h.rows), nnz = static_cast<int64_t>(h.nnz);
+        in.read(row_ptr, sizeof(int64_t) * (rows + 1), "row_ptr");
+        in.read(col_idx, sizeof(int32_t) * nnz, "col_idx");
+        in.read(values, sizeof(float) * nnz, "values");
+        Validator val{row_ptr, rows, static_cast<int64_t>(h.cols), nnz, in.path};
+        val.ends();
+        val.feed(col_idx, 0, nnz);
+    });
+}
+
+// Device buffers: row_ptr[rows+1], col_idx[nnz], values[nnz] (sizes from alsk_cache_header).
+alsk_status alsk_dev_load_cache(const char* path, int64_t* row_ptr, int32_t* col_idx, float* values, void* stream) {
+    return guard([&] {
+        require_device();
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        File in(path, "rb");
+        const Header h = read_header(in);
+        const int64_t rows = static_cast<int64_t>(h.rows), nnz = static_cast<int64_t>(h.nnz);
+        std::vector<int64_t> rp(static_cast<size_t>(rows) + 1);
+        in.read(rp.data(), sizeof(int64_t) * rp.size(), "row_ptr");
+        Validator val{rp.data(), rows, static_cast<int64_t>(h.cols), nnz, in.path};
+        val.ends();
+        ALSK_CUDA(cudaMemcpyAsync(row_ptr, rp.data(), sizeof(int64_t) * rp.size(), cudaMemcpyHostToDevice, s));
+        // two pinned staging buffers, 64 MB each: read chunk k+1 while chunk k uploads
+        constexpr size_t kChunk = size_t(64) << 20;
+        void* stage[2] = {nullptr, nullptr};
+        cudaEvent_t done[2] = {nullptr, nullptr};
+        struct Cleanup {
+            void** st;
+            cudaEvent_t* ev;
+            cudaStream_t s;
+            ~Cleanup() {
+                cudaStreamSynchronize(s);
+                for (int i = 0; i < 2; ++i) {
+                    if (st[i]) cudaFreeHost(st[i]);
+                    if (ev[i]) cudaEventDestroy(ev[i]);
+                }
+            }
+        } cleanup{stage, done, s};
+        for (int i = 0; i < 2; ++i) {
+            ALSK_CUDA(cudaMallocHost(&stage[i], kChunk));
+            ALSK_CUDA(cudaEventCreateWithFlags(&done[i], cudaEventDisableTiming));
+        }
+        int buf = 0;
+        auto stream_array = [&](void* dst, size_t elem, int64_t count, const char* what, bool validate) {
+            const int64_t per = static_cast<int64_t>(kChunk / elem);
+            for (int64_t k0 = 0; k0 < count; k0 += per, buf ^= 1) {
+                const int64_t k1 = std::min(count, k0 + per);
+                ALSK_CUDA(cudaEventSynchronize(done[buf]));  // the previous upload from this buffer is done
+                in.read(stage[buf], elem * (k1 - k0), what);
+                if (validate) {
+                    val.feed(static_cast<const int32_t*>(stage[buf]), k0, k1);
+                    val.last = static_cast<const int32_t*>(stage[buf])[k1 - k0 - 1];
+                }
+                ALSK_CUDA(cudaMemcpyAsync(static_cast<char*>(dst) + elem * k0, stage[buf], elem * (k1 - k0),
+                                          cudaMemcpyHostToDevice, s));
+                ALSK_CUDA(cudaEventRecord(done[buf], s));
+            }
+        };
+        stream_array(col_idx, sizeof(int32_t), nnz, "col_idx", true);
+        val.feed(nullptr, nnz, nnz);  // rows with no entries after the last chunk
+        stream_array(values, sizeof(float), nnz, "values", false);
+        ALSK_CUDA(cudaStreamSynchronize(s));
+    });
 }
 
 }  // extern "C"

@@ -9,13 +9,15 @@ only for device allocation and the current stream; every kernel is libalskit_cud
 from __future__ import annotations
 
 import ctypes as C
+import os
 from typing import Optional
 
 import numpy as np
 import torch
 
 from . import _native as N
-from .alskit import (TRIPLET_DTYPE, CscMatrix, CsrMatrix, FactorMatrix, SolverConfig, _check)
+from .alskit import (TRIPLET_DTYPE, CscMatrix, CsrMatrix, FactorMatrix, SolverConfig, _check,
+                     cache_header)
 
 LIB = N.LIB
 PREC_FP64_EXACT = 0
@@ -43,6 +45,18 @@ class DeviceCsr:
     @staticmethod
     def from_host(r: CsrMatrix, device) -> "DeviceCsr":
         return DeviceCsr(r.rows, r.cols, r.row_ptr, r.col_idx, r.values, device, r.col_offset)
+
+    @staticmethod
+    def from_cache(path, device) -> "DeviceCsr":
+        """Load a binary ratings cache (dataio.hpp:133-163) straight into HBM: the file is
+        streamed through pinned staging and validated on the host as it passes."""
+        rows, cols, nnz = cache_header(path)
+        rp = torch.empty(rows + 1, dtype=torch.int64, device=device)
+        ci = torch.empty(max(nnz, 1), dtype=torch.int32, device=device)
+        va = torch.empty(max(nnz, 1), dtype=torch.float32, device=device)
+        _check(LIB.alsk_dev_load_cache(os.fsencode(path), rp.data_ptr(), ci.data_ptr(), va.data_ptr(),
+                                       stream_handle()))
+        return DeviceCsr(rows, cols, rp, ci[:nnz], va[:nnz], device)
 
     def transpose(self) -> "DeviceCsr":
         """Stable device transpose (csr_to_csc, sparse.hpp:185-207) viewed as the CSR of R^T."""
