@@ -3,6 +3,8 @@
 // libalskit_cuda.so. Exit code 0 = all passed; prints one line per failure.
 #include <cmath>
 #include <cstdio>
+#include <filesystem>
+#include <unistd.h>
 #include <random>
 #include <set>
 #include <string>
@@ -72,6 +74,26 @@ int main() {
         const GridPartition g = grid_partition(id, 2, 2);
         CHECK(g.block(0, 0).nnz() == 2 && g.block(1, 1).nnz() == 2 && g.block(1, 0).nnz() == 0);
         CHECK(g.block(1, 1).col_offset == 2 && (g.block(1, 1).col_idx == std::vector<index_t>{2, 3}));
+    }
+    // ---- binary cache (test_dataio.cpp:112-146) ----
+    {
+        std::mt19937_64 rng(17);
+        const CsrMatrix a = csr_from_triplets(11, 23, random_triplets(rng, 11, 23, 140));
+        const auto dir = std::filesystem::temp_directory_path() / ("alsk_dropin_" + std::to_string(::getpid()));
+        std::filesystem::create_directories(dir);
+        const auto path = dir / "r.cache";
+        save_binary_cache(a, path);
+        const CsrMatrix b = load_binary_cache(path);
+        CHECK(a.rows == b.rows && a.cols == b.cols && a.row_ptr == b.row_ptr && a.col_idx == b.col_idx &&
+              a.values == b.values);
+        std::filesystem::resize_file(path, std::filesystem::file_size(path) - 5);
+        CHECK(throws_with<IoError>([&] { load_binary_cache(path); }, "cache size does not match its header"));
+        const auto junk = dir / "junk.cache";
+        std::FILE* fj = std::fopen(junk.c_str(), "wb");
+        std::fputs("this is not a cache file at all, but long enough to read", fj);
+        std::fclose(fj);
+        CHECK(throws_with<IoError>([&] { load_binary_cache(junk); }, "bad magic"));
+        std::filesystem::remove_all(dir);
     }
     // ---- solver (test_solver.cpp) ----
     {
