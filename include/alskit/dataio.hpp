@@ -1,12 +1,15 @@
-// alskit drop-in (B200): the binary ratings cache of the reference's
-// proj/include/alskit/dataio.hpp:116-163, served by libalskit_cuda.so (same file format,
-// same IoError texts). The other dataio.hpp members (text loaders, split, checkpoints,
-// BlockStream) are outside the hot-path scope.
+// alskit drop-in (B200): the binary ratings cache and the factor checkpoints of the
+// reference's proj/include/alskit/dataio.hpp:116-163 and 546-786, served by
+// libalskit_cuda.so (same file formats, names and IoError texts). The other dataio.hpp
+// members (text loaders, split, BlockStream) are outside the hot-path scope.
 #pragma once
 
 #include <filesystem>
+#include <optional>
+#include <string>
 
 #include "alskit/common.hpp"
+#include "alskit/factor.hpp"
 #include "alskit/sparse.hpp"
 
 namespace alskit {
@@ -31,5 +34,99 @@ inline CsrMatrix load_binary_cache(const std::filesystem::path& path) {
     detail::check(alsk_load_cache(path.c_str(), a.row_ptr.data(), a.col_idx.data(), a.values.data()));
     return a;
 }
+
+// ---- checkpoints (dataio.hpp:546-786) ----
+
+enum class FactorKind { x = 0, theta = 1 };  // dataio.hpp:548
+
+inline const char* factor_kind_name(FactorKind k) noexcept { return k == FactorKind::x ? "x" : "theta"; }
+
+struct Checkpoint {  // dataio.hpp:556-561
+    int iteration = 0;
+    FactorKind which = FactorKind::x;
+    FactorMatrix factor;
+    std::uint64_t digest = 0;
+};
+
+inline std::filesystem::path checkpoint_path(const std::filesystem::path& dir, int iteration, FactorKind which) {
+    char buf[4096];
+    detail::check(alsk_checkpoint_path(dir.c_str(), iteration, static_cast<int>(which), buf, sizeof buf));
+    return buf;
+}
+
+/// dataio.hpp:600-624: temp file + rename; returns the final path.
+inline std::filesystem::path write_checkpoint(const Checkpoint& cp, const std::filesystem::path& dir) {
+    detail::check(alsk_checkpoint_write(dir.c_str(), cp.iteration, static_cast<int>(cp.which), cp.factor.rows,
+                                        cp.factor.f, cp.digest, cp.factor.entries.data()));
+    return checkpoint_path(dir, cp.iteration, cp.which);
+}
+
+/// dataio.hpp:627-651
+inline Checkpoint read_checkpoint(const std::filesystem::path& path) {
+    int iteration = 0, which = 0, f = 0;
+    std::int64_t rows = 0;
+    std::uint64_t digest = 0;
+    detail::check(alsk_checkpoint_header(path.c_str(), &iteration, &which, &rows, &f, &digest));
+    Checkpoint cp;
+    cp.iteration = iteration;
+    cp.which = static_cast<FactorKind>(which);
+    cp.factor = FactorMatrix(rows, f);
+    cp.digest = digest;
+    detail::check(alsk_checkpoint_read(path.c_str(), cp.factor.entries.data()));
+    return cp;
+}
+
+namespace detail {
+inline std::optional<std::filesystem::path> latest_of(const std::filesystem::path& dir, int which) {
+    char buf[4096];
+    int found = 0;
+    check(alsk_checkpoint_latest(dir.c_str(), which, buf, sizeof buf, &found));
+    if (!found) return std::nullopt;
+    return std::filesystem::path(buf);
+}
+}  // namespace detail
+
+/// dataio.hpp:659-686
+inline std::optional<Checkpoint> restore_latest(const std::filesystem::path& dir,
+                                                std::optional<std::uint64_t> expected_digest = std::nullopt) {
+    const auto p = detail::latest_of(dir, -1);
+    if (!p) return std::nullopt;
+    Checkpoint cp = read_checkpoint(*p);
+    if (expected_digest && cp.digest != *expected_digest)
+        throw InputError(p->string() + ": checkpoint config digest mismatch (run has " +
+                         std::to_string(*expected_digest) + ", checkpoint has " + std::to_string(cp.digest) + ")");
+    return cp;
+}
+
+/// dataio.hpp:689-708
+inline std::optional<Checkpoint> restore_latest_of(const std::filesystem::path& dir, FactorKind which) {
+    const auto p = detail::latest_of(dir, static_cast<int>(which));
+    if (!p) return std::nullopt;
+    return read_checkpoint(*p);
+}
+
+/// dataio.hpp:717-786: one background writer, at most one write in flight, sticky errors.
+/// submit_device() is the B200 addition: the factor is snapshotted from HBM on `stream`.
+class CheckpointWriter {
+  public:
+    explicit CheckpointWriter(const std::filesystem::path& dir) { detail::check(alsk_ckpt_writer_create(dir.c_str(), &h_)); }
+    ~CheckpointWriter() { alsk_ckpt_writer_destroy(h_); }
+    CheckpointWriter(const CheckpointWriter&) = delete;
+    CheckpointWriter& operator=(const CheckpointWriter&) = delete;
+
+    void submit(const Checkpoint& cp) {
+        detail::check(alsk_ckpt_writer_submit_host(h_, cp.iteration, static_cast<int>(cp.which), cp.factor.rows,
+                                                   cp.factor.f, cp.digest, cp.factor.entries.data()));
+    }
+    void submit_device(int iteration, FactorKind which, const real_t* d_factor, offset_t rows, int f,
+                       std::uint64_t digest, void* stream = nullptr) {
+        detail::check(alsk_ckpt_writer_submit_device(h_, iteration, static_cast<int>(which), rows, f, digest,
+                                                     d_factor, stream));
+    }
+    void flush() { detail::check(alsk_ckpt_writer_flush(h_)); }
+
+  private:
+    void* h_ = nullptr;
+};
 
 }  // namespace alskit

@@ -252,6 +252,32 @@ alsk_status alsk_load_cache(const char* path, int64_t* row_ptr, int32_t* col_idx
 alsk_status alsk_dev_load_cache(const char* path, int64_t* row_ptr, int32_t* col_idx, float* values,
                                 void* stream);
 
+/* Factor checkpoints (replace write_checkpoint / read_checkpoint / restore_latest /
+ * CheckpointWriter, dataio.hpp:546-786): same file format (56-byte header: magic "ALSKCPKT",
+ * version, iteration, which (0 = x, 1 = theta), rows, f, digest; then rows*f f32), same
+ * ckpt_%06d_{x,theta}.bin names, atomic temp+rename, same IoError texts. */
+alsk_status alsk_checkpoint_write(const char* dir, int iteration, int which, int64_t rows, int f, uint64_t digest,
+                                  const float* entries);
+alsk_status alsk_checkpoint_path(const char* dir, int iteration, int which, char* out, size_t cap);
+alsk_status alsk_checkpoint_header(const char* path, int* iteration, int* which, int64_t* rows, int* f,
+                                   uint64_t* digest);
+alsk_status alsk_checkpoint_read(const char* path, float* entries);
+alsk_status alsk_dev_checkpoint_read(const char* path, float* d_entries, void* stream);
+/* which = -1: newest of either kind (theta outranks x at the same iteration); 0 / 1: that
+ * kind only. *found = 0 when the directory holds none. */
+alsk_status alsk_checkpoint_latest(const char* dir, int which, char* out, size_t cap, int* found);
+/* Background writer: submit_device orders a D2H copy of the factor after `stream` on a
+ * private copy stream into pinned memory and returns; one worker thread writes the file.
+ * At most one snapshot in flight (submit waits for the previous write); write errors are
+ * sticky and returned by the next submit or flush. */
+alsk_status alsk_ckpt_writer_create(const char* dir, void** writer);
+alsk_status alsk_ckpt_writer_submit_device(void* writer, int iteration, int which, int64_t rows, int f,
+                                           uint64_t digest, const float* d_factor, void* stream);
+alsk_status alsk_ckpt_writer_submit_host(void* writer, int iteration, int which, int64_t rows, int f,
+                                         uint64_t digest, const float* entries);
+alsk_status alsk_ckpt_writer_flush(void* writer);
+void alsk_ckpt_writer_destroy(void* writer);
+
 /* Device loss/rmse; result written to *out (host) after a stream sync. */
 alsk_status alsk_dev_loss(const alsk_csr* r, const int64_t* col_nnz, const float* x,
                           const float* theta, int64_t theta_rows, int f, double lambda,

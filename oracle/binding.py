@@ -189,6 +189,24 @@ class Reference(_Lib):
     def save_cache(self, csr, path: str) -> int:
         return self.call("save_cache", C.byref(csr), str(path).encode())
 
+    def write_checkpoint(self, dir: str, iteration, which, rows, f, digest, entries) -> int:
+        e = np.ascontiguousarray(entries, np.float32)
+        return self.call("write_checkpoint", str(dir).encode(), C.c_int(iteration), C.c_int(which), C.c_int64(rows),
+                         C.c_int(f), C.c_uint64(digest), _p(e))
+
+    def read_checkpoint(self, path: str, cap: int):
+        it, wh, f = C.c_int(), C.c_int(), C.c_int()
+        rows, dg = C.c_int64(), C.c_uint64()
+        e = np.zeros(max(cap, 1), np.float32)
+        st = self.call("read_checkpoint", str(path).encode(), C.byref(it), C.byref(wh), C.byref(rows), C.byref(f),
+                       C.byref(dg), _p(e), C.c_int64(cap))
+        return st, it.value, wh.value, rows.value, f.value, dg.value, e[: rows.value * f.value]
+
+    def restore_latest(self, dir: str):
+        it, wh, found = C.c_int(), C.c_int(), C.c_int()
+        st = self.call("restore_latest_iteration", str(dir).encode(), C.byref(it), C.byref(wh), C.byref(found))
+        return st, (it.value, wh.value) if found.value else None
+
     def load_cache(self, path: str, cap_rows: int, cap_nnz: int):
         rows, cols, nnz = C.c_int64(), C.c_int64(), C.c_int64()
         rp = np.zeros(cap_rows + 1, np.int64)

@@ -284,4 +284,42 @@ alsk_status ref_load_cache(const char* path, int64_t* rows, int64_t* cols, int64
     });
 }
 
+// checkpoints, the reference's own writer/reader (dataio.hpp:600-651) and restore_latest
+// (dataio.hpp:659-686), for cross-checking file for file
+alsk_status ref_write_checkpoint(const char* dir, int iteration, int which, int64_t rows, int f, uint64_t digest,
+                                 const float* entries) {
+    return guarded([&] {
+        R::Checkpoint cp;
+        cp.iteration = iteration;
+        cp.which = static_cast<R::FactorKind>(which);
+        cp.factor = R::FactorMatrix(rows, f);
+        std::memcpy(cp.factor.entries.data(), entries, sizeof(float) * rows * f);
+        cp.digest = digest;
+        R::write_checkpoint(cp, dir);
+    });
+}
+alsk_status ref_read_checkpoint(const char* path, int* iteration, int* which, int64_t* rows, int* f,
+                                uint64_t* digest, float* entries, int64_t cap) {
+    return guarded([&] {
+        const R::Checkpoint cp = R::read_checkpoint(path);
+        *iteration = cp.iteration;
+        *which = static_cast<int>(cp.which);
+        *rows = cp.factor.rows;
+        *f = cp.factor.f;
+        *digest = cp.digest;
+        if (static_cast<int64_t>(cp.factor.entries.size()) <= cap)
+            std::memcpy(entries, cp.factor.entries.data(), sizeof(float) * cp.factor.entries.size());
+    });
+}
+alsk_status ref_restore_latest_iteration(const char* dir, int* iteration, int* which, int* found) {
+    return guarded([&] {
+        const auto cp = R::restore_latest(dir);
+        *found = cp ? 1 : 0;
+        if (cp) {
+            *iteration = cp->iteration;
+            *which = static_cast<int>(cp->which);
+        }
+    });
+}
+
 }  // extern "C"

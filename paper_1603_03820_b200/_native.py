@@ -77,6 +77,18 @@ _SIGS = {
     "alsk_save_cache": (C.c_int, [CsrP, C.c_char_p]),
     "alsk_load_cache": (C.c_int, [C.c_char_p, vp, vp, vp]),
     "alsk_dev_load_cache": (C.c_int, [C.c_char_p, vp, vp, vp, vp]),
+    "alsk_checkpoint_write": (C.c_int, [C.c_char_p, C.c_int, C.c_int, i64, C.c_int, C.c_uint64, vp]),
+    "alsk_checkpoint_path": (C.c_int, [C.c_char_p, C.c_int, C.c_int, C.c_char_p, C.c_size_t]),
+    "alsk_checkpoint_header": (C.c_int, [C.c_char_p, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(i64),
+                                         C.POINTER(C.c_int), C.POINTER(C.c_uint64)]),
+    "alsk_checkpoint_read": (C.c_int, [C.c_char_p, vp]),
+    "alsk_dev_checkpoint_read": (C.c_int, [C.c_char_p, vp, vp]),
+    "alsk_checkpoint_latest": (C.c_int, [C.c_char_p, C.c_int, C.c_char_p, C.c_size_t, C.POINTER(C.c_int)]),
+    "alsk_ckpt_writer_create": (C.c_int, [C.c_char_p, C.POINTER(vp)]),
+    "alsk_ckpt_writer_submit_device": (C.c_int, [vp, C.c_int, C.c_int, i64, C.c_int, C.c_uint64, vp, vp]),
+    "alsk_ckpt_writer_submit_host": (C.c_int, [vp, C.c_int, C.c_int, i64, C.c_int, C.c_uint64, vp]),
+    "alsk_ckpt_writer_flush": (C.c_int, [vp]),
+    "alsk_ckpt_writer_destroy": (None, [vp]),
     "alsk_dev_partial_hermitian_f32": (C.c_int, [CsrP, vp, i64, C.c_int, C.c_double, i64, i64, vp, vp]),
     "alsk_dev_solve_packed_f32": (C.c_int, [vp, i64, C.c_int, vp, vp]),
     "alsk_dev_loss": (C.c_int, [CsrP, vp, vp, vp, i64, C.c_int, C.c_double, f64p, vp]),

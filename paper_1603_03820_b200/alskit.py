@@ -521,6 +521,78 @@ def load_binary_cache(path) -> CsrMatrix:
     return CsrMatrix(rows, cols, 0, rp, ci, va)
 
 
+# ---------------------------------------------------------------- checkpoints (dataio.hpp:546-708)
+class FactorKind(enum.IntEnum):
+    """dataio.hpp:548: theta outranks x at the same iteration."""
+    x = 0
+    theta = 1
+
+
+@dataclass
+class Checkpoint:
+    """dataio.hpp:556-561"""
+    iteration: int = 0
+    which: FactorKind = FactorKind.x
+    factor: FactorMatrix = field(default_factory=lambda: FactorMatrix(0, 1, np.zeros(0, np.float32)))
+    digest: int = 0
+
+
+def checkpoint_path(dir, iteration: int, which: FactorKind) -> str:
+    buf = C.create_string_buffer(4096)
+    _check(LIB.alsk_checkpoint_path(os.fsencode(dir), iteration, int(which), buf, len(buf)))
+    return os.fsdecode(buf.value)
+
+
+def write_checkpoint(cp: Checkpoint, dir) -> str:
+    """dataio.hpp:600-624: atomic temp + rename; returns the final path."""
+    e = np.ascontiguousarray(cp.factor.entries, np.float32)
+    _check(LIB.alsk_checkpoint_write(os.fsencode(dir), cp.iteration, int(cp.which), cp.factor.rows, cp.factor.f,
+                                     cp.digest & (2**64 - 1), _p(e)))
+    return checkpoint_path(dir, cp.iteration, cp.which)
+
+
+def checkpoint_header(path) -> tuple:
+    it, wh, f = C.c_int(), C.c_int(), C.c_int()
+    rows, dg = C.c_int64(), C.c_uint64()
+    _check(LIB.alsk_checkpoint_header(os.fsencode(path), C.byref(it), C.byref(wh), C.byref(rows), C.byref(f),
+                                      C.byref(dg)))
+    return it.value, FactorKind(wh.value), rows.value, f.value, dg.value
+
+
+def read_checkpoint(path) -> Checkpoint:
+    """dataio.hpp:627-651: bit-identical to what was written."""
+    it, wh, rows, f, dg = checkpoint_header(path)
+    e = np.empty(rows * f, np.float32)
+    _check(LIB.alsk_checkpoint_read(os.fsencode(path), _p(e)))
+    return Checkpoint(it, wh, FactorMatrix(rows, f, e), dg)
+
+
+def latest_checkpoint_path(dir, which: Optional[FactorKind] = None) -> Optional[str]:
+    buf = C.create_string_buffer(4096)
+    found = C.c_int()
+    _check(LIB.alsk_checkpoint_latest(os.fsencode(dir), -1 if which is None else int(which), buf, len(buf),
+                                      C.byref(found)))
+    return os.fsdecode(buf.value) if found.value else None
+
+
+def restore_latest(dir, expected_digest: Optional[int] = None) -> Optional[Checkpoint]:
+    """dataio.hpp:659-686: newest by (iteration, which); a digest mismatch is an InputError."""
+    p = latest_checkpoint_path(dir)
+    if p is None:
+        return None
+    cp = read_checkpoint(p)
+    if expected_digest is not None and cp.digest != expected_digest:
+        raise InputError(f"{p}: checkpoint config digest mismatch (run has {expected_digest}, checkpoint has "
+                         f"{cp.digest})")
+    return cp
+
+
+def restore_latest_of(dir, which: FactorKind) -> Optional[Checkpoint]:
+    """dataio.hpp:689-708"""
+    p = latest_checkpoint_path(dir, which)
+    return None if p is None else read_checkpoint(p)
+
+
 FP32_ENGINES = {"auto": 0, "ffma": 1, "tensor": 2}
 
 

@@ -14,6 +14,7 @@
 #include "alskit_cuda.h"
 #include "kernels.cuh"
 #include "cache_io.cuh"
+#include "checkpoint_io.cuh"
 
 namespace alsk {
 
@@ -1011,5 +1012,104 @@ alsk_status alsk_dev_load_cache(const char* path, int64_t* row_ptr, int32_t* col
         ALSK_CUDA(cudaStreamSynchronize(s));
     });
 }
+
+// ---- factor checkpoints (dataio.hpp:546-786) ----
+
+alsk_status alsk_checkpoint_write(const char* dir, int iteration, int which, int64_t rows, int f, uint64_t digest,
+                                  const float* entries) {
+    return guard([&] {
+        if (which != 0 && which != 1) fail_input("factor kind must be 0 (x) or 1 (theta)");
+        write_checkpoint_file(dir, iteration, which, rows, f, digest, entries);
+    });
+}
+
+alsk_status alsk_checkpoint_path(const char* dir, int iteration, int which, char* out, size_t cap) {
+    return guard([&] {
+        const std::string p = (fs::path(dir) / checkpoint_name(iteration, which)).string();
+        if (p.size() + 1 > cap) fail_input("path buffer too small");
+        std::memcpy(out, p.c_str(), p.size() + 1);
+    });
+}
+
+alsk_status alsk_checkpoint_header(const char* path, int* iteration, int* which, int64_t* rows, int* f,
+                                   uint64_t* digest) {
+    return guard([&] {
+        File in(path, "rb");
+        const CkptHeader h = read_checkpoint_header(in);
+        *iteration = h.iteration;
+        *which = h.which;
+        *rows = h.rows;
+        *f = h.f;
+        *digest = h.digest;
+    });
+}
+
+alsk_status alsk_checkpoint_read(const char* path, float* entries) {
+    return guard([&] {
+        File in(path, "rb");
+        const CkptHeader h = read_checkpoint_header(in);
+        in.read(entries, sizeof(float) * static_cast<size_t>(h.rows) * h.f, "payload");
+    });
+}
+
+// Restore a factor straight into HBM (rows*f floats at d_entries), through pinned staging.
+alsk_status alsk_dev_checkpoint_read(const char* path, float* d_entries, void* stream) {
+    return guard([&] {
+        require_device();
+        File in(path, "rb");
+        const CkptHeader h = read_checkpoint_header(in);
+        const size_t bytes = sizeof(float) * static_cast<size_t>(h.rows) * h.f;
+        if (!bytes) return;
+        void* stage = nullptr;
+        ALSK_CUDA(cudaMallocHost(&stage, bytes));
+        struct Free {
+            void* p;
+            ~Free() { cudaFreeHost(p); }
+        } free_stage{stage};
+        in.read(stage, bytes, "payload");
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        ALSK_CUDA(cudaMemcpyAsync(d_entries, stage, bytes, cudaMemcpyHostToDevice, s));
+        ALSK_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
+// Newest checkpoint under dir (which = -1: either kind, theta outranking x at the same
+// iteration; 0 / 1: that kind only). *found = 0 and out = "" when there is none.
+alsk_status alsk_checkpoint_latest(const char* dir, int which, char* out, size_t cap, int* found) {
+    return guard([&] {
+        const std::string p = latest_checkpoint(dir, which);
+        if (p.size() + 1 > cap) fail_input("path buffer too small");
+        std::memcpy(out, p.c_str(), p.size() + 1);
+        *found = p.empty() ? 0 : 1;
+    });
+}
+
+alsk_status alsk_ckpt_writer_create(const char* dir, void** writer) {
+    return guard([&] {
+        require_device();
+        *writer = new DeviceWriter(dir);
+    });
+}
+
+alsk_status alsk_ckpt_writer_submit_device(void* writer, int iteration, int which, int64_t rows, int f,
+                                           uint64_t digest, const float* d_factor, void* stream) {
+    return guard([&] {
+        static_cast<DeviceWriter*>(writer)->submit_device(iteration, which, rows, f, digest, d_factor,
+                                                          static_cast<cudaStream_t>(stream));
+    });
+}
+
+alsk_status alsk_ckpt_writer_submit_host(void* writer, int iteration, int which, int64_t rows, int f,
+                                         uint64_t digest, const float* entries) {
+    return guard([&] {
+        static_cast<DeviceWriter*>(writer)->submit_host(iteration, which, rows, f, digest, entries);
+    });
+}
+
+alsk_status alsk_ckpt_writer_flush(void* writer) {
+    return guard([&] { static_cast<DeviceWriter*>(writer)->flush(); });
+}
+
+void alsk_ckpt_writer_destroy(void* writer) { delete static_cast<DeviceWriter*>(writer); }
 
 }  // extern "C"

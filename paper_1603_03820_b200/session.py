@@ -17,7 +17,8 @@ import torch
 
 from . import _native as N
 from .alskit import (TRIPLET_DTYPE, CscMatrix, CsrMatrix, FactorMatrix, SolverConfig, _check,
-                     cache_header)
+                     cache_header, checkpoint_header, checkpoint_path, restore_latest,
+                     FactorKind, InputError, IterationMetrics)
 
 LIB = N.LIB
 PREC_FP64_EXACT = 0
@@ -148,3 +149,89 @@ class AlsSession:
         x = FactorMatrix(self.m, self.f, self.X.cpu().numpy().copy())
         t = FactorMatrix(self.n, self.f, self.T.cpu().numpy().copy())
         return x, t
+
+    def load_factor(self, which: FactorKind, path) -> None:
+        """Restore X or Theta from a checkpoint file straight into HBM."""
+        _, _, rows, f, _ = checkpoint_header(path)
+        want = (self.m if which == FactorKind.x else self.n, self.f)
+        if (rows, f) != want:
+            raise InputError(f"{path}: checkpoint holds a {rows}x{f} factor, the run needs {want[0]}x{want[1]}")
+        dst = self.X if which == FactorKind.x else self.T
+        _check(LIB.alsk_dev_checkpoint_read(os.fsencode(path), dst.data_ptr(), stream_handle()))
+
+
+class DeviceCheckpointWriter:
+    """CheckpointWriter (dataio.hpp:717-786) fed from HBM: submit() queues a D2H copy of the
+    factor behind the current stream into pinned memory and returns; one native worker
+    thread writes the file (atomic temp + rename). At most one snapshot in flight; write
+    errors are sticky and raised by the next submit() or flush()."""
+
+    def __init__(self, dir):
+        self.h = C.c_void_p()
+        _check(LIB.alsk_ckpt_writer_create(os.fsencode(dir), C.byref(self.h)))
+
+    def submit(self, iteration: int, which: FactorKind, factor: torch.Tensor, rows: int, f: int, digest: int):
+        _check(LIB.alsk_ckpt_writer_submit_device(self.h, iteration, int(which), rows, f, digest & (2**64 - 1),
+                                                  factor.data_ptr(), stream_handle()))
+
+    def flush(self) -> None:
+        _check(LIB.alsk_ckpt_writer_flush(self.h))
+
+    def close(self) -> None:
+        if self.h:
+            LIB.alsk_ckpt_writer_destroy(self.h)
+            self.h = C.c_void_p()
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def __del__(self):
+        self.close()
+
+
+def train_resumable(sess: AlsSession, iterations: int, checkpoint_dir, digest: int, resume: bool = True,
+                    after_iteration=None) -> tuple:
+    """The iteration loop of train_run (driver.hpp:183-262) on a device session: resume
+    from the newest compatible checkpoint (Theta@t also loads X@t; a lone X@t finishes
+    iteration t's Theta half first), snapshot after every half through the device writer,
+    flush at the end. Returns (start_iteration, [IterationMetrics])."""
+    completed, dangling_x = 0, False
+    if resume:
+        latest = restore_latest(checkpoint_dir, digest)
+        if latest is not None:
+            completed = latest.iteration
+            if latest.which == FactorKind.theta:
+                sess.load_factor(FactorKind.theta, checkpoint_path(checkpoint_dir, completed, FactorKind.theta))
+                px = checkpoint_path(checkpoint_dir, completed, FactorKind.x)
+                if checkpoint_header(px)[4] != digest:
+                    raise InputError(f"checkpoint config digest mismatch at iteration {completed}")
+                sess.load_factor(FactorKind.x, px)
+            else:
+                sess.load_factor(FactorKind.x, checkpoint_path(checkpoint_dir, completed, FactorKind.x))
+                dangling_x = True
+    start = completed if dangling_x else completed + 1
+    rows = []
+    with DeviceCheckpointWriter(checkpoint_dir) as w:
+        def row(t):
+            m = IterationMetrics(t, sess.loss(), sess.rmse())
+            rows.append(m)
+            return after_iteration is None or after_iteration(t, sess)
+
+        go = True
+        if dangling_x:
+            sess.half_theta()
+            w.submit(completed, FactorKind.theta, sess.T, sess.n, sess.f, digest)
+            go = row(completed)
+        t = completed + 1
+        while go and t <= iterations:
+            sess.half_x()
+            w.submit(t, FactorKind.x, sess.X, sess.m, sess.f, digest)
+            sess.half_theta()
+            w.submit(t, FactorKind.theta, sess.T, sess.n, sess.f, digest)
+            go = row(t)
+            t += 1
+        w.flush()
+    return start, rows

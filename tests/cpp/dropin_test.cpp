@@ -93,6 +93,21 @@ int main() {
         std::fputs("this is not a cache file at all, but long enough to read", fj);
         std::fclose(fj);
         CHECK(throws_with<IoError>([&] { load_binary_cache(junk); }, "bad magic"));
+        // checkpoints (dataio.hpp:546-786)
+        const FactorMatrix fx = random_factor(9, 4, 5);
+        const auto ck = dir / "ck";
+        write_checkpoint({3, FactorKind::x, fx, 42}, ck);
+        const Checkpoint back = read_checkpoint(checkpoint_path(ck, 3, FactorKind::x));
+        CHECK(back.iteration == 3 && back.which == FactorKind::x && back.digest == 42 && back.factor.entries == fx.entries);
+        {
+            CheckpointWriter w(ck);
+            w.submit({3, FactorKind::theta, fx, 42});
+            w.flush();
+        }
+        const auto latest = restore_latest(ck, 42);
+        CHECK(latest && latest->iteration == 3 && latest->which == FactorKind::theta);
+        CHECK(throws_with<InputError>([&] { restore_latest(ck, 7); }, "digest mismatch"));
+        CHECK(!restore_latest(dir / "none"));
         std::filesystem::remove_all(dir);
     }
     // ---- solver (test_solver.cpp) ----
