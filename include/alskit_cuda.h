@@ -323,6 +323,14 @@ alsk_status alsk_split_train_test(const alsk_csr* r, double holdout, uint64_t se
                                   int64_t* k_out, int64_t* train_row_ptr, int32_t* train_col_idx,
                                   float* train_values, alsk_triplet* test_out);
 
+/* The same split with the CSR on the device (all pointers device memory): the held-out
+ * positions come from the same host Fisher-Yates (bit-exact), the compaction into the train
+ * CSR and the row-major test triplets runs in HBM. Two calls as above (train_row_ptr NULL:
+ * only k). */
+alsk_status alsk_dev_split_train_test(const alsk_csr* r, double holdout, uint64_t seed, int64_t* k_out,
+                                      int64_t* train_row_ptr, int32_t* train_col_idx, float* train_values,
+                                      alsk_triplet* test_out, void* stream);
+
 /* Deterministic synthetic generator: row degree
  * floor(nnz(u+1)/m)-floor(nnz u/m), columns by Floyd sampling from mt19937_64(mix_seed(seed,u)),
  * values from a planted rank-10 model + U[-0.5,0.5) noise. Row-parallel on host threads.

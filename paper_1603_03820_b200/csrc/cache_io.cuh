@@ -10,8 +10,9 @@
 // checked in the reference's order (row_ptr ends, then row by row: monotone, range,
 // strictly increasing columns).
 //
-// The device loader streams the file through two pinned staging buffers: chunk k is copied
-// to the device while chunk k+1 is read, and validated on the host as it passes.
+// The device loader streams the file through two pinned staging buffers (kept for the
+// process): chunk k is copied to the device while chunk k+1 is read, and validated on the
+// host as it passes.
 #pragma once
 #include <cuda_runtime.h>
 
@@ -19,6 +20,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <cstring>
+#include <mutex>
 #include <string>
 #include <sys/stat.h>
 #include <vector>
@@ -112,6 +114,27 @@ struct Validator {
         }
     }
 };
+
+// Pinned staging for the device loaders: two 32 MB buffers and their upload-done events,
+// allocated on first use and kept for the process (cudaMallocHost of fresh buffers per load
+// cost more than the upload itself); one load at a time holds them.
+struct PinnedStage {
+    static constexpr size_t kChunk = size_t(32) << 20;
+    std::mutex mu;
+    void* buf[2] = {nullptr, nullptr};
+    cudaEvent_t ev[2] = {nullptr, nullptr};
+    void ensure() {
+        for (int i = 0; i < 2; ++i) {
+            if (!buf[i]) ALSK_CUDA(cudaMallocHost(&buf[i], kChunk));
+            if (!ev[i]) ALSK_CUDA(cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming));
+        }
+    }
+};
+
+PinnedStage& pinned_stage() {
+    static PinnedStage* s = new PinnedStage();  // never destroyed: outlives the CUDA context teardown
+    return *s;
+}
 
 }  // namespace
 }  // namespace alsk

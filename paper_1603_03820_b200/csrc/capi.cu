@@ -731,6 +731,21 @@ alsk_status alsk_dev_csr_to_csc(const alsk_csr* a, int64_t* col_ptr_out, int32_t
     });
 }
 
+// split_train_test (dataio.hpp:251-290) on device arrays: host Fisher-Yates picks the
+// held-out positions (bit-exact with the reference), the device compacts the CSR. With
+// train_row_ptr == NULL only *k_out is set (two-call sizing, like alsk_split_train_test).
+alsk_status alsk_dev_split_train_test(const alsk_csr* r, double holdout, uint64_t seed, int64_t* k_out,
+                                      int64_t* train_row_ptr, int32_t* train_col_idx, float* train_values,
+                                      alsk_triplet* test_out, void* stream) {
+    return guard([&] {
+        *k_out = split_holdout_count(r->nnz, holdout);
+        if (train_row_ptr == nullptr) return;
+        require_device();
+        split_train_test_device(dev_view(r), holdout, seed, train_row_ptr, train_col_idx, train_values, test_out,
+                                as_stream(stream));
+    });
+}
+
 alsk_status alsk_dev_partial_hermitian(const alsk_csr* r, const float* theta, int64_t theta_rows,
                                        int f, double lambda, int64_t row_begin, int64_t row_end,
                                        double* out_packed, void* stream) {
@@ -970,26 +985,17 @@ alsk_status alsk_dev_load_cache(const char* path, int64_t* row_ptr, int32_t* col
         Validator val{rp.data(), rows, static_cast<int64_t>(h.cols), nnz, in.path};
         val.ends();
         ALSK_CUDA(cudaMemcpyAsync(row_ptr, rp.data(), sizeof(int64_t) * rp.size(), cudaMemcpyHostToDevice, s));
-        // two pinned staging buffers, 64 MB each: read chunk k+1 while chunk k uploads
-        constexpr size_t kChunk = size_t(64) << 20;
-        void* stage[2] = {nullptr, nullptr};
-        cudaEvent_t done[2] = {nullptr, nullptr};
-        struct Cleanup {
-            void** st;
-            cudaEvent_t* ev;
+        // process-wide pinned staging (allocated once): read chunk k+1 while chunk k uploads
+        PinnedStage& ps = pinned_stage();
+        std::lock_guard<std::mutex> hold(ps.mu);
+        ps.ensure();
+        void* const* stage = ps.buf;
+        cudaEvent_t* done = ps.ev;
+        constexpr size_t kChunk = PinnedStage::kChunk;
+        struct Drain {
             cudaStream_t s;
-            ~Cleanup() {
-                cudaStreamSynchronize(s);
-                for (int i = 0; i < 2; ++i) {
-                    if (st[i]) cudaFreeHost(st[i]);
-                    if (ev[i]) cudaEventDestroy(ev[i]);
-                }
-            }
-        } cleanup{stage, done, s};
-        for (int i = 0; i < 2; ++i) {
-            ALSK_CUDA(cudaMallocHost(&stage[i], kChunk));
-            ALSK_CUDA(cudaEventCreateWithFlags(&done[i], cudaEventDisableTiming));
-        }
+            ~Drain() { cudaStreamSynchronize(s); }  // the buffers are reused by the next load
+        } drain{s};
         int buf = 0;
         auto stream_array = [&](void* dst, size_t elem, int64_t count, const char* what, bool validate) {
             const int64_t per = static_cast<int64_t>(kChunk / elem);

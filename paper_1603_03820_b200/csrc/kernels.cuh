@@ -121,6 +121,11 @@ void csr_from_triplets_device(int64_t m, int64_t n, const int64_t* rows, const i
 template <class T>
 void exclusive_scan_ptr_i64(const T* in, int64_t n, int64_t* out, cudaStream_t s);
 
+// split_train_test on the device (split.cu; dataio.hpp:251-290)
+int64_t split_holdout_count(int64_t nnz, double holdout);
+void split_train_test_device(const DevCsr& r, double holdout, uint64_t seed, int64_t* train_row_ptr,
+                             int32_t* train_col_idx, float* train_values, alsk_triplet* test, cudaStream_t s);
+
 // Grid partition state on the device (sparse.hpp:71-84): cuts on the host, per-row split
 // offsets and per-block row pointers on the device.
 struct GridDevice {

@@ -59,6 +59,24 @@ class DeviceCsr:
                                        stream_handle()))
         return DeviceCsr(rows, cols, rp, ci[:nnz], va[:nnz], device)
 
+    def split_train_test(self, holdout_fraction: float, seed: int):
+        """split_train_test (dataio.hpp:251-290) in HBM: returns (train DeviceCsr, test triplets
+        as a (k, 24-byte) uint8 device tensor in TRIPLET_DTYPE layout), bit-identical to the
+        host split."""
+        k = C.c_int64()
+        _check(LIB.alsk_dev_split_train_test(C.byref(self.c), holdout_fraction, seed & (2**64 - 1), C.byref(k),
+                                             None, None, None, None, None))
+        dev = self.values.device
+        kk, keep = k.value, self.nnz - k.value
+        rp = torch.empty(self.rows + 1, dtype=torch.int64, device=dev)
+        ci = torch.empty(max(keep, 1), dtype=torch.int32, device=dev)
+        va = torch.empty(max(keep, 1), dtype=torch.float32, device=dev)
+        te = torch.empty((max(kk, 1), TRIPLET_DTYPE.itemsize), dtype=torch.uint8, device=dev)
+        _check(LIB.alsk_dev_split_train_test(C.byref(self.c), holdout_fraction, seed & (2**64 - 1), C.byref(k),
+                                             rp.data_ptr(), ci.data_ptr(), va.data_ptr(), te.data_ptr(),
+                                             stream_handle()))
+        return DeviceCsr(self.rows, self.cols, rp, ci[:keep], va[:keep], dev), te[:kk]
+
     def transpose(self) -> "DeviceCsr":
         """Stable device transpose (csr_to_csc, sparse.hpp:185-207) viewed as the CSR of R^T."""
         dev = self.values.device
