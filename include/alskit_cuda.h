@@ -278,6 +278,26 @@ alsk_status alsk_ckpt_writer_submit_host(void* writer, int iteration, int which,
 alsk_status alsk_ckpt_writer_flush(void* writer);
 void alsk_ckpt_writer_destroy(void* writer);
 
+/* Persisted grids (persist_grid / load_grid_meta / load_block, dataio.hpp:352-439): a
+ * grid.meta text file plus block_<i>_<j>.bin binary caches (alsk_save_cache per block). */
+alsk_status alsk_persist_grid_meta(const char* dir, int p, int q, int64_t rows, int64_t cols, const int64_t* row_cuts,
+                                   const int64_t* col_cuts);
+alsk_status alsk_block_path(const char* dir, int i, int j, char* out, size_t cap);
+/* row_cuts[q+1] / col_cuts[p+1] may be NULL (first call: sizes only). */
+alsk_status alsk_grid_meta(const char* dir, int* p, int* q, int64_t* rows, int64_t* cols, int64_t* row_cuts,
+                           int64_t* col_cuts);
+/* Out-of-core block stream (BlockStream, dataio.hpp:447-524) into HBM: a loader thread
+ * reads, validates and uploads blocks in the given order (pairs i0,j0,i1,j1,...) two ahead.
+ * next() fills *out with device pointers (col_offset restored from grid.meta) and orders
+ * `stream` after the upload; they stay valid until the following next() call, whose
+ * position on `stream` gates the slot's reuse. *has_block = 0 once the plan is exhausted;
+ * a loader error ("block (i, j): ...") surfaces on the next() that would return it. */
+alsk_status alsk_block_stream_open(const char* dir, const int* order_ij, int count, void** stream_out);
+alsk_status alsk_block_stream_next(void* block_stream, void* stream, int* has_block, int* i, int* j, alsk_csr* out);
+void alsk_block_stream_close(void* block_stream);
+/* Utility: synchronous device-to-host copy on `stream`. */
+alsk_status alsk_dev_to_host(void* dst, const void* src, size_t bytes, void* stream);
+
 /* Device loss/rmse; result written to *out (host) after a stream sync. */
 alsk_status alsk_dev_loss(const alsk_csr* r, const int64_t* col_nnz, const float* x,
                           const float* theta, int64_t theta_rows, int f, double lambda,

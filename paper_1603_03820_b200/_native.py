@@ -77,6 +77,14 @@ _SIGS = {
     "alsk_save_cache": (C.c_int, [CsrP, C.c_char_p]),
     "alsk_load_cache": (C.c_int, [C.c_char_p, vp, vp, vp]),
     "alsk_dev_load_cache": (C.c_int, [C.c_char_p, vp, vp, vp, vp]),
+    "alsk_persist_grid_meta": (C.c_int, [C.c_char_p, C.c_int, C.c_int, i64, i64, vp, vp]),
+    "alsk_block_path": (C.c_int, [C.c_char_p, C.c_int, C.c_int, C.c_char_p, C.c_size_t]),
+    "alsk_grid_meta": (C.c_int, [C.c_char_p, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(i64), C.POINTER(i64),
+                                 vp, vp]),
+    "alsk_block_stream_open": (C.c_int, [C.c_char_p, vp, C.c_int, C.POINTER(vp)]),
+    "alsk_block_stream_next": (C.c_int, [vp, vp, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int), CsrP]),
+    "alsk_block_stream_close": (None, [vp]),
+    "alsk_dev_to_host": (C.c_int, [vp, vp, C.c_size_t, vp]),
     "alsk_dev_split_train_test": (C.c_int, [CsrP, C.c_double, C.c_uint64, C.POINTER(i64), vp, vp, vp, vp, vp]),
     "alsk_checkpoint_write": (C.c_int, [C.c_char_p, C.c_int, C.c_int, i64, C.c_int, C.c_uint64, vp]),
     "alsk_checkpoint_path": (C.c_int, [C.c_char_p, C.c_int, C.c_int, C.c_char_p, C.c_size_t]),

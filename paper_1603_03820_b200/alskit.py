@@ -521,6 +521,57 @@ def load_binary_cache(path) -> CsrMatrix:
     return CsrMatrix(rows, cols, 0, rp, ci, va)
 
 
+# ---------------------------------------------------------------- persisted grids (dataio.hpp:352-540)
+@dataclass
+class GridMeta:
+    """dataio.hpp:354-361"""
+    p: int = 1
+    q: int = 1
+    rows: int = 0
+    cols: int = 0
+    row_cuts: np.ndarray = field(default_factory=lambda: np.zeros(2, np.int64))
+    col_cuts: np.ndarray = field(default_factory=lambda: np.zeros(2, np.int64))
+
+
+@dataclass(frozen=True)
+class BlockRef:
+    """dataio.hpp:364-369: column partition i, row partition j."""
+    i: int = 0
+    j: int = 0
+
+
+def block_path(dir, i: int, j: int) -> str:
+    buf = C.create_string_buffer(4096)
+    _check(LIB.alsk_block_path(os.fsencode(dir), i, j, buf, len(buf)))
+    return os.fsdecode(buf.value)
+
+
+def persist_grid(grid: GridPartition, dir) -> None:
+    """dataio.hpp:381-400: grid.meta plus one binary cache per block."""
+    rc = np.ascontiguousarray(grid.row_cuts, np.int64)
+    cc = np.ascontiguousarray(grid.col_cuts, np.int64)
+    _check(LIB.alsk_persist_grid_meta(os.fsencode(dir), grid.p, grid.q, grid.rows, grid.cols, _p(rc), _p(cc)))
+    for j in range(grid.q):
+        for i in range(grid.p):
+            save_binary_cache(grid.block(i, j), block_path(dir, i, j))
+
+
+def load_grid_meta(dir) -> GridMeta:
+    """dataio.hpp:402-419"""
+    p, q = C.c_int(), C.c_int()
+    rows, cols = C.c_int64(), C.c_int64()
+    _check(LIB.alsk_grid_meta(os.fsencode(dir), C.byref(p), C.byref(q), C.byref(rows), C.byref(cols), None, None))
+    rc = np.empty(q.value + 1, np.int64)
+    cc = np.empty(p.value + 1, np.int64)
+    _check(LIB.alsk_grid_meta(os.fsencode(dir), C.byref(p), C.byref(q), C.byref(rows), C.byref(cols), _p(rc), _p(cc)))
+    return GridMeta(p.value, q.value, rows.value, cols.value, rc, cc)
+
+
+def row_major_order(meta: GridMeta) -> list:
+    """dataio.hpp:528-534: row partitions outer, column partitions inner."""
+    return [BlockRef(i, j) for j in range(meta.q) for i in range(meta.p)]
+
+
 # ---------------------------------------------------------------- checkpoints (dataio.hpp:546-708)
 class FactorKind(enum.IntEnum):
     """dataio.hpp:548: theta outranks x at the same iteration."""

@@ -15,6 +15,7 @@
 #include "kernels.cuh"
 #include "cache_io.cuh"
 #include "checkpoint_io.cuh"
+#include "grid_io.cuh"
 
 namespace alsk {
 
@@ -1117,5 +1118,71 @@ alsk_status alsk_ckpt_writer_flush(void* writer) {
 }
 
 void alsk_ckpt_writer_destroy(void* writer) { delete static_cast<DeviceWriter*>(writer); }
+
+// ---- persisted grids and the out-of-core block stream (dataio.hpp:352-540) ----
+
+alsk_status alsk_persist_grid_meta(const char* dir, int p, int q, int64_t rows, int64_t cols, const int64_t* row_cuts,
+                                   const int64_t* col_cuts) {
+    return guard([&] {
+        GridMetaH g;
+        g.p = p;
+        g.q = q;
+        g.rows = rows;
+        g.cols = cols;
+        g.row_cuts.assign(row_cuts, row_cuts + q + 1);
+        g.col_cuts.assign(col_cuts, col_cuts + p + 1);
+        write_grid_meta(dir, g);
+    });
+}
+
+alsk_status alsk_block_path(const char* dir, int i, int j, char* out, size_t cap) {
+    return guard([&] {
+        const std::string p = block_path(dir, i, j);
+        if (p.size() + 1 > cap) fail_input("path buffer too small");
+        std::memcpy(out, p.c_str(), p.size() + 1);
+    });
+}
+
+alsk_status alsk_grid_meta(const char* dir, int* p, int* q, int64_t* rows, int64_t* cols, int64_t* row_cuts,
+                           int64_t* col_cuts) {
+    return guard([&] {
+        const GridMetaH g = read_grid_meta(dir);
+        *p = g.p;
+        *q = g.q;
+        *rows = g.rows;
+        *cols = g.cols;
+        if (row_cuts) std::copy(g.row_cuts.begin(), g.row_cuts.end(), row_cuts);
+        if (col_cuts) std::copy(g.col_cuts.begin(), g.col_cuts.end(), col_cuts);
+    });
+}
+
+alsk_status alsk_block_stream_open(const char* dir, const int* order_ij, int count, void** stream_out) {
+    return guard([&] {
+        require_device();
+        if (count < 0) fail_input("block count must be >= 0");
+        *stream_out = new DeviceBlockStream(dir, std::vector<int>(order_ij, order_ij + 2 * count));
+    });
+}
+
+alsk_status alsk_block_stream_next(void* bs, void* stream, int* has_block, int* i, int* j, alsk_csr* out) {
+    return guard([&] {
+        DeviceBlockStream::Out o{};
+        *has_block = static_cast<DeviceBlockStream*>(bs)->next(as_stream(stream), o) ? 1 : 0;
+        if (!*has_block) return;
+        *i = o.i;
+        *j = o.j;
+        *out = alsk_csr{o.rows, o.cols, o.col_offset, o.nnz, o.row_ptr, o.col_idx, o.values};
+    });
+}
+
+void alsk_block_stream_close(void* bs) { delete static_cast<DeviceBlockStream*>(bs); }
+
+alsk_status alsk_dev_to_host(void* dst, const void* src, size_t bytes, void* stream) {
+    return guard([&] {
+        require_device();
+        ALSK_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, as_stream(stream)));
+        ALSK_CUDA(cudaStreamSynchronize(as_stream(stream)));
+    });
+}
 
 }  // extern "C"

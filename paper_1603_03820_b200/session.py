@@ -18,7 +18,7 @@ import torch
 from . import _native as N
 from .alskit import (TRIPLET_DTYPE, CscMatrix, CsrMatrix, FactorMatrix, SolverConfig, _check,
                      cache_header, checkpoint_header, checkpoint_path, restore_latest,
-                     FactorKind, InputError, IterationMetrics)
+                     FactorKind, InputError, IterationMetrics, BlockRef)
 
 LIB = N.LIB
 PREC_FP64_EXACT = 0
@@ -253,3 +253,85 @@ def train_resumable(sess: AlsSession, iterations: int, checkpoint_dir, digest: i
             t += 1
         w.flush()
     return start, rows
+
+
+class DeviceBlock:
+    """A streamed grid block in HBM (the C-ABI view of the stream's slot); valid until the
+    stream's next next()."""
+
+    def __init__(self, c: N.CsrT):
+        self.c = c
+        self.rows, self.cols, self.col_offset, self.nnz = c.rows, c.cols, c.col_offset, c.nnz
+
+    def to_host(self) -> CsrMatrix:
+        rp = np.empty(self.rows + 1, np.int64)
+        ci = np.empty(self.nnz, np.int32)
+        va = np.empty(self.nnz, np.float32)
+        s = stream_handle()
+        for dst, src in ((rp, self.c.row_ptr), (ci, self.c.col_idx), (va, self.c.values)):
+            if dst.nbytes:
+                _check(LIB.alsk_dev_to_host(dst.ctypes.data, src, dst.nbytes, s))
+        return CsrMatrix(self.rows, self.cols, self.col_offset, rp, ci, va)
+
+
+class DeviceBlockStream:
+    """BlockStream (dataio.hpp:447-524) into HBM: iterate to get (BlockRef, DeviceBlock) in
+    plan order, each upload overlapped with the work on the previous blocks."""
+
+    def __init__(self, dir, order):
+        flat = np.array([v for b in order for v in (b.i, b.j)] or [0], np.int32)
+        self.h = C.c_void_p()
+        _check(LIB.alsk_block_stream_open(os.fsencode(dir), flat.ctypes.data, len(order), C.byref(self.h)))
+
+    def __iter__(self):
+        return self
+
+    def __next__(self):
+        has, i, j = C.c_int(), C.c_int(), C.c_int()
+        c = N.CsrT()
+        _check(LIB.alsk_block_stream_next(self.h, stream_handle(), C.byref(has), C.byref(i), C.byref(j), C.byref(c)))
+        if not has.value:
+            raise StopIteration
+        return BlockRef(i.value, j.value), DeviceBlock(c)
+
+    def close(self) -> None:
+        if self.h:
+            LIB.alsk_block_stream_close(self.h)
+            self.h = C.c_void_p()
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def __del__(self):
+        self.close()
+
+
+def out_of_core_update_x(dir, theta: torch.Tensor, f: int, lam: float, out: torch.Tensor) -> None:
+    """The X half over a persisted grid that need not fit in HBM (the
+    SU-ALS scale-up, parallel.hpp:487-583, fed by the block stream): for each row partition
+    j, the FP32 partial Hermitians of its blocks (i, j) against Theta's column slab i are
+    summed (panel-blocked packed rows) and solved with the batched TMEM Cholesky. Blocks
+    arrive in row-major order, each upload overlapping the kernels of the previous one."""
+    from .alskit import load_grid_meta, row_major_order
+    from .distributed import cuda_partial_hermitian_f32, cuda_solve_packed_f32, packed_stride
+    meta = load_grid_meta(dir)
+    per = packed_stride(f)
+    dev = theta.device
+    rows_max = int(np.max(np.diff(meta.row_cuts))) if meta.q else 0
+    acc = torch.empty(max(rows_max, 1) * per, dtype=torch.float32, device=dev)
+    part = torch.empty_like(acc)
+    with DeviceBlockStream(dir, row_major_order(meta)) as bs:
+        for ref, blk in bs:
+            lo, hi = int(meta.col_cuts[ref.i]), int(meta.col_cuts[ref.i + 1])
+            rows = blk.rows
+            dst = acc if ref.i == 0 else part
+            if rows:
+                cuda_partial_hermitian_f32(blk, theta[lo * f:], hi - lo, f, lam, 0, rows, dst)
+                if ref.i:
+                    acc[: rows * per].add_(part[: rows * per])
+            if ref.i == meta.p - 1 and rows:
+                r0 = int(meta.row_cuts[ref.j])
+                cuda_solve_packed_f32(acc, rows, f, out[r0 * f:])
