@@ -11,8 +11,8 @@
 // strictly increasing columns).
 //
 // The device loader streams the file through two pinned staging buffers (kept for the
-// process): chunk k is copied to the device while chunk k+1 is read, and validated on the
-// host as it passes.
+// process): chunk k is copied to the device while chunk k+1 is read; the CSR invariants are
+// then checked in HBM (validate.cu) and only a failing row is re-read to build the message.
 #pragma once
 #include <cuda_runtime.h>
 
@@ -114,6 +114,24 @@ struct Validator {
         }
     }
 };
+
+// The device check (csr_first_bad_row) found row u to be the first bad one: rebuild the
+// reference's message from that row alone (its column slice read back from HBM).
+[[noreturn]] void report_bad_row(const int64_t* rp, int64_t rows, int64_t cols, int64_t nnz, const std::string& path,
+                                 int64_t u, const int32_t* d_ci, cudaStream_t s) {
+    const int64_t b = rp[u];
+    const int64_t e = std::min(std::max(rp[u + 1], b), nnz);
+    std::vector<int32_t> row(static_cast<size_t>(std::max<int64_t>(e - b, 0)));
+    if (!row.empty()) {
+        ALSK_CUDA(cudaMemcpyAsync(row.data(), d_ci + b, sizeof(int32_t) * row.size(), cudaMemcpyDeviceToHost, s));
+        ALSK_CUDA(cudaStreamSynchronize(s));
+    }
+    Validator val{rp, rows, cols, nnz, path};
+    val.u = u;
+    val.kpos = b;
+    val.feed(row.data(), b, std::max(e, b));
+    val.bad("row " + std::to_string(u) + " failed the device check");  // not reached
+}
 
 // Pinned staging for the device loaders: two 32 MB buffers and their upload-done events,
 // allocated on first use and kept for the process (cudaMallocHost of fresh buffers per load

@@ -998,25 +998,22 @@ alsk_status alsk_dev_load_cache(const char* path, int64_t* row_ptr, int32_t* col
             ~Drain() { cudaStreamSynchronize(s); }  // the buffers are reused by the next load
         } drain{s};
         int buf = 0;
-        auto stream_array = [&](void* dst, size_t elem, int64_t count, const char* what, bool validate) {
+        auto stream_array = [&](void* dst, size_t elem, int64_t count, const char* what) {
             const int64_t per = static_cast<int64_t>(kChunk / elem);
             for (int64_t k0 = 0; k0 < count; k0 += per, buf ^= 1) {
                 const int64_t k1 = std::min(count, k0 + per);
                 ALSK_CUDA(cudaEventSynchronize(done[buf]));  // the previous upload from this buffer is done
                 in.read(stage[buf], elem * (k1 - k0), what);
-                if (validate) {
-                    val.feed(static_cast<const int32_t*>(stage[buf]), k0, k1);
-                    val.last = static_cast<const int32_t*>(stage[buf])[k1 - k0 - 1];
-                }
                 ALSK_CUDA(cudaMemcpyAsync(static_cast<char*>(dst) + elem * k0, stage[buf], elem * (k1 - k0),
                                           cudaMemcpyHostToDevice, s));
                 ALSK_CUDA(cudaEventRecord(done[buf], s));
             }
         };
-        stream_array(col_idx, sizeof(int32_t), nnz, "col_idx", true);
-        val.feed(nullptr, nnz, nnz);  // rows with no entries after the last chunk
-        stream_array(values, sizeof(float), nnz, "values", false);
-        ALSK_CUDA(cudaStreamSynchronize(s));
+        stream_array(col_idx, sizeof(int32_t), nnz, "col_idx");
+        stream_array(values, sizeof(float), nnz, "values");
+        // the CSR invariants are checked in HBM (validate.cu), the host only reads and copies
+        const int64_t bad = csr_first_bad_row(row_ptr, col_idx, rows, static_cast<int64_t>(h.cols), nnz, s);
+        if (bad >= 0) report_bad_row(rp.data(), rows, static_cast<int64_t>(h.cols), nnz, in.path, bad, col_idx, s);
     });
 }
 

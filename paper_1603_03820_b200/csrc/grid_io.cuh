@@ -3,8 +3,8 @@
 // load_block, dataio.hpp:352-439), and BlockStream (dataio.hpp:447-524) re-done for HBM.
 //
 // DeviceBlockStream: one loader thread reads blocks in plan order into per-slot pinned
-// buffers (validated like load_binary_cache, shape-checked against grid.meta, errors prefixed
-// "block (i, j): " as the reference's), uploads each on a private stream and queues it
+// buffers (validated like load_binary_cache: row_ptr ends on the host, the rest in HBM;
+// shape-checked against grid.meta; errors prefixed "block (i, j): " as the reference's), uploads each on a private stream and queues it
 // (depth 2, as the reference's). next() hands the consumer device pointers and orders the
 // consumer's stream after the upload; the slot is recycled only after the consumer's stream
 // has passed the following next() (an event on the consumer's stream gates the reuse), so
@@ -167,9 +167,9 @@ class DeviceBlockStream {
             const size_t bytes = sizeof(int64_t) * (rows + 1) + sizeof(int32_t) * nnz + sizeof(float) * nnz;
             // the previous upload from this slot's pinned buffer, and the consumer's use of
             // its device copy, must both be over before either is overwritten
-            ALSK_CUDA(cudaEventSynchronize(s.uploaded));
-            ALSK_CUDA(cudaEventSynchronize(s.released));
-            if (bytes > s.cap) {
+            ALSK_CUDA(cudaEventSynchronize(s.uploaded));  // the pinned buffer is free
+            if (bytes > s.cap) {  // growing also frees the device copy: the consumer must be done
+                ALSK_CUDA(cudaEventSynchronize(s.released));
                 if (s.host) ALSK_CUDA(cudaFreeHost(s.host));
                 if (s.dev) ALSK_CUDA(cudaFree(s.dev));
                 s.host = s.dev = nullptr;
@@ -185,10 +185,14 @@ class DeviceBlockStream {
             in.read(ci + nnz, sizeof(float) * nnz, "values");
             Validator val{rp, rows, static_cast<int64_t>(h.cols), nnz, in.path};
             val.ends();
-            val.feed(ci, 0, nnz);
             ALSK_CUDA(cudaStreamWaitEvent(upload_, s.released, 0));
             ALSK_CUDA(cudaMemcpyAsync(s.dev, s.host, bytes, cudaMemcpyHostToDevice, upload_));
             ALSK_CUDA(cudaEventRecord(s.uploaded, upload_));
+            // the rest of validate() in HBM (validate.cu); syncs the upload stream
+            const auto* dci = reinterpret_cast<const int32_t*>(s.dev + sizeof(int64_t) * (rows + 1));
+            const int64_t bad = csr_first_bad_row(reinterpret_cast<const int64_t*>(s.dev), dci, rows,
+                                                  static_cast<int64_t>(h.cols), nnz, upload_);
+            if (bad >= 0) report_bad_row(rp, rows, static_cast<int64_t>(h.cols), nnz, in.path, bad, dci, upload_);
             s.i = i;
             s.j = j;
             s.rows = rows;

@@ -121,6 +121,10 @@ void csr_from_triplets_device(int64_t m, int64_t n, const int64_t* rows, const i
 template <class T>
 void exclusive_scan_ptr_i64(const T* in, int64_t n, int64_t* out, cudaStream_t s);
 
+// CSR invariant check after a raw upload (validate.cu): first failing row or -1; syncs s
+int64_t csr_first_bad_row(const int64_t* rp, const int32_t* ci, int64_t rows, int64_t cols, int64_t nnz,
+                          cudaStream_t s);
+
 // split_train_test on the device (split.cu; dataio.hpp:251-290)
 int64_t split_holdout_count(int64_t nnz, double holdout);
 void split_train_test_device(const DevCsr& r, double holdout, uint64_t seed, int64_t* train_row_ptr,
