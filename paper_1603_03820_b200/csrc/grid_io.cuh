@@ -71,6 +71,46 @@ GridMetaH read_grid_meta(const std::string& dir) {  // dataio.hpp:402-419
     return g;
 }
 
+// Pinned host buffers outlive the streams that used them (cudaMallocHost of a few hundred
+// MB costs more than reading the block): returned here on close, reused by the next stream.
+struct PinnedPool {
+    std::mutex mu;
+    std::vector<std::pair<char*, size_t>> free;
+    char* take(size_t bytes, size_t& cap) {
+        {
+            std::lock_guard<std::mutex> lock(mu);
+            for (size_t k = 0; k < free.size(); ++k)
+                if (free[k].second >= bytes) {
+                    char* p = free[k].first;
+                    cap = free[k].second;
+                    free.erase(free.begin() + static_cast<long>(k));
+                    return p;
+                }
+        }
+        char* p = nullptr;
+        ALSK_CUDA(cudaMallocHost(reinterpret_cast<void**>(&p), bytes));
+        cap = bytes;
+        return p;
+    }
+    void give(char* p, size_t cap) {
+        if (!p) return;
+        std::lock_guard<std::mutex> lock(mu);
+        free.emplace_back(p, cap);
+        if (free.size() > 3) {  // keep the three largest (one stream's slots)
+            auto smallest = free.begin();
+            for (auto it = free.begin(); it != free.end(); ++it)
+                if (it->second < smallest->second) smallest = it;
+            cudaFreeHost(smallest->first);
+            free.erase(smallest);
+        }
+    }
+};
+
+PinnedPool& pinned_pool() {
+    static PinnedPool* p = new PinnedPool();  // never destroyed: outlives the CUDA context teardown
+    return *p;
+}
+
 class DeviceBlockStream {
   public:
     struct Out {
@@ -108,8 +148,8 @@ class DeviceBlockStream {
         cudaStreamSynchronize(upload_);
         for (Slot& s : slots_) {
             cudaEventSynchronize(s.released);
-            if (s.host) cudaFreeHost(s.host);
-            if (s.dev) cudaFree(s.dev);
+            pinned_pool().give(s.host, s.hcap);
+            if (s.dev) cudaFreeAsync(s.dev, upload_);
             cudaEventDestroy(s.uploaded);
             cudaEventDestroy(s.released);
         }
@@ -149,7 +189,7 @@ class DeviceBlockStream {
     struct Slot {
         char* host = nullptr;  // pinned: row_ptr | col_idx | values, the device layout
         char* dev = nullptr;
-        size_t cap = 0;
+        size_t cap = 0, hcap = 0;
         cudaEvent_t uploaded = nullptr, released = nullptr;
         bool busy = false;
         int i = 0, j = 0;
@@ -168,14 +208,20 @@ class DeviceBlockStream {
             // the previous upload from this slot's pinned buffer, and the consumer's use of
             // its device copy, must both be over before either is overwritten
             ALSK_CUDA(cudaEventSynchronize(s.uploaded));  // the pinned buffer is free
-            if (bytes > s.cap) {  // growing also frees the device copy: the consumer must be done
-                ALSK_CUDA(cudaEventSynchronize(s.released));
-                if (s.host) ALSK_CUDA(cudaFreeHost(s.host));
-                if (s.dev) ALSK_CUDA(cudaFree(s.dev));
-                s.host = s.dev = nullptr;
+            if (bytes > s.hcap) {
+                pinned_pool().give(s.host, s.hcap);
+                s.host = nullptr;
+                s.hcap = 0;
+                s.host = pinned_pool().take(bytes, s.hcap);
+            }
+            // everything below on the upload stream runs after the consumer released the slot
+            ALSK_CUDA(cudaStreamWaitEvent(upload_, s.released, 0));
+            if (bytes > s.cap) {  // device slots come from the stream-ordered pool (retained)
+                retain_pool_memory();
+                if (s.dev) ALSK_CUDA(cudaFreeAsync(s.dev, upload_));  // after the consumer's release
+                s.dev = nullptr;
                 s.cap = 0;
-                ALSK_CUDA(cudaMallocHost(reinterpret_cast<void**>(&s.host), bytes));
-                ALSK_CUDA(cudaMalloc(reinterpret_cast<void**>(&s.dev), bytes));
+                ALSK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&s.dev), bytes, upload_));
                 s.cap = bytes;
             }
             auto* rp = reinterpret_cast<int64_t*>(s.host);
@@ -185,7 +231,6 @@ class DeviceBlockStream {
             in.read(ci + nnz, sizeof(float) * nnz, "values");
             Validator val{rp, rows, static_cast<int64_t>(h.cols), nnz, in.path};
             val.ends();
-            ALSK_CUDA(cudaStreamWaitEvent(upload_, s.released, 0));
             ALSK_CUDA(cudaMemcpyAsync(s.dev, s.host, bytes, cudaMemcpyHostToDevice, upload_));
             ALSK_CUDA(cudaEventRecord(s.uploaded, upload_));
             // the rest of validate() in HBM (validate.cu); syncs the upload stream
