@@ -15,7 +15,9 @@
 
 #include <cmath>
 #include <cstdint>
+#include <memory>
 #include <random>
+#include <thread>
 #include <vector>
 
 #include "common.cuh"
@@ -86,14 +88,28 @@ uint64_t bounded(std::mt19937_64& rng, uint64_t range) {  // dataio.hpp:98-105
 
 // The reference's partial Fisher-Yates over positions (dataio.hpp:259-266), 32-bit
 // positions when they fit (the swaps are the same), emitted as a bitmask.
+// The draws do not depend on the array, so they are taken first and the swaps run with
+// the partner slot prefetched a few dozen swaps ahead (the random partner reads are the
+// cost: one cache miss each); the identity fill is split over threads.
 template <class P>
 void held_mask(int64_t nnz, int64_t k, uint64_t seed, std::vector<uint32_t>& mask) {
-    std::vector<P> pos(static_cast<size_t>(nnz));
-    for (int64_t i = 0; i < nnz; ++i) pos[i] = static_cast<P>(i);
+    std::unique_ptr<P[]> pos(new P[static_cast<size_t>(nnz)]);  // not value-initialised: filled below
+    {
+        const int nt = nnz >= (int64_t(1) << 22) ? 8 : 1;
+        std::vector<std::thread> th;
+        for (int t = 0; t < nt; ++t)
+            th.emplace_back([&, t] {
+                for (int64_t i = nnz * t / nt, e = nnz * (t + 1) / nt; i < e; ++i) pos[i] = static_cast<P>(i);
+            });
+        for (auto& x : th) x.join();
+    }
+    std::unique_ptr<P[]> js(new P[static_cast<size_t>(k)]);
     std::mt19937_64 rng(seed);
+    for (int64_t t = 0; t < k; ++t) js[t] = static_cast<P>(t + static_cast<int64_t>(bounded(rng, static_cast<uint64_t>(nnz - t))));
+    constexpr int64_t kAhead = 48;
     for (int64_t t = 0; t < k; ++t) {
-        const int64_t j = t + static_cast<int64_t>(bounded(rng, static_cast<uint64_t>(nnz - t)));
-        std::swap(pos[t], pos[j]);
+        if (t + kAhead < k) __builtin_prefetch(&pos[js[t + kAhead]], 1, 0);
+        std::swap(pos[t], pos[js[t]]);
     }
     mask.assign(static_cast<size_t>((nnz + 31) / 32), 0u);
     for (int64_t t = 0; t < k; ++t) {
