@@ -23,6 +23,8 @@
 #include <mutex>
 #include <string>
 #include <sys/stat.h>
+#include <thread>
+#include <unistd.h>
 #include <vector>
 
 #include "common.cuh"
@@ -53,6 +55,38 @@ struct File {
         if (bytes && std::fwrite(src, 1, bytes, f) != bytes) fail_io("write failed for " + path);
     }
 };
+
+// Positional read or write of bytes at offset with up to four threads (pread/pwrite share no
+// file position); one thread below 8 MB, where start-up costs more than it saves. A single
+// reader tops out near 6.5 GB/s from the page cache. Returns false on a short transfer.
+// (Checkpoint writes stay single-stream: they are bound by the kernel's dirty-page
+// writeback, ~70 ms per 192 MB factor and slower once throttled; threads did not help.)
+inline bool parallel_pio(int fd, char* buf, size_t bytes, size_t offset, bool write) {
+    constexpr int kThreads = 4;
+    const int nt = bytes >= (size_t(8) << 20) ? kThreads : 1;
+    const size_t piece = (bytes + nt - 1) / nt;
+    bool ok[kThreads] = {true, true, true, true};
+    auto work = [&](int t) {
+        size_t lo = std::min(bytes, piece * t);
+        const size_t hi = std::min(bytes, lo + piece);
+        while (lo < hi) {
+            const ssize_t got = write ? ::pwrite(fd, buf + lo, hi - lo, static_cast<off_t>(offset + lo))
+                                      : ::pread(fd, buf + lo, hi - lo, static_cast<off_t>(offset + lo));
+            if (got <= 0) {
+                ok[t] = false;
+                return;
+            }
+            lo += static_cast<size_t>(got);
+        }
+    };
+    std::thread th[kThreads - 1];
+    for (int t = 1; t < nt; ++t) th[t - 1] = std::thread(work, t);
+    work(0);
+    for (int t = 1; t < nt; ++t) th[t - 1].join();
+    for (int t = 0; t < nt; ++t)
+        if (!ok[t]) return false;
+    return true;
+}
 
 struct Header {
     uint64_t rows, cols, nnz;

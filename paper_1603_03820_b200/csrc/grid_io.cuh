@@ -15,8 +15,6 @@
 
 #include <condition_variable>
 #include <deque>
-#include <fcntl.h>
-#include <unistd.h>
 #include <fstream>
 #include <mutex>
 #include <string>
@@ -111,34 +109,6 @@ struct PinnedPool {
 PinnedPool& pinned_pool() {
     static PinnedPool* p = new PinnedPool();  // never destroyed: outlives the CUDA context teardown
     return *p;
-}
-
-// Read bytes at offset from the open file with up to kReaders threads (pread: no shared file
-// position); the size was checked against the header, so a short read is a truncation.
-void parallel_pread(File& in, char* dst, size_t bytes, size_t offset) {
-    constexpr int kReaders = 4;
-    const int fd = fileno(in.f);
-    // small blocks: one reader (thread start-up would cost more than it saves)
-    const int readers = bytes >= (size_t(8) << 20) ? kReaders : 1;
-    const size_t piece = (bytes + readers - 1) / readers;
-    bool ok[kReaders] = {true, true, true, true};
-    auto work = [&](int t) {
-        size_t lo = std::min(bytes, piece * t), hi = std::min(bytes, lo + piece);
-        while (lo < hi) {
-            const ssize_t got = ::pread(fd, dst + lo, hi - lo, static_cast<off_t>(offset + lo));
-            if (got <= 0) {
-                ok[t] = false;
-                return;
-            }
-            lo += static_cast<size_t>(got);
-        }
-    };
-    std::thread th[kReaders - 1];
-    for (int t = 1; t < readers; ++t) th[t - 1] = std::thread(work, t);
-    work(0);
-    for (int t = 1; t < readers; ++t) th[t - 1].join();
-    for (bool o : ok)
-        if (!o) fail_io(in.path + ": truncated while reading values");
 }
 
 class DeviceBlockStream {
@@ -258,7 +228,7 @@ class DeviceBlockStream {
             // the payload after the 40-byte header is already the slot layout
             // (row_ptr | col_idx | values): one read, split over a few threads (a single
             // reader tops out near 6.5 GB/s from the page cache)
-            parallel_pread(in, s.host, bytes, 40);
+            if (!parallel_pio(fileno(in.f), s.host, bytes, 40, false)) fail_io(in.path + ": truncated while reading values");
             Validator val{rp, rows, static_cast<int64_t>(h.cols), nnz, in.path};
             val.ends();
             ALSK_CUDA(cudaMemcpyAsync(s.dev, s.host, bytes, cudaMemcpyHostToDevice, upload_));
