@@ -998,19 +998,24 @@ alsk_status alsk_dev_load_cache(const char* path, int64_t* row_ptr, int32_t* col
             ~Drain() { cudaStreamSynchronize(s); }  // the buffers are reused by the next load
         } drain{s};
         int buf = 0;
-        auto stream_array = [&](void* dst, size_t elem, int64_t count, const char* what) {
+        // positional, multi-threaded reads of each chunk (the size matched the header, so a
+        // short read is a truncation)
+        auto stream_array = [&](void* dst, size_t elem, int64_t count, const char* what, size_t file_off) {
             const int64_t per = static_cast<int64_t>(kChunk / elem);
             for (int64_t k0 = 0; k0 < count; k0 += per, buf ^= 1) {
                 const int64_t k1 = std::min(count, k0 + per);
                 ALSK_CUDA(cudaEventSynchronize(done[buf]));  // the previous upload from this buffer is done
-                in.read(stage[buf], elem * (k1 - k0), what);
+                if (!parallel_pio(fileno(in.f), static_cast<char*>(stage[buf]), elem * (k1 - k0), file_off + elem * k0,
+                                  false))
+                    fail_io(in.path + ": truncated while reading " + what);
                 ALSK_CUDA(cudaMemcpyAsync(static_cast<char*>(dst) + elem * k0, stage[buf], elem * (k1 - k0),
                                           cudaMemcpyHostToDevice, s));
                 ALSK_CUDA(cudaEventRecord(done[buf], s));
             }
         };
-        stream_array(col_idx, sizeof(int32_t), nnz, "col_idx");
-        stream_array(values, sizeof(float), nnz, "values");
+        const size_t ci_off = 40 + sizeof(int64_t) * static_cast<size_t>(rows + 1);
+        stream_array(col_idx, sizeof(int32_t), nnz, "col_idx", ci_off);
+        stream_array(values, sizeof(float), nnz, "values", ci_off + sizeof(int32_t) * static_cast<size_t>(nnz));
         // the CSR invariants are checked in HBM (validate.cu), the host only reads and copies
         const int64_t bad = csr_first_bad_row(row_ptr, col_idx, rows, static_cast<int64_t>(h.cols), nnz, s);
         if (bad >= 0) report_bad_row(rp.data(), rows, static_cast<int64_t>(h.cols), nnz, in.path, bad, col_idx, s);
