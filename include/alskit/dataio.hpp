@@ -1,11 +1,12 @@
-// alskit drop-in (B200): the binary ratings cache and the factor checkpoints of the
-// reference's proj/include/alskit/dataio.hpp:116-163 and 546-786, served by
-// libalskit_cuda.so (same file formats, names and IoError texts). The other dataio.hpp
-// members (text loaders, split, BlockStream) are outside the hot-path scope.
+// alskit drop-in (B200): the binary ratings cache, grid persistence and block streaming, and
+// the factor checkpoints of the reference's proj/include/alskit/dataio.hpp:116-163, 352-540
+// and 546-786, served by libalskit_cuda.so (same file formats, names and IoError texts).
+// The text loaders and duplicate_synthesize are outside the hot-path scope.
 #pragma once
 
 #include <filesystem>
 #include <optional>
+#include <vector>
 #include <string>
 
 #include "alskit/common.hpp"
@@ -34,6 +35,103 @@ inline CsrMatrix load_binary_cache(const std::filesystem::path& path) {
     detail::check(alsk_load_cache(path.c_str(), a.row_ptr.data(), a.col_idx.data(), a.values.data()));
     return a;
 }
+
+// ---- grid persistence and streaming (dataio.hpp:352-540) ----
+
+struct GridMeta {  // dataio.hpp:354-361
+    int p = 1;
+    int q = 1;
+    offset_t rows = 0;
+    offset_t cols = 0;
+    std::vector<offset_t> row_cuts;
+    std::vector<offset_t> col_cuts;
+};
+
+struct BlockRef {  // dataio.hpp:364-369
+    int i = 0;
+    int j = 0;
+    friend bool operator==(const BlockRef&, const BlockRef&) = default;
+};
+
+namespace detail {
+inline std::filesystem::path block_path(const std::filesystem::path& dir, int i, int j) {
+    char buf[4096];
+    check(alsk_block_path(dir.c_str(), i, j, buf, sizeof buf));
+    return buf;
+}
+}  // namespace detail
+
+/// dataio.hpp:381-400
+inline void persist_grid(const GridPartition& grid, const std::filesystem::path& dir) {
+    detail::check(alsk_persist_grid_meta(dir.c_str(), grid.p, grid.q, grid.rows, grid.cols, grid.row_cuts.data(),
+                                         grid.col_cuts.data()));
+    for (int j = 0; j < grid.q; ++j)
+        for (int i = 0; i < grid.p; ++i) save_binary_cache(grid.block(i, j), detail::block_path(dir, i, j));
+}
+
+/// dataio.hpp:402-419
+inline GridMeta load_grid_meta(const std::filesystem::path& dir) {
+    GridMeta m;
+    detail::check(alsk_grid_meta(dir.c_str(), &m.p, &m.q, &m.rows, &m.cols, nullptr, nullptr));
+    m.row_cuts.resize(static_cast<std::size_t>(m.q) + 1);
+    m.col_cuts.resize(static_cast<std::size_t>(m.p) + 1);
+    detail::check(alsk_grid_meta(dir.c_str(), &m.p, &m.q, &m.rows, &m.cols, m.row_cuts.data(), m.col_cuts.data()));
+    return m;
+}
+
+/// dataio.hpp:423-439 (host copy of one block)
+inline CsrMatrix load_block(const std::filesystem::path& dir, const GridMeta& meta, int i, int j) {
+    if (i < 0 || i >= meta.p || j < 0 || j >= meta.q)
+        throw InputError("block (" + std::to_string(i) + ", " + std::to_string(j) + ") lies outside the " +
+                         std::to_string(meta.p) + "x" + std::to_string(meta.q) + " grid");
+    try {
+        CsrMatrix b = load_binary_cache(detail::block_path(dir, i, j));
+        if (b.rows != meta.row_cuts[static_cast<std::size_t>(j) + 1] - meta.row_cuts[static_cast<std::size_t>(j)] ||
+            b.cols != meta.cols)
+            throw IoError("shape does not match the grid metadata");
+        b.col_offset = meta.col_cuts[static_cast<std::size_t>(i)];
+        return b;
+    } catch (const IoError& e) {
+        throw IoError("block (" + std::to_string(i) + ", " + std::to_string(j) + "): " + std::string(e.what()));
+    }
+}
+
+/// dataio.hpp:528-534
+inline std::vector<BlockRef> row_major_order(const GridMeta& meta) {
+    std::vector<BlockRef> order;
+    for (int j = 0; j < meta.q; ++j)
+        for (int i = 0; i < meta.p; ++i) order.push_back({i, j});
+    return order;
+}
+
+/// BlockStream (dataio.hpp:447-524) into HBM: next() yields each block's device arrays
+/// (valid until the following next(), which orders their reuse after `stream`).
+class DeviceBlockStream {
+  public:
+    struct Block {
+        BlockRef ref;
+        alsk_csr device;  // rows, cols, col_offset, nnz and device pointers
+    };
+    DeviceBlockStream(const std::filesystem::path& dir, const std::vector<BlockRef>& order) {
+        std::vector<int> flat;
+        for (const BlockRef& b : order) flat.insert(flat.end(), {b.i, b.j});
+        detail::check(alsk_block_stream_open(dir.c_str(), flat.data(), static_cast<int>(order.size()), &h_));
+    }
+    ~DeviceBlockStream() { alsk_block_stream_close(h_); }
+    DeviceBlockStream(const DeviceBlockStream&) = delete;
+    DeviceBlockStream& operator=(const DeviceBlockStream&) = delete;
+
+    std::optional<Block> next(void* stream = nullptr) {
+        int has = 0;
+        Block b{};
+        detail::check(alsk_block_stream_next(h_, stream, &has, &b.ref.i, &b.ref.j, &b.device));
+        if (!has) return std::nullopt;
+        return b;
+    }
+
+  private:
+    void* h_ = nullptr;
+};
 
 // ---- checkpoints (dataio.hpp:546-786) ----
 

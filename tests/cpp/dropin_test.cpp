@@ -93,6 +93,30 @@ int main() {
         std::fputs("this is not a cache file at all, but long enough to read", fj);
         std::fclose(fj);
         CHECK(throws_with<IoError>([&] { load_binary_cache(junk); }, "bad magic"));
+        // grid persistence and streaming (dataio.hpp:352-540)
+        {
+            std::mt19937_64 rg(23);
+            const CsrMatrix big = csr_from_triplets(40, 30, random_triplets(rg, 40, 30, 300));
+            const GridPartition g = grid_partition(big, 3, 2);
+            const auto gd = dir / "grid";
+            persist_grid(g, gd);
+            const GridMeta meta = load_grid_meta(gd);
+            CHECK(meta.p == 3 && meta.q == 2 && meta.row_cuts == g.row_cuts && meta.col_cuts == g.col_cuts);
+            const CsrMatrix b = load_block(gd, meta, 1, 1);
+            CHECK(b.col_offset == g.block(1, 1).col_offset && b.col_idx == g.block(1, 1).col_idx &&
+                  b.values == g.block(1, 1).values);
+            CHECK(throws_with<InputError>([&] { load_block(gd, meta, 3, 0); }, "lies outside the 3x2 grid"));
+            int n = 0;
+            offset_t nnz = 0;
+            DeviceBlockStream bs(gd, row_major_order(meta));
+            while (auto blk = bs.next()) {
+                CHECK(blk->ref == row_major_order(meta)[static_cast<std::size_t>(n)]);
+                CHECK(blk->device.nnz == g.block(blk->ref.i, blk->ref.j).nnz());
+                nnz += blk->device.nnz;
+                ++n;
+            }
+            CHECK(n == 6 && nnz == big.nnz());
+        }
         // checkpoints (dataio.hpp:546-786)
         const FactorMatrix fx = random_factor(9, 4, 5);
         const auto ck = dir / "ck";
