@@ -119,10 +119,10 @@ def test_errors_match_the_reference(A, ref, tmp_path):
 
 
 # ---------------------------------------------------------------- device writer and resume
-def _session(A, seed=3):
+def _session(A, seed=3, fp64=True):
     from paper_1603_03820_b200.session import AlsSession
     r = A.synth_csr(700, 300, 9000, seed)
-    cfg = A.SolverConfig(f=24, lambda_=0.05, accumulate_double=True)
+    cfg = A.SolverConfig(f=24, lambda_=0.05, accumulate_double=fp64)
     x0 = A.random_factor(r.rows, cfg.f, 42)
     t0 = A.random_factor(r.cols, cfg.f, A.mix_seed(42, 1))
     return r, cfg, lambda: AlsSession(r, None, None, cfg, x0, t0)
@@ -162,13 +162,15 @@ def test_device_writer_errors_are_sticky(A, gpu, tmp_path):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("precision", ["fp64", "fp32_tensor"])
 @pytest.mark.parametrize("stop_after", ["x", "theta"])
-def test_resume_is_bit_exact(A, gpu, tmp_path, stop_after):
+def test_resume_is_bit_exact(A, gpu, tmp_path, stop_after, precision):
     """test_driver.cpp:280-317: a run interrupted and resumed ends with the same factors as
     an uninterrupted one. Interrupted after Theta@2, or after X@3 (the dangling X case:
-    Theta@3 is recomputed first)."""
+    Theta@3 is recomputed first). Both precisions: the tensor-core path is deterministic
+    too (no atomics in the Hermitian or the solve)."""
     from paper_1603_03820_b200.session import train_resumable
-    r, cfg, make = _session(A)
+    r, cfg, make = _session(A, fp64=precision == "fp64")
     full = make()
     start, rows = train_resumable(full, 5, tmp_path / "full", digest=99)
     assert start == 1 and [m.iteration for m in rows] == [1, 2, 3, 4, 5]
