@@ -470,10 +470,8 @@ def split_train_test(r: CsrMatrix, holdout_fraction: float, seed: int) -> SplitR
     """dataio.hpp:251-290 (host, bit-exact)."""
     c = r._c()
     k = C.c_int64()
-    st = LIB.alsk_split_train_test(C.byref(c), holdout_fraction, seed & (2**64 - 1), C.byref(k),
-                                   None, None, None, None)
-    if st != 0:
-        raise InputError("holdout fraction must lie strictly between 0 and 1")
+    _check(LIB.alsk_split_train_test(C.byref(c), holdout_fraction, seed & (2**64 - 1), C.byref(k),
+                                     None, None, None, None))
     kk = k.value
     trp = np.empty(r.rows + 1, np.int64)
     tci = np.empty(r.nnz() - kk, np.int32)
@@ -489,9 +487,7 @@ def synth_csr(m: int, n: int, nnz: int, seed: int, threads: int = 0) -> CsrMatri
     rp = np.empty(m + 1, np.int64)
     ci = np.empty(nnz, np.int32)
     va = np.empty(nnz, np.float32)
-    st = LIB.alsk_synth_csr(m, n, nnz, seed & (2**64 - 1), threads, _p(rp), _p(ci), _p(va))
-    if st != 0:
-        raise InputError("invalid synthetic shape")
+    _check(LIB.alsk_synth_csr(m, n, nnz, seed & (2**64 - 1), threads, _p(rp), _p(ci), _p(va)))
     return CsrMatrix(m, n, 0, rp, ci, va)
 
 

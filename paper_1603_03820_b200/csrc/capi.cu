@@ -38,6 +38,9 @@ struct Profile {
 
 }  // namespace
 
+// For the host-only entry points (host_data.cpp), which return a status without a guard.
+void set_last_error(const char* msg) { t_error = msg; }
+
 bool prof_on() { return g_prof.on; }
 void prof_add(int phase, float ms) {
     g_prof.phase_ms[phase] += ms;

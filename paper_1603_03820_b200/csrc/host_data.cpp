@@ -13,6 +13,10 @@
 
 #include "alskit_cuda.h"
 
+namespace alsk {
+void set_last_error(const char* msg);  // capi.cu
+}
+
 namespace {
 
 // splitmix64 finaliser (common.hpp:70-75)
@@ -55,7 +59,10 @@ void alsk_random_factor(int64_t rows, int f, uint64_t seed, float* out) {
 alsk_status alsk_split_train_test(const alsk_csr* r, double holdout, uint64_t seed, int64_t* k_out,
                                   int64_t* train_row_ptr, int32_t* train_col_idx,
                                   float* train_values, alsk_triplet* test_out) {
-    if (!(holdout > 0.0) || !(holdout < 1.0)) return ALSK_ERR_INPUT;
+    if (!(holdout > 0.0) || !(holdout < 1.0)) {  // dataio.hpp:253-254
+        alsk::set_last_error("holdout fraction must lie strictly between 0 and 1");
+        return ALSK_ERR_INPUT;
+    }
     const int64_t nnz = r->nnz;
     const int64_t k = static_cast<int64_t>(std::floor(holdout * static_cast<double>(nnz)));
     *k_out = k;
@@ -136,13 +143,19 @@ extern "C" {
 
 alsk_status alsk_synth_csr(int64_t m, int64_t n, int64_t nnz, uint64_t seed, int threads,
                            int64_t* row_ptr, int32_t* col_idx, float* values) {
-    if (m < 1 || n < 1 || nnz < 0) return ALSK_ERR_INPUT;
+    if (m < 1 || n < 1 || nnz < 0) {
+        alsk::set_last_error("invalid synthetic shape");
+        return ALSK_ERR_INPUT;
+    }
     const uint64_t seed_x = mix_seed(seed, 1001), seed_t = mix_seed(seed, 1002);
     for (int64_t u = 0; u <= m; ++u)
         row_ptr[u] = static_cast<int64_t>((static_cast<unsigned __int128>(nnz) * static_cast<uint64_t>(u)) /
                                           static_cast<uint64_t>(m));
     for (int64_t u = 0; u < m; ++u)
-        if (row_ptr[u + 1] - row_ptr[u] > n) return ALSK_ERR_INPUT;  // more ratings than columns
+        if (row_ptr[u + 1] - row_ptr[u] > n) {  // more ratings than columns
+            alsk::set_last_error("invalid synthetic shape: a row would need more ratings than columns");
+            return ALSK_ERR_INPUT;
+        }
     if (threads <= 0) threads = static_cast<int>(std::max(1u, std::thread::hardware_concurrency()));
     std::vector<float> tstar(static_cast<size_t>(n) * kPlanted);
     parallel_rows(n, threads, [&](int64_t v0, int64_t v1) {

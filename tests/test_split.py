@@ -22,6 +22,8 @@ def test_fraction_outside_unit_interval_is_an_input_error(A):
         st = N.LIB.alsk_dev_split_train_test(C.byref(c), frac, 1, C.byref(k), None, None, None, None, None)
         assert st == 1
         assert N.LIB.alsk_last_error().decode() == "holdout fraction must lie strictly between 0 and 1"
+        with pytest.raises(A.InputError, match="^holdout fraction must lie strictly between 0 and 1$"):
+            A.split_train_test(r, frac, 1)  # the host split reports the same text
     assert N.LIB.alsk_dev_split_train_test(C.byref(c), 0.25, 1, C.byref(k), None, None, None, None, None) == 0
     assert k.value == 2  # floor(10 * 0.25)
 
