@@ -25,6 +25,33 @@ __device__ __forceinline__ double dot_rows(const float* __restrict__ a, const fl
     return s;
 }
 
+// The same dot with 16-byte operand loads (f % 4 == 0, 16-byte aligned rows): the products
+// are still added one by one in ascending index order, so the result is bit-identical to
+// dot_rows; a lane's gathered row costs f/4 load instructions instead of f.
+__device__ __forceinline__ double dot_rows4(const float* __restrict__ a, const float* __restrict__ b, int f) {
+    const float4* a4 = reinterpret_cast<const float4*>(a);
+    const float4* b4 = reinterpret_cast<const float4*>(b);
+    double s = 0.0;
+    for (int i = 0; i < f / 4; ++i) {
+        const float4 p = a4[i], q = __ldg(b4 + i);
+        s += static_cast<double>(p.x) * static_cast<double>(q.x);
+        s += static_cast<double>(p.y) * static_cast<double>(q.y);
+        s += static_cast<double>(p.z) * static_cast<double>(q.z);
+        s += static_cast<double>(p.w) * static_cast<double>(q.w);
+    }
+    return s;
+}
+
+template <bool VEC>
+__device__ __forceinline__ double dot_any(const float* __restrict__ a, const float* __restrict__ b, int f) {
+    if constexpr (VEC) return dot_rows4(a, b, f);
+    else return dot_rows(a, b, f);
+}
+
+inline bool vec4_ok(const float* a, const float* b, int f) {
+    return f % 4 == 0 && (reinterpret_cast<uintptr_t>(a) & 15) == 0 && (reinterpret_cast<uintptr_t>(b) & 15) == 0;
+}
+
 // Deterministic block reduction of one double per thread; result in thread 0.
 __device__ __forceinline__ double block_sum(double v) {
     __shared__ double red[kThreads / 32];
@@ -40,6 +67,7 @@ __device__ __forceinline__ double block_sum(double v) {
 }
 
 // Squared residuals over the CSR; one warp per row, lanes over the row's ratings.
+template <bool VEC>
 __global__ void loss_sq_kernel(const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col_idx,
                                const float* __restrict__ values, int64_t rows,
                                const float* __restrict__ x, const float* __restrict__ theta, int f,
@@ -52,7 +80,7 @@ __global__ void loss_sq_kernel(const int64_t* __restrict__ row_ptr, const int32_
         const float* xu = x + u * f;
         for (int64_t k = row_ptr[u] + lane; k < row_ptr[u + 1]; k += 32) {
             const double d = static_cast<double>(values[k]) -
-                             dot_rows(xu, theta + static_cast<int64_t>(col_idx[k]) * f, f);
+                             dot_any<VEC>(xu, theta + static_cast<int64_t>(col_idx[k]) * f, f);
             acc += d * d;
         }
     }
@@ -92,6 +120,7 @@ __global__ void col_count_kernel(const int32_t* __restrict__ col_idx, int64_t nn
         atomicAdd(counts + col_idx[k], 1ull);
 }
 
+template <bool VEC>
 __global__ void rmse_kernel(const int64_t* __restrict__ rows, const int64_t* __restrict__ cols,
                             const float* __restrict__ values, int64_t count,
                             const float* __restrict__ x, int64_t x_rows,
@@ -105,7 +134,7 @@ __global__ void rmse_kernel(const int64_t* __restrict__ rows, const int64_t* __r
             atomicMin(first_bad, static_cast<unsigned long long>(t));
             continue;
         }
-        const double d = static_cast<double>(values[t]) - dot_rows(x + r * f, theta + c * f, f);
+        const double d = static_cast<double>(values[t]) - dot_any<VEC>(x + r * f, theta + c * f, f);
         acc += d * d;
     }
     const double t = block_sum(acc);
@@ -142,7 +171,10 @@ double loss_device(const DevCsr& r, const int64_t* col_nnz, const float* x, cons
     DevBuf partial(sizeof(double) * 3 * kMaxBlocks, s);
     double* p = partial.as<double>();
     const int b1 = blocks_for(r.rows * 32, kThreads);
-    loss_sq_kernel<<<b1, kThreads, 0, s>>>(r.row_ptr, r.col_idx, r.values, r.rows, x, theta, f, p);
+    if (vec4_ok(x, theta, f))
+        loss_sq_kernel<true><<<b1, kThreads, 0, s>>>(r.row_ptr, r.col_idx, r.values, r.rows, x, theta, f, p);
+    else
+        loss_sq_kernel<false><<<b1, kThreads, 0, s>>>(r.row_ptr, r.col_idx, r.values, r.rows, x, theta, f, p);
     ALSK_LAUNCHED();
     const int b2 = blocks_for(r.rows, kThreads);
     reg_kernel<<<b2, kThreads, 0, s>>>(r.row_ptr, nullptr, r.rows, x, f, p + kMaxBlocks);
@@ -164,8 +196,12 @@ double rmse_device(const int64_t* rows, const int64_t* cols, const float* values
     DevBuf bad(sizeof(unsigned long long), s);
     ALSK_CUDA(cudaMemsetAsync(bad.as<void>(), 0xff, sizeof(unsigned long long), s));
     const int b = blocks_for(count, kThreads);
-    rmse_kernel<<<b, kThreads, 0, s>>>(rows, cols, values, count, x, x_rows, theta, theta_rows, f,
-                                       partial.as<double>(), bad.as<unsigned long long>());
+    if (vec4_ok(x, theta, f))
+        rmse_kernel<true><<<b, kThreads, 0, s>>>(rows, cols, values, count, x, x_rows, theta, theta_rows, f,
+                                                 partial.as<double>(), bad.as<unsigned long long>());
+    else
+        rmse_kernel<false><<<b, kThreads, 0, s>>>(rows, cols, values, count, x, x_rows, theta, theta_rows, f,
+                                                  partial.as<double>(), bad.as<unsigned long long>());
     ALSK_LAUNCHED();
     unsigned long long first_bad = 0;
     d2h(&first_bad, bad.as<unsigned long long>(), 1, s);
