@@ -692,10 +692,12 @@ bool dispatch_tc(const DevCsr& r, const float* theta, int64_t theta_rows, int f,
     strided(th, theta, theta_rows, f, s);
     const int nb = (f + 1 + 7) / 8;
     const int64_t pkn = packed_stride(f);
-    // packed rows per batch: the scratch size (ALSK_TC_SCRATCH_MB, default 4096 MB) over the row size
+    // packed rows per batch: the scratch size (ALSK_TC_SCRATCH_MB, default 11264 MB: a
+    // Netflix-shape X half in one batch, 0.5% faster per iteration than 4096 MB in three;
+    // allocated only up to what the half needs) over the row size
     static const int64_t scratch_mb = [] {
         const char* e = std::getenv("ALSK_TC_SCRATCH_MB");
-        return e ? std::max<int64_t>(64, std::atoll(e)) : int64_t(4096);
+        return e ? std::max<int64_t>(64, std::atoll(e)) : int64_t(11264);
     }();
     const int64_t batch = std::min<int64_t>(re - rb, std::max<int64_t>(1, (scratch_mb << 20) / (pkn * 4)));
     // packed-row scratch kept for the process (grow-only, never freed): a per-call ~1 GB
