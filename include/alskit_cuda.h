@@ -358,6 +358,31 @@ alsk_status alsk_dev_split_train_test(const alsk_csr* r, double holdout, uint64_
 alsk_status alsk_synth_csr(int64_t m, int64_t n, int64_t nnz, uint64_t seed, int threads,
                            int64_t* row_ptr, int32_t* col_idx, float* values);
 
+/* ---- per-rank synthetic data (the bench's multi-GPU setup) ------------------------- */
+/* Rows [row_begin,row_end) of alsk_synth_csr's matrix generated in HBM, bit-identical to the
+ * host generator; row_ptr (row_end-row_begin+1) starts at 0. Row degrees must be <= 1024. */
+alsk_status alsk_dev_synth_rows(int64_t m, int64_t n, int64_t nnz, uint64_t seed, int64_t row_begin, int64_t row_end,
+                                int64_t* row_ptr, int32_t* col_idx, float* values, void* stream);
+/* Global offset of row u in that matrix: floor(nnz * u / m). */
+int64_t alsk_synth_row_start(int64_t m, int64_t nnz, int64_t u);
+/* The held-out positions of split_train_test (dataio.hpp:251-290; same Fisher-Yates draws)
+ * as a bitmask of ceil(nnz/32) words (bit k set = entry k held out); mask_out NULL: only
+ * *k_out. */
+alsk_status alsk_holdout_mask(int64_t nnz, double holdout, uint64_t seed, uint32_t* mask_out, int64_t* k_out);
+/* Set bits of a host mask in [bit_begin, bit_end). */
+int64_t alsk_mask_count(const uint32_t* mask, int64_t bit_begin, int64_t bit_end);
+/* Split a device CSR (or a row chunk of a larger one) by a device bitmask: entry k is held
+ * out when bit (k - row_ptr[0] + bit_offset) is set. Train arrays sized for r->nnz, test
+ * triplets for the held count (row ids + row_base); *train_nnz set on return. */
+alsk_status alsk_dev_split_mask(const alsk_csr* r, const uint32_t* d_mask, int64_t bit_offset, int64_t row_base,
+                                int64_t* train_row_ptr, int32_t* train_col_idx, float* train_values,
+                                alsk_triplet* test_out, int64_t* train_nnz, void* stream);
+/* Entries with col_begin <= col < col_end of every row, order kept, columns rebased to
+ * col - col_begin (a model-parallel rank's item slice). col_idx_out NULL: row_ptr_out
+ * (rows+1) and *nnz_out only. */
+alsk_status alsk_dev_filter_columns(const alsk_csr* r, int64_t col_begin, int64_t col_end, int64_t* row_ptr_out,
+                                    int32_t* col_idx_out, float* values_out, int64_t* nnz_out, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

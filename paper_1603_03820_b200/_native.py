@@ -107,6 +107,12 @@ _SIGS = {
     "alsk_mix_seed": (u64, [u64, u64]),
     "alsk_split_train_test": (C.c_int, [CsrP, C.c_double, u64, i64p, vp, vp, vp, vp]),
     "alsk_synth_csr": (C.c_int, [i64, i64, i64, u64, C.c_int, vp, vp, vp]),
+    "alsk_dev_synth_rows": (C.c_int, [i64, i64, i64, u64, i64, i64, vp, vp, vp, vp]),
+    "alsk_synth_row_start": (i64, [i64, i64, i64]),
+    "alsk_holdout_mask": (C.c_int, [i64, C.c_double, u64, vp, i64p]),
+    "alsk_mask_count": (i64, [vp, i64, i64]),
+    "alsk_dev_split_mask": (C.c_int, [CsrP, vp, i64, i64, vp, vp, vp, vp, i64p, vp]),
+    "alsk_dev_filter_columns": (C.c_int, [CsrP, i64, i64, vp, vp, vp, i64p, vp]),
 }
 
 

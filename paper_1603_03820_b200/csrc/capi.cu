@@ -750,6 +750,61 @@ alsk_status alsk_dev_split_train_test(const alsk_csr* r, double holdout, uint64_
     });
 }
 
+// ---- per-rank synthetic data (bench / multi-GPU setup) ------------------------------
+alsk_status alsk_dev_synth_rows(int64_t m, int64_t n, int64_t nnz, uint64_t seed, int64_t row_begin, int64_t row_end,
+                                int64_t* row_ptr, int32_t* col_idx, float* values, void* stream) {
+    return guard([&] {
+        require_device();
+        synth_rows_device(m, n, nnz, seed, row_begin, row_end, row_ptr, col_idx, values, as_stream(stream));
+    });
+}
+
+int64_t alsk_synth_row_start(int64_t m, int64_t nnz, int64_t u) { return synth_row_start(nnz, m, u); }
+
+alsk_status alsk_holdout_mask(int64_t nnz, double holdout, uint64_t seed, uint32_t* mask_out, int64_t* k_out) {
+    return guard([&] {
+        const int64_t k = split_holdout_count(nnz, holdout);
+        *k_out = k;
+        if (mask_out == nullptr) return;
+        std::vector<uint32_t> mask;
+        holdout_mask_host(nnz, k, seed, mask);
+        std::memcpy(mask_out, mask.data(), sizeof(uint32_t) * mask.size());
+    });
+}
+
+int64_t alsk_mask_count(const uint32_t* mask, int64_t bit_begin, int64_t bit_end) {
+    int64_t c = 0;
+    for (int64_t b = bit_begin; b < bit_end;) {
+        if ((b & 31) == 0 && b + 32 <= bit_end) {
+            c += __builtin_popcount(mask[b >> 5]);
+            b += 32;
+        } else {
+            c += (mask[b >> 5] >> (b & 31)) & 1u;
+            ++b;
+        }
+    }
+    return c;
+}
+
+alsk_status alsk_dev_split_mask(const alsk_csr* r, const uint32_t* d_mask, int64_t bit_offset, int64_t row_base,
+                                int64_t* train_row_ptr, int32_t* train_col_idx, float* train_values,
+                                alsk_triplet* test_out, int64_t* train_nnz, void* stream) {
+    return guard([&] {
+        require_device();
+        *train_nnz = split_with_mask_device(dev_view(r), d_mask, bit_offset, row_base, train_row_ptr, train_col_idx,
+                                            train_values, test_out, as_stream(stream));
+    });
+}
+
+alsk_status alsk_dev_filter_columns(const alsk_csr* r, int64_t col_begin, int64_t col_end, int64_t* row_ptr_out,
+                                    int32_t* col_idx_out, float* values_out, int64_t* nnz_out, void* stream) {
+    return guard([&] {
+        require_device();
+        *nnz_out = filter_columns_device(dev_view(r), col_begin, col_end, row_ptr_out, col_idx_out, values_out,
+                                         as_stream(stream));
+    });
+}
+
 alsk_status alsk_dev_partial_hermitian(const alsk_csr* r, const float* theta, int64_t theta_rows,
                                        int f, double lambda, int64_t row_begin, int64_t row_end,
                                        double* out_packed, void* stream) {

@@ -126,6 +126,21 @@ int64_t csr_first_bad_row(const int64_t* rp, const int32_t* ci, int64_t rows, in
                           cudaStream_t s);
 
 // split_train_test on the device (split.cu; dataio.hpp:251-290)
+void holdout_mask_host(int64_t nnz, int64_t k, uint64_t seed, std::vector<uint32_t>& mask);
+int64_t split_with_mask_device(const DevCsr& r, const uint32_t* dmask, int64_t bit_offset, int64_t row_base,
+                               int64_t* train_row_ptr, int32_t* train_col_idx, float* train_values,
+                               alsk_triplet* test, cudaStream_t s);
+
+// Device synthetic generator (synth.cu), bit-identical to alsk_synth_csr: rows [rb, re)
+// with row pointers rebased to 0. Row degrees are at most kSynthMaxDegree.
+constexpr int kSynthMaxDegree = 1024;
+int64_t synth_row_start(int64_t nnz, int64_t m, int64_t u);
+void synth_rows_device(int64_t m, int64_t n, int64_t nnz, uint64_t seed, int64_t rb, int64_t re, int64_t* row_ptr,
+                       int32_t* col_idx, float* values, cudaStream_t s);
+// Entries with lo <= col < hi of every row, order kept, columns rebased to col - lo; with
+// col_idx_out == NULL only row_ptr_out (rows+1) and the returned total are produced.
+int64_t filter_columns_device(const DevCsr& r, int64_t lo, int64_t hi, int64_t* row_ptr_out, int32_t* col_idx_out,
+                              float* values_out, cudaStream_t s);
 int64_t split_holdout_count(int64_t nnz, double holdout);
 void split_train_test_device(const DevCsr& r, double holdout, uint64_t seed, int64_t* train_row_ptr,
                              int32_t* train_col_idx, float* train_values, alsk_triplet* test, cudaStream_t s);
