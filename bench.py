@@ -1,23 +1,33 @@
 #!/usr/bin/env python
-"""bench.py — seconds per ALS iteration (X half-sweep + Theta half-sweep) on the
-Netflix-shape synthetic workload (480,189 x 17,770, 99M ratings, 10% holdout, f=100,
-lambda=0.05), BASELINE.json's metric.
+"""bench.py — seconds per ALS iteration (X half-sweep + Theta half-sweep), BASELINE.json's
+metric, on the Netflix-shape synthetic workload by default (480,189 x 17,770, 99M ratings,
+10% holdout, f=100, lambda=0.05); --config picks another named shape (ml1m, yahoo,
+hugewiki, sparkals).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config netflix]
 
-N>1 runs under torchrun, one rank per GPU: rows of X (then Theta) are model-partitioned
-over the ranks with the other factor replicated, and the solved slices are all-gathered
-over NCCL after each half. Timing: CUDA events on the launching stream
-between barriers + synchronize, max over ranks. Inputs (CSR 713 MB, CSC 713 MB) exceed L2,
-so no explicit flush is needed.
+--gpus N > 1 without torchrun in the environment re-launches itself under
+`torch.distributed.run` with N ranks (127.0.0.1 rendezvous), one process per GPU. Multi-GPU
+runs use libalskit_cuda's C++ session (alsk_mp_*) with NCCL inside the library:
+model-parallel rows of X then Theta with in-place all-gathers (netflix, yahoo, hugewiki), or
+the hybrid split with a data-parallel Theta half and a partial-Hermitian reduce-scatter
+(sparkals). Every rank builds only its own share of the data in HBM from the row-seeded
+generator; the holdout split runs once (rank 0) and travels as a bitmask.
 
-Extra keys: roofline (the tensor-core Hermitian kernel vs the measured dense tensor peak
-taken as TF32 = bf16/2 from MEASURED_PEAKS.json, with the FP32-FFMA-equivalent fraction the
-north star quotes beside it, and the batched-Cholesky phase), cpu_baseline
-(the UNMODIFIED reference compiled into oracle/_ref, timed on this host's cores on a bounded
-row sample, extrapolated by nonzeros), e2e (the same metric through the host-buffer C ABI:
-alsk_update_x / alsk_update_theta on pinned host buffers, H2D + D2H inside the timed region;
-at N > 1 GPUs each rank's input slices from pinned memory around the model-parallel step).
+Timing: W warm-up iterations, then K iterations between a barrier + synchronize on each
+side, CUDA events on the launching stream, max over ranks. Inputs (CSR + CSC of the train
+matrix, >= 1.4 GB at Netflix) exceed L2, so no flush is needed.
+
+Extra keys: roofline (the dominant kernel against its measured peak; for N > 1 also the
+collectives' bytes and bus bandwidth against NVLink), cpu_baseline (the unmodified
+reference, oracle/_ref, run in a separate process on a bounded sample that keeps every
+host thread busy), e2e (the same metric through the host-buffer C ABI, H2D + D2H inside the
+timed region).
+
+--impl reference runs the reference's own train_run iteration (oracle/_ref: update_x on the
+train CSR, then on its transpose; threads = hardware_concurrency) on the same input bytes,
+read from a shared binary cache with the reference's load_binary_cache. That process never
+loads libalskit_cuda.so.
 """
 from __future__ import annotations
 
@@ -25,6 +35,7 @@ import argparse
 import ctypes as C
 import json
 import os
+import socket
 import subprocess
 import sys
 import time
@@ -35,13 +46,31 @@ import numpy as np
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
+# name: (m, n, nnz_total, f, lambda)  — SURVEY.md §8(d); lambdas from PAPER.md Table 4
 CONFIGS = {
-    # name: (m, n, nnz_total, f, lambda)
     "ml1m": (6040, 3706, 1000209, 10, 0.05),
     "netflix": (480189, 17770, 99_000_000, 100, 0.05),
     "yahoo": (1000990, 624961, 252_800_000, 100, 1.4),
+    "hugewiki": (50082604, 39781, 3_100_000_000, 100, 0.05),
+    "sparkals": (660_000_000, 2_400_000, 3_500_000_000, 10, 0.05),
 }
-SHAPE_ID = {"ml1m": 0, "netflix": 1, "yahoo": 2}
+SHAPE_ID = {"ml1m": 0, "netflix": 1, "yahoo": 2, "hugewiki": 3, "sparkals": 4}
+# shapes whose whole matrix the CPU reference can hold and iterate in a bench run
+REF_FULL = {"ml1m", "netflix", "yahoo"}
+RUN_SEED = 42
+MASK64 = (1 << 64) - 1
+
+
+def mix_seed(seed: int, salt: int) -> int:
+    """splitmix64 finaliser (reference common.hpp:70-75)."""
+    z = (seed + 0x9E3779B97F4A7C15 * (salt + 1)) & MASK64
+    z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & MASK64
+    z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & MASK64
+    return z ^ (z >> 31)
+
+
+def data_seed(cfg: str) -> int:
+    return mix_seed(RUN_SEED, 100 + SHAPE_ID[cfg])
 
 
 def parse():
@@ -51,9 +80,16 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="netflix", choices=list(CONFIGS))
+    ap.add_argument("--precision", default="fp32", choices=["fp32", "fp64"],
+                    help="fp32: the FP32 path (tensor cores where 16 <= f <= 119); fp64: the reference-order "
+                         "FP64-exact kernels (SolverConfig.accumulate_double, the drop-in's default)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--e2e-dist", action="store_true", help="the multi-GPU end-to-end leg even at one GPU")
+    ap.add_argument("--cache-dir", default=os.environ.get("ALSK_BENCH_CACHE", "/tmp/alsk_bench_cache"))
+    ap.add_argument("--cpu-sample", action="store_true",
+                    help="(reference arm) the bounded cpu_baseline sample instead of full iterations")
+    ap.add_argument("--ref-max-iters", type=int, default=3, help="(reference arm) cap on timed full iterations")
+    ap.add_argument("--dry-run", action="store_true", help="rendezvous only: every rank reports in, no GPU work")
     return ap.parse_args()
 
 
@@ -61,13 +97,34 @@ def dist_env():
     return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
 
 
-def make_data(cfg_name):
-    """Deterministic synthetic ratings + the reference driver's split (driver.hpp:113)."""
-    from paper_1603_03820_b200 import alskit as A
-    m, n, nnz, f, lam = CONFIGS[cfg_name]
-    R = A.synth_csr(m, n, nnz, A.mix_seed(42, 100 + SHAPE_ID[cfg_name]))
-    sp = A.split_train_test(R, 0.1, A.mix_seed(42, 2))
-    return sp.train, sp.test
+def free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def spawn(args) -> int:
+    """Re-launch this script under torch.distributed.run with --gpus ranks."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={free_port()}", str(Path(__file__).resolve()), *sys.argv[1:]]
+    return subprocess.run(cmd).returncode
+
+
+def cache_path(args) -> Path:
+    return Path(args.cache_dir) / f"{args.config}_{data_seed(args.config):016x}.cache"
+
+
+def cpu_info() -> dict:
+    model = None
+    try:
+        for line in Path("/proc/cpuinfo").read_text().splitlines():
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"cpu_model": model, "hardware_concurrency": os.cpu_count(),
+            "sched_getaffinity": len(os.sched_getaffinity(0))}
 
 
 # ------------------------------------------------------------------ clocks ---------
@@ -111,92 +168,176 @@ class Clocks:
 
 
 # ------------------------------------------------------------------ reference arm --
-def cpu_reference_sample(train, test, cfg_name, target_s=12.0):
-    """Time the UNMODIFIED reference (oracle/_ref) update_x on all host threads, on a row
-    sample of each half, extrapolated to a full iteration by nonzero count. Only the
-    cpu_baseline leg / --impl reference may run this."""
-    from oracle import binding
-    from paper_1603_03820_b200 import alskit as A
+def _ref():
+    from oracle import binding  # the reference arm loads oracle/_ref only
     ref = binding.reference()
     if ref is None:
-        return None
-    m, n, nnz, f, lam = CONFIGS[cfg_name]
-    threads = ref.hardware_threads()
-    csc = A.csr_to_csc(train) if A.device_available() else None
-    if csc is None:
-        st, cp, ri, vv = binding.oracle().csr_to_csc(binding.csr_struct(m, n, train.row_ptr, train.col_idx, train.values))
-        rt = (cp, ri, vv)
-    else:
-        rt = (csc.col_ptr, csc.row_idx, csc.values)
-    x0 = A.random_factor(m, f, 42).entries
-    t0 = A.random_factor(n, f, A.mix_seed(42, 1)).entries
+        raise RuntimeError("oracle/_ref not built (needs /root/reference at build time)")
+    return ref
 
-    def sample(row_ptr, col_idx, values, rows, cols, theta, theta_rows, k):
-        rp = (row_ptr[: k + 1]).copy()
-        nz = int(rp[-1])
-        c = binding.csr_struct(k, cols, rp, col_idx[:nz].copy(), values[:nz].copy())
+
+def ref_prepare(args, ref) -> tuple[dict, int, int]:
+    """Shared binary cache (written once with the reference's save_binary_cache from the
+    shared generator) -> the reference's load / split / transpose / init."""
+    m, n, nnz, f, lam = CONFIGS[args.config]
+    path = cache_path(args)
+    setup = {}
+    if not path.exists():
+        path.parent.mkdir(parents=True, exist_ok=True)
+        tmp = path.with_suffix(f".tmp{os.getpid()}")
         t = time.perf_counter()
-        st, _ = ref.update_x(c, theta, theta_rows, f, lam, acc_double=1, batch_rows=4096, threads=0)
-        dt = time.perf_counter() - t
+        st = ref.bench_write_cache(m, n, nnz, data_seed(args.config), tmp)
         assert st == 0, ref.last_error()
-        return dt, nz
+        os.replace(tmp, path)
+        setup["write_cache_s"] = time.perf_counter() - t
+    st, nz_train, n_test, secs = ref.bench_prepare(path, 0.1, RUN_SEED, f, lam)
+    assert st == 0, ref.last_error()
+    setup.update({"load_binary_cache_s": secs[0], "split_train_test_s": secs[1], "transpose_s": secs[2],
+                  "random_factor_s": secs[3], "cache": str(path)})
+    return setup, nz_train, n_test
 
-    # size the samples from a small probe so each half costs ~target_s/2
-    total_x = int(train.row_ptr[-1])
-    kx = max(64, min(m, 2000))
-    dx, nzx = sample(train.row_ptr, train.col_idx, train.values, m, n, t0, n, kx)
-    kx = int(min(m, max(kx, kx * (target_s / 2) / max(dx, 1e-3))))
-    dx, nzx = sample(train.row_ptr, train.col_idx, train.values, m, n, t0, n, kx)
-    kt = max(4, min(n, 40))
-    dt_, nzt = sample(rt[0], rt[1], rt[2], n, m, x0, m, kt)
-    kt = int(min(n, max(kt, kt * (target_s / 2) / max(dt_, 1e-3))))
-    dt_, nzt = sample(rt[0], rt[1], rt[2], n, m, x0, m, kt)
-    per_iter = dx * total_x / nzx + dt_ * total_x / nzt
+
+def ref_sample(args, ref, nz_train: int) -> dict:
+    """Bounded sample that keeps every reference thread busy: whole update_x batches
+    (batch_rows = 4096, parallel_for chunks of 32 rows, solver.hpp:107, 330-345) of each
+    half, extrapolated to a full iteration by nonzero count."""
+    kx, kt = 32 * 4096, 4096
+    st, dx, dt, nzx, nzt = ref.bench_sample(kx, kt)
+    assert st == 0, ref.last_error()
+    per_iter = dx * nz_train / nzx + dt * nz_train / nzt
+    threads = ref.hardware_threads()
     return {"value": per_iter, "unit": "s/ALS-iter", "cores": threads, "kind": "reference",
-            "sample": f"reference update_x (accumulate_double, threads=0) on the first {kx} rows "
-                      f"({nzx} nnz) of the X-half and {kt} items ({nzt} nnz) of the Theta-half, "
-                      f"{dx:.2f}s + {dt_:.2f}s, extrapolated by nnz to {total_x} train ratings per half"}
+            "sample": f"reference update_x (accumulate_double, threads=0 -> {threads}) on the first {kx} rows "
+                      f"({nzx} nnz) of the X half and the first {kt} items ({nzt} nnz) of the Theta half: "
+                      f"{dx:.2f} s + {dt:.2f} s, extrapolated by nnz to {nz_train} train ratings per half",
+            **cpu_info()}
 
 
 def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
         return
-    train, test = make_data(args.config)
     m, n, nnz, f, lam = CONFIGS[args.config]
-    vals = []
-    base = None
-    for i in range(args.warmup + args.steps):
-        b = cpu_reference_sample(train, test, args.config, target_s=8.0)
-        if b is None:
-            print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built (needs /root/reference at build time)"}))
-            return
-        if i >= args.warmup:
-            vals.append(b["value"])
-        base = b
-    v = float(np.median(vals))
-    base["value"] = v
+    base_line = {"impl": "reference", "metric": f"s/ALS-iter ({args.config}-shape f={f})", "unit": "s/ALS-iter",
+                 "n_gpus": args.gpus, "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
+                 "dtype": "f64-accumulate", "data": "synthetic (planted rank-10 + U[-0.5,0.5) noise; SURVEY §8(d) "
+                 "generator), shared binary cache"}
+    if args.config not in REF_FULL:
+        print(json.dumps({**base_line, "unavailable": f"the CPU reference cannot hold and iterate the "
+                          f"{args.config} shape ({nnz} ratings) within a bench run; see DESIGN.md"}))
+        return
+    ref = _ref()
+    setup, nz_train, n_test = ref_prepare(args, ref)
+    if args.cpu_sample:
+        print(json.dumps(ref_sample(args, ref, nz_train)))
+        return
+    warm = min(args.warmup, 1)
+    steps = max(1, min(args.steps, args.ref_max_iters))
+    for _ in range(warm):
+        st, _, _ = ref.bench_iteration()
+        assert st == 0, ref.last_error()
+    halves = []
+    for _ in range(steps):
+        st, xs, ts = ref.bench_iteration()
+        assert st == 0, ref.last_error()
+        halves.append((xs, ts))
+    it = [x + t for x, t in halves]
+    v = float(np.median(it))
+    st, loss, rmse, loss_s, rmse_s = ref.bench_eval()
+    threads = ref.hardware_threads()
     print(json.dumps({
-        "impl": "reference", "metric": f"s/ALS-iter ({args.config}-shape f={f})", "value": v, "unit": "s/ALS-iter",
-        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": v * 1e3,
-        "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64-accumulate",
-        "data": "synthetic (planted rank-10 + U[-0.5,0.5) noise; SURVEY \u00a78(d) generator)",
-        "config": {"workload": args.config, "m": m, "n": n, "nnz_total": nnz, "nnz_train": int(train.row_ptr[-1]),
-                   "f": f, "lambda": lam, "holdout": 0.1, "parallelism": "host threads (reference thread pool)"},
-        "cpu_baseline": base, "e2e": {"value": v, "unit": "s/ALS-iter", "h2d_bytes_per_step": 0,
-                                      "d2h_bytes_per_step": 0}}))
+        **base_line, "value": v, "steps": steps, "warmup": warm, "steps_requested": args.steps,
+        "warmup_requested": args.warmup, "ms_per_step": v * 1e3,
+        "config": {"workload": args.config, "m": m, "n": n, "nnz_total": nnz, "nnz_train": nz_train, "f": f,
+                   "lambda": lam, "holdout": 0.1, "parallelism": f"host threads (reference thread pool, {threads})"},
+        "iterations_s": [{"x_half": x, "theta_half": t} for x, t in halves],
+        "eval": {"train_J": loss, "test_rmse": rmse, "loss_s": loss_s, "rmse_s": rmse_s,
+                 "note": "serial in the reference; timed apart, not part of the iteration"},
+        "setup": setup,
+        "cpu_baseline": {"value": v, "unit": "s/ALS-iter", "cores": threads, "kind": "reference",
+                         "sample": f"{steps} full iteration(s) of train_run's loop (driver.hpp:256-258) after "
+                                   f"{warm} warm-up, median", **cpu_info()},
+        "e2e": {"value": v, "unit": "s/ALS-iter", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}))
+    ref.bench_release()
+
+
+def cpu_baseline_subprocess(args) -> dict | None:
+    """The reference's bounded sample, in its own process (which never loads libalskit_cuda)."""
+    cmd = [sys.executable, str(Path(__file__).resolve()), "--impl", "reference", "--cpu-sample", "--config",
+           args.config, "--cache-dir", args.cache_dir]
+    env = {k: v for k, v in os.environ.items() if k not in ("RANK", "WORLD_SIZE", "LOCAL_RANK")}
+    res = subprocess.run(cmd, capture_output=True, text=True, env=env, timeout=900)
+    for line in reversed(res.stdout.splitlines()):
+        if line.startswith("{"):
+            return json.loads(line)
+    return {"unavailable": (res.stderr or res.stdout)[-300:]}
 
 
 # ------------------------------------------------------------------ our arm --------
+def dry_run(args):
+    import torch.distributed as dist
+    import torch
+    rank, world, local = dist_env()
+    if world > 1:
+        dist.init_process_group("gloo")
+    seen = [None] * world
+    me = {"rank": rank, "local_rank": local, "pid": os.getpid()}
+    if world > 1:
+        dist.all_gather_object(seen, me)
+    else:
+        seen = [me]
+    if rank == 0:
+        print(json.dumps({"dry_run": True, "n_gpus": world, "requested": args.gpus, "ranks": seen}))
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    del torch
+
+
 def fp32_peak_probe():
-    """Measured FFMA throughput of this device (TFLOP/s), from libalskit_cuda's probe kernel."""
     from paper_1603_03820_b200 import _native as N
     fn = getattr(N.LIB, "alsk_fp32_peak_probe", None)
-    if fn is None:
-        return None
-    fn.restype = C.c_double
-    fn.argtypes = []
-    return float(fn())
+    return float(fn()) if fn is not None else None
+
+
+def phase(N, k):
+    ms, n = C.c_double(), C.c_uint64()
+    N.LIB.alsk_profile_phase(k, C.byref(ms), C.byref(n))
+    return ms.value, n.value
+
+
+def build_inputs(args, rank, world, dev):
+    """This rank's train CSR slices and test triplets (datagen.build_rank_data), or at one
+    GPU the shared binary cache when the reference arm left one (same bytes)."""
+    import torch
+    import torch.distributed as dist
+    from paper_1603_03820_b200 import datagen as G
+    from paper_1603_03820_b200.session import DeviceCsr
+    m, n, nnz, f, lam = CONFIGS[args.config]
+    mode = "hybrid" if (args.config == "sparkals" and world > 1) else "model"
+    path = cache_path(args)
+    t0 = time.perf_counter()
+    if world == 1 and path.exists():
+        R = DeviceCsr.from_cache(path, dev)
+        x, test = R.split_train_test(0.1, G.split_seed())
+        del R
+        t = x.transpose()
+        src = f"binary cache {path} (the reference arm's input bytes), device split"
+        rd = G.RankData(args.config, m, n, f, lam, 0, 1, mode, (0, m), (0, n), x, t, test, nnz, x.nnz)
+    else:
+        if rank == 0:
+            mask = G.holdout_mask(nnz, 0.1, G.split_seed())
+        else:
+            mask = np.zeros(max(1, (nnz + 31) // 32), np.uint32)
+        if world > 1:
+            tm = torch.from_numpy(mask.view(np.int32))
+            dist.broadcast(tm, src=0)
+        rd = G.build_rank_data(args.config, rank, world, dev, mask, mode=mode)
+        del mask
+        src = "row-seeded device generator per rank (bit-identical to the shared cache) + holdout bitmask " \
+              "from rank 0"
+    torch.cuda.synchronize()
+    return rd, mode, src, time.perf_counter() - t0
 
 
 def run_ours(args):
@@ -204,275 +345,291 @@ def run_ours(args):
     import torch.distributed as dist
     from paper_1603_03820_b200 import _native as N
     from paper_1603_03820_b200 import alskit as A
-    from paper_1603_03820_b200.session import DeviceCsr, PREC_FP32
+    from paper_1603_03820_b200.distributed import HYBRID, MODEL, MultiGpuALS, NativeComm
+    from paper_1603_03820_b200.session import PREC_FP32, PREC_FP64_EXACT
 
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        dist.init_process_group("gloo")  # plumbing (id exchange, barriers, max of timings)
+    comm = NativeComm.from_process_group(local) if world > 1 else None
     m, n, nnz, f, lam = CONFIGS[args.config]
-    train, test = make_data(args.config)
-    nz_train = int(train.row_ptr[-1])
-    R = DeviceCsr.from_host(train, dev)
-    RT = R.transpose()
-    from paper_1603_03820_b200.distributed import ModelParallelALS
-    als = ModelParallelALS(R, RT, m, n, f, lam, PREC_FP32,
-                           torch.from_numpy(A.random_factor(m, f, 42).entries).to(dev),
-                           torch.from_numpy(A.random_factor(n, f, A.mix_seed(42, 1)).entries).to(dev))
-    step = als.step
+    prec = PREC_FP64_EXACT if args.precision == "fp64" else PREC_FP32
+    rd, mode_name, data_src, setup_s = build_inputs(args, rank, world, dev)
+    mode = HYBRID if mode_name == "hybrid" else MODEL
+    theta0 = torch.from_numpy(A.random_factor(n, f, A.mix_seed(RUN_SEED, 1)).entries).to(dev)
+    # X needs no initial value: the first X half overwrites it (train_run, driver.hpp:256)
+    als = MultiGpuALS(comm, mode, m, n, f, lam, prec, rd.x, rd.t, None, theta0)
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
 
     for _ in range(args.warmup):
-        step()
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
+        als.step()
+    als.check()
+    barrier()
     launches0 = A.kernel_launch_count()
-    clocks = Clocks(ROOT / "gpurun_out" / f"clocks_rank{rank}.csv") if (ROOT / "gpurun_out").exists() else Clocks(Path(f"/tmp/clocks_rank{rank}.csv"))
+    clocks = Clocks((ROOT / "gpurun_out" if (ROOT / "gpurun_out").exists() else Path("/tmp")) /
+                    f"clocks_rank{rank}.csv")
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with clocks:
         N.LIB.alsk_profile_begin()
         torch.cuda.synchronize()
-        e0.record()
+        e0.record(stream)
         for _ in range(args.steps):
-            step()
-        e1.record()
+            als.step()
+        e1.record(stream)
         torch.cuda.synchronize()
-        kms, kl = C.c_double(), C.c_uint64()
-        hm, hn, sm_, sn = C.c_double(), C.c_uint64(), C.c_double(), C.c_uint64()
-        N.LIB.alsk_profile_phases(C.byref(hm), C.byref(hn), C.byref(sm_), C.byref(sn))
-        N.LIB.alsk_profile_end(C.byref(kms), C.byref(kl))
-    ms = e0.elapsed_time(e1) / args.steps
+        als.check()
+        herm = phase(N, 0)
+        solve = phase(N, 1)
+        fused = phase(N, 2)
+        coll = phase(N, 3)
+        N.LIB.alsk_profile_end(C.byref(C.c_double()), C.byref(C.c_uint64()))
+    ms_local = e0.elapsed_time(e1) / args.steps
     launches = A.kernel_launch_count() - launches0
+    coll_bytes, coll_calls = als.collective_stats()
+    per_rank = np.array([ms_local, herm[0], solve[0], fused[0], coll[0], rd.x.nnz, rd.t.nnz, launches], np.float64)
     if world > 1:
-        t = torch.tensor([ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
-        dist.barrier()
-    # objective / RMSE after the run (reported, not timed)
+        import torch as _t
+        allr = [_t.zeros(len(per_rank), dtype=_t.float64) for _ in range(world)]
+        dist.all_gather(allr, _t.from_numpy(per_rank))
+        table = np.stack([a.numpy() for a in allr])
+    else:
+        table = per_rank[None, :]
+    ms = float(table[:, 0].max())  # max over ranks
+
+    # test RMSE after the run (reported, not timed): per-rank squared-error sums combined
     rmse = None
-    if rank == 0 and test is not None:
-        out = C.c_double()
-        tt = np.ascontiguousarray(test)
-        rows = torch.from_numpy(tt["row"].copy()).to(dev)
-        cols = torch.from_numpy(tt["col"].copy()).to(dev)
-        vals = torch.from_numpy(tt["value"].copy()).to(dev)
-        X, T = als.factors()
-        A._check(N.LIB.alsk_dev_rmse(rows.data_ptr(), cols.data_ptr(), vals.data_ptr(), len(tt), X.data_ptr(), m,
-                                     T.data_ptr(), n, f, C.byref(out), torch.cuda.current_stream().cuda_stream))
-        rmse = out.value
+    if rd.test.shape[0] > 0 or world > 1:
+        sse, cnt = 0.0, 0
+        if rd.test.shape[0] > 0:
+            tt = rd.test.view(torch.int64)  # rows of TRIPLET_DTYPE: row i64, col i64, value f32 (+pad)
+            rows = tt[:, 0].contiguous()
+            cols = tt[:, 1].contiguous()
+            vals = rd.test[:, 16:20].contiguous().view(torch.float32).reshape(-1)
+            xp, xb, tp = als.pointers()
+            out = C.c_double()
+            if xb:  # hybrid: the X slab starts at global row xb
+                xp -= xb * f * 4
+            A._check(N.LIB.alsk_dev_rmse(rows.data_ptr(), cols.data_ptr(), vals.data_ptr(), rows.numel(), xp,
+                                         rd.xs[1], tp, n, f, C.byref(out), stream.cuda_stream))
+            sse, cnt = out.value ** 2 * rows.numel(), rows.numel()
+        if world > 1:
+            import torch as _t
+            v = _t.tensor([sse, float(cnt)], dtype=_t.float64)
+            dist.all_reduce(v)
+            sse, cnt = float(v[0]), int(v[1])
+        rmse = (sse / cnt) ** 0.5 if cnt else None
 
     result = None
     if rank == 0:
-        flops_half = nz_train * (f * (f + 1) + 2 * f)  # Nz (f(f+1) + 2f) per half-sweep
-        ffma_peak = fp32_peak_probe()
-        nominal_ffma = 148 * 128 * 2 * 1.965e9 / 1e12
+        nz_x, nz_t = float(table[0, 5]), float(table[0, 6])
+        nz_train_total = float(table[:, 5].sum())
         peaks = {}
         try:
             peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
         except (OSError, ValueError):
             pass
-        bf16 = peaks.get("bf16_tflops")
-        tf32_peak = bf16 / 2 if bf16 else 2250.0 / 2 * 1.0  # dense TF32 = half the dense bf16 rate
-        traffic = None
-        tf = ROOT / "profiles" / "traffic.json"
-        if tf.exists():
-            try:
-                traffic = json.loads(tf.read_text()).get(args.config)
-            except (OSError, ValueError):
-                traffic = None
-        if hn.value > 0:
-            # tensor-core engine: Hermitian launches and batched-Cholesky launches timed apart
-            herm_flops = 2 * args.steps * flops_half / world
-            herm_ms_launch = hm.value / hn.value
-            flops_launch = herm_flops / hn.value
-            achieved = flops_launch / (herm_ms_launch * 1e-3) / 1e12
-            solve_flops = args.steps * (m + n) * (f ** 3 / 3 + 2 * f * f) / world
-            pk_row = 4 * (((f * (f + 1) // 2 + f) + 3) // 4 * 4)
-            herm_bytes = args.steps * (2 * nz_train * (4 * f + 8) + 8 * (m + n + 2) + (m + n) * pk_row) / world
-            roof = {"bound": "tensor", "kernel": "tc_update_kernel (tcgen05 tf32x2 Hermitian + bias, packed rows)",
-                    "achieved": achieved, "peak": tf32_peak, "unit": "TFLOP/s", "frac": achieved / tf32_peak,
-                    "peak_source": "MEASURED_PEAKS.json bf16_tflops / 2 (dense TF32)" if bf16 else
-                    "nominal dense TF32 (MEASURED_PEAKS.json absent)",
-                    "traffic": traffic, "flops_per_launch": flops_launch, "kernel_ms_avg": herm_ms_launch,
-                    "launches": int(hn.value), "kernel_share_of_step": (hm.value / args.steps) / ms,
-                    "fp32_ffma_equiv": {"peak": ffma_peak or nominal_ffma, "frac": achieved / (ffma_peak or nominal_ffma),
-                                        "peak_source": "measured FFMA probe (alsk_fp32_peak_probe)"},
-                    # a split-precision tensor-core kernel is also reported
-                    # against the TF32 peak / 3 (three tf32 products per FP32-accurate product)
-                    "tf32x3_equiv": {"peak": tf32_peak / 3, "frac": achieved / (tf32_peak / 3)},
-                    # the same launches against HBM: algorithmic bytes = per rating the column
-                    # index, the value and the gathered factor row (4f), per row the row pointer
-                    # and the packed A/B row written for the solve
-                    "gather": {"bytes_per_launch": herm_bytes / hn.value,
-                               "achieved": herm_bytes / (hm.value * 1e-3) / 1e9, "peak": peaks.get("hbm_gbs"),
-                               "unit": "GB/s",
-                               "frac": (herm_bytes / (hm.value * 1e-3) / 1e9) / peaks["hbm_gbs"]
-                               if peaks.get("hbm_gbs") else None,
-                               "peak_source": "MEASURED_PEAKS.json hbm_gbs"},
-                    "solve": {"kernel": "tc_solve_kernel (TMEM-resident Cholesky, tensor-core rank-8 updates)",
-                              "ms_per_step": sm_.value / args.steps, "launches": int(sn.value),
-                              "achieved_tflops": solve_flops / (sm_.value * 1e-3) / 1e12 if sm_.value else None,
-                              "share_of_step": (sm_.value / args.steps) / ms}}
-        else:
-            # FFMA engine (f outside the tensor-core range): one fused kernel per half
-            kernel_ms = kms.value / max(kl.value, 1)
-            nbk = (f + 1 + 7) // 8
-            kname = (f"small_update_kernel<{f}> (thread or warp per row: hermitian+bias+cholesky+solve in registers)"
-                     if f <= 15 else f"fused_update_kernel<{nbk}> (hermitian+bias+cholesky+solve)")
-            if f <= 32:
-                # small f is HBM-bound; algorithmic gather bytes per half
-                bytes_half = (nz_train * (4 + 4 + 4 * f) + 8 * (max(m, n) + 1)) / world
-                achieved = bytes_half / (kernel_ms * 1e-3) / 1e9
-                hbm = peaks.get("hbm_gbs")
-                roof = {"bound": "hbm", "kernel": kname, "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                        "frac": achieved / hbm if hbm else None, "peak_source": "MEASURED_PEAKS.json hbm_gbs",
-                        "traffic": None, "bytes_per_launch": bytes_half, "kernel_ms_avg": kernel_ms,
-                        "kernel_share_of_step": (kms.value / args.steps) / ms}
-            else:
-                achieved = flops_half / world / (kernel_ms * 1e-3) / 1e12
-                peak = ffma_peak or nominal_ffma
-                roof = {"bound": "fp32-fma", "kernel": kname,
-                        "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
-                        "peak_source": "measured FFMA probe (alsk_fp32_peak_probe)", "traffic": traffic,
-                        "flops_per_launch": flops_half / world, "kernel_ms_avg": kernel_ms,
-                        "kernel_share_of_step": (kms.value / args.steps) / ms}
+        roof = roofline(args, f, m, n, nz_x, nz_t, world, herm, solve, fused, coll, coll_bytes, coll_calls, ms, peaks)
         result = {
             "metric": f"s/ALS-iter ({args.config}-shape f={f})",
             "value": ms / 1e3, "unit": "s/ALS-iter", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms, "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
-            "dtype": "f32", "data": "synthetic (planted rank-10 + U[-0.5,0.5) noise; SURVEY §8(d) generator)",
-            "config": {"workload": args.config, "m": m, "n": n, "nnz_total": nnz, "nnz_train": nz_train, "f": f,
-                       "lambda": lam, "holdout": 0.1, "parallelism": f"model-parallel rows x{world} + NCCL all-gather"
-                       if world > 1 else "single GPU", "l2": f"inputs > L2 (CSR+CSC {2 * (8 * (m + n) / 2 + 8 * nz_train) / 1e9:.1f} GB), no flush",
+            "dtype": "f32" if prec == PREC_FP32 else "f64-accumulate",
+            "data": "synthetic (planted rank-10 + U[-0.5,0.5) noise; SURVEY §8(d) generator)",
+            "config": {"workload": args.config, "m": m, "n": n, "nnz_total": nnz, "nnz_train": int(nz_train_total),
+                       "f": f, "lambda": lam, "holdout": 0.1,
+                       "parallelism": ("single GPU" if world == 1 else
+                                       f"{'hybrid: model-parallel X + data-parallel Theta (NCCL reduce-scatter)' if mode == HYBRID else 'model-parallel rows'}"
+                                       f" x{world} + NCCL all-gather (libalskit_cuda alsk_mp)"),
+                       "precision": args.precision, "input": data_src, "setup_s": round(setup_s, 2),
+                       "l2": "inputs > L2 (train CSR + CSC), no flush",
                        "engine": A.fp32_engine()},
             "roofline": roof,
-            "gpu_launches": int(launches),
+            "gpu_launches": int(table[:, 7].sum()),
             "test_rmse_after_run": rmse,
+            "per_rank_ms": [round(float(v), 3) for v in table[:, 0]],
         }
         cs = clocks.summary(local)
         if cs:
             result["clocks"] = cs
-    if world > 1:
-        dist.barrier()
-    if not args.no_e2e and (world > 1 or args.e2e_dist):
-        e2e = run_e2e_dist(args, train, R, RT, als, rank, world, dev)
+    barrier()
+    if not args.no_e2e and args.config in REF_FULL:
+        e2e = run_e2e(args, rd, als, comm, rank, world, dev, prec)
         if rank == 0:
             result["e2e"] = e2e
-    return result, train, test
+    als.close()
+    return result
 
 
-def run_e2e_dist(args, train, R, RT, als, rank, world, dev):
-    """End to end at N GPUs: every step each rank copies its share of the inputs from pinned
-    host memory (the CSR rows of its X slice, the CSC columns of its Theta slice, and the
-    starting Theta), runs the model-parallel iteration (NCCL all-gathers included) and copies
-    its solved X and Theta slices back. Max over ranks of the wall time per step."""
+def roofline(args, f, m, n, nz_x, nz_t, world, herm, solve, fused, coll, coll_bytes, coll_calls, ms, peaks):
+    """The dominant kernel against its measured peak (SURVEY.md §8(d) units), plus the
+    collectives at N > 1. Figures are rank 0's (its launches, its nonzeros)."""
+    steps = args.steps
+    flops_per_nz = f * (f + 1) + 2 * f  # lower triangle as FMA = 2 flop, + B
+    bf16 = peaks.get("bf16_tflops")
+    hbm = peaks.get("hbm_gbs")
+    ffma = fp32_peak_probe() or 148 * 128 * 2 * 1.965e9 / 1e12
+    herm_ms, herm_n = herm
+    if herm_n > 0 and f > 15:
+        # tensor-core engine: Hermitian (tc_update_kernel) and batched Cholesky timed apart
+        flops = steps * (nz_x + nz_t) * flops_per_nz
+        achieved = flops / (herm_ms * 1e-3) / 1e12
+        tf32 = bf16 / 2 if bf16 else 2250.0 / 2
+        rows = (m + n) / world
+        solve_flops = steps * rows * (f ** 3 / 3 + 2 * f * f)
+        pk_row = 4 * (8 * (((f + 7) // 8) * (f + 1) - 4 * ((f + 7) // 8) * ((f + 7) // 8 - 1)))
+        hbytes = steps * ((nz_x + nz_t) * (4 * f + 8) + 8 * (rows + 2) + rows * pk_row)
+        roof = {"bound": "tensor", "kernel": "tc_update_kernel (tcgen05 tf32x2 Hermitian + bias, packed rows)",
+                "achieved": achieved, "peak": tf32, "unit": "TFLOP/s", "frac": achieved / tf32,
+                "peak_source": "MEASURED_PEAKS.json bf16_tflops / 2 (dense TF32)" if bf16 else "nominal dense TF32",
+                "traffic": traffic_for(args.config, f),
+                "flops_per_launch": flops / herm_n, "kernel_ms_avg": herm_ms / herm_n, "launches": int(herm_n),
+                "kernel_share_of_step": (herm_ms / steps) / ms,
+                "fp32_ffma_equiv": {"peak": ffma, "frac": achieved / ffma,
+                                    "peak_source": "measured FFMA probe (alsk_fp32_peak_probe)"},
+                "tf32x3_equiv": {"peak": tf32 / 3, "frac": achieved / (tf32 / 3)},
+                "gather": {"bytes_per_launch": hbytes / herm_n, "achieved": hbytes / (herm_ms * 1e-3) / 1e9,
+                           "peak": hbm, "unit": "GB/s",
+                           "frac": hbytes / (herm_ms * 1e-3) / 1e9 / hbm if hbm else None},
+                "solve": {"kernel": "tc_solve_kernel (TMEM-resident Cholesky, tensor-core rank-8 updates)",
+                          "ms_per_step": solve[0] / steps, "launches": int(solve[1]),
+                          "achieved_tflops": solve_flops / (solve[0] * 1e-3) / 1e12 if solve[0] else None,
+                          "share_of_step": (solve[0] / steps) / ms}}
+    else:
+        # register/FFMA engines (f <= 15 here): HBM-bound gather, SURVEY.md §8(d)
+        kms, kn = (fused if fused[1] else herm)
+        rows = (m + n) / world
+        bytes_ = steps * ((nz_x + nz_t) * (8 + 4 * f) + 8 * (rows + 2))
+        kname = (f"small_update_kernel<{f}> (thread or warp per row; Hermitian + bias + Cholesky in registers)"
+                 if f <= 15 else "fused_update_kernel (FFMA)")
+        achieved = bytes_ / (kms * 1e-3) / 1e9 if kms else None
+        roof = {"bound": "hbm", "kernel": kname, "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                "frac": achieved / hbm if (hbm and achieved) else None, "peak_source": "MEASURED_PEAKS.json hbm_gbs",
+                "traffic": traffic_for(args.config, f), "bytes_per_launch": bytes_ / max(kn, 1),
+                "kernel_ms_avg": kms / max(kn, 1), "launches": int(kn),
+                "kernel_share_of_step": (kms / steps) / ms if kms else None}
+    if world > 1:
+        nvl = peaks.get("nvlink_gbs") or 900.0
+        gb_s = coll_bytes / (coll[0] * 1e-3) / 1e9 if coll[0] else None
+        roof["collectives"] = {
+            "kind": "ncclAllGather (in place)" + (" + ncclReduceScatter" if args.config == "sparkals" else ""),
+            "bytes_per_rank_per_step": coll_bytes / steps, "calls_per_step": coll_calls / steps,
+            "ms_per_step": coll[0] / steps, "busbw_gbs": gb_s, "peak": nvl,
+            "frac": gb_s / nvl if gb_s else None,
+            "peak_source": "MEASURED_PEAKS.json nvlink_gbs" if peaks.get("nvlink_gbs") else
+            "nominal NVLink 5 per direction (900 GB/s)",
+            "share_of_step": (coll[0] / steps) / ms,
+            "bytes_formula": "(P-1)/P * rows * f * 4 per all-gather (SURVEY §8(d))"}
+    return roof
+
+
+def traffic_for(config, f):
+    tf = ROOT / "profiles" / "traffic.json"
+    try:
+        t = json.loads(tf.read_text())
+        return t.get(config)
+    except (OSError, ValueError):
+        return None
+
+
+def run_e2e(args, rd, als, comm, rank, world, dev, prec):
+    """The same metric end to end. One GPU: the reference-facing host-buffer C ABI
+    (alsk_update_x + alsk_update_theta on pinned host CSR/CSC/factors). N GPUs: every rank
+    copies its CSR slices and the starting Theta from pinned host memory, runs the
+    multi-GPU iteration, and copies its solved X and Theta slices back. Wall clock, max over
+    ranks."""
     import torch
     import torch.distributed as dist
-    from paper_1603_03820_b200 import alskit as A
-    m, n, nnz, f, lam = CONFIGS[args.config]
-    (rb, re), (cb, ce) = als.xs[rank], als.ts[rank]
-    csc = A.csr_to_csc(train)
-    k0, k1 = int(train.row_ptr[rb]), int(train.row_ptr[re])
-    c0, c1 = int(csc.col_ptr[cb]), int(csc.col_ptr[ce])
-    pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()  # noqa: E731
-    ci_h, vv_h = pin(train.col_idx[k0:k1]), pin(train.values[k0:k1])
-    ri_h, cv_h = pin(csc.row_idx[c0:c1]), pin(csc.values[c0:c1])
-    t_h = pin(A.random_factor(n, f, A.mix_seed(42, 1)).entries)
-    x_out = torch.empty((re - rb) * f, dtype=torch.float32).pin_memory()
-    t_out = torch.empty((ce - cb) * f, dtype=torch.float32).pin_memory()
-
-    side = torch.cuda.Stream(device=dev)  # the CSC slice uploads run under the X half-sweep
-
-    def step():
-        main = torch.cuda.current_stream()
-        side.wait_stream(main)
-        with torch.cuda.stream(side):
-            RT.col_idx[c0:c1].copy_(ri_h, non_blocking=True)
-            RT.values[c0:c1].copy_(cv_h, non_blocking=True)
-        R.col_idx[k0:k1].copy_(ci_h, non_blocking=True)
-        R.values[k0:k1].copy_(vv_h, non_blocking=True)
-        als.T[: n * f].copy_(t_h, non_blocking=True)
-        als.half_x()
-        main.wait_stream(side)
-        als.half_theta()
-        x_out.copy_(als.X[rb * f: re * f], non_blocking=True)
-        t_out.copy_(als.T[cb * f: ce * f], non_blocking=True)
-        torch.cuda.synchronize()
-
-    for _ in range(max(1, args.warmup // 2)):
-        step()
-    steps = max(2, args.steps // 2)
-    if world > 1:
-        dist.barrier()
-    t = time.perf_counter()
-    for _ in range(steps):
-        step()
-    sec = torch.tensor([(time.perf_counter() - t) / steps, 0.0, 0.0], dtype=torch.float64, device=dev)
-    sec[1] = (k1 - k0) * 8 + (c1 - c0) * 8 + n * f * 4
-    sec[2] = ((re - rb) + (ce - cb)) * f * 4
-    if world > 1:
-        mx = sec[:1].clone()
-        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
-        dist.all_reduce(sec, op=dist.ReduceOp.SUM)
-        sec[0] = mx[0]
-    return {"value": float(sec[0]), "unit": "s/ALS-iter", "h2d_bytes_per_step": int(sec[1]),
-            "d2h_bytes_per_step": int(sec[2]),
-            "path": f"model-parallel iteration on {world} GPU(s) from pinned host buffers (each rank: its CSR rows, "
-                    "CSC columns and the starting Theta H2D, its X and Theta slices D2H), wall clock, max over ranks",
-            "steps": steps}
-
-
-def run_e2e(args, train, test):
-    """Same metric through the host-buffer C ABI (reference-facing call): pinned host CSR, CSC
-    and factors; every step copies the inputs H2D and the solved factors D2H."""
-    import torch
     from paper_1603_03820_b200 import _native as N
     from paper_1603_03820_b200 import alskit as A
     m, n, nnz, f, lam = CONFIGS[args.config]
-    csc = A.csr_to_csc(train)
-    pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()  # noqa: E731
-    rp, ci, vv = pin(train.row_ptr), pin(train.col_idx), pin(train.values)
-    cp, ri, cv = pin(csc.col_ptr), pin(csc.row_idx), pin(csc.values)
-    X = pin(A.random_factor(m, f, 42).entries)
-    T = pin(A.random_factor(n, f, A.mix_seed(42, 1)).entries)
-    nz = int(train.row_ptr[-1])
-    csr = N.CsrT(m, n, 0, nz, rp.data_ptr(), ci.data_ptr(), vv.data_ptr())
-    cfg = N.SolverConfigT(f, lam, 16, 4096, 0, 0, 42)
+    pin = lambda t: t.cpu().pin_memory()  # noqa: E731
+    theta_h = pin(torch.from_numpy(A.random_factor(n, f, A.mix_seed(RUN_SEED, 1)).entries))
+    if world == 1:
+        x, t = rd.x, rd.t
+        rp, ci, vv = pin(x.row_ptr[: x.rows + 1]), pin(x.col_idx[: x.nnz]), pin(x.values[: x.nnz])
+        cp, ri, cv = pin(t.row_ptr[: t.rows + 1]), pin(t.col_idx[: t.nnz]), pin(t.values[: t.nnz])
+        X = torch.zeros(m * f, dtype=torch.float32).pin_memory()
+        T = theta_h.clone().pin_memory()
+        csr = N.CsrT(m, n, 0, x.nnz, rp.data_ptr(), ci.data_ptr(), vv.data_ptr())
+        cfg = N.SolverConfigT(f, lam, 16, 4096, 1 if args.precision == "fp64" else 0, 0, RUN_SEED)
 
-    def step():
-        A._check(N.LIB.alsk_update_x(C.byref(csr), T.data_ptr(), n, f, C.byref(cfg), X.data_ptr()))
-        A._check(N.LIB.alsk_update_theta(m, n, nz, cp.data_ptr(), ri.data_ptr(), cv.data_ptr(), X.data_ptr(), m, f,
-                                         C.byref(cfg), T.data_ptr()))
+        def step():
+            T.copy_(theta_h)
+            A._check(N.LIB.alsk_update_x(C.byref(csr), T.data_ptr(), n, f, C.byref(cfg), X.data_ptr()))
+            A._check(N.LIB.alsk_update_theta(m, n, x.nnz, cp.data_ptr(), ri.data_ptr(), cv.data_ptr(), X.data_ptr(),
+                                             m, f, C.byref(cfg), T.data_ptr()))
+        h2d = rp.nbytes + ci.nbytes + vv.nbytes + cp.nbytes + ri.nbytes + cv.nbytes + theta_h.nbytes + X.nbytes
+        d2h = X.nbytes + T.nbytes
+        path = "alsk_update_x + alsk_update_theta (host buffers, pinned), wall clock per step"
+    else:
+        x, t = rd.x, rd.t
+        xi, xv = pin(x.col_idx[: x.nnz]), pin(x.values[: x.nnz])
+        ti, tv = pin(t.col_idx[: t.nnz]), pin(t.values[: t.nnz])
+        xp, xb, tp = als.pointers()
+        (rb, re), (cb, ce) = als.xs, als.ts
+        x_out = torch.empty((re - rb) * f, dtype=torch.float32).pin_memory()
+        t_out = torch.empty((ce - cb) * f, dtype=torch.float32).pin_memory()
+        stream = torch.cuda.current_stream()
 
+        def step():
+            x.col_idx[: x.nnz].copy_(xi, non_blocking=True)
+            x.values[: x.nnz].copy_(xv, non_blocking=True)
+            t.col_idx[: t.nnz].copy_(ti, non_blocking=True)
+            t.values[: t.nnz].copy_(tv, non_blocking=True)
+            A._check(N.LIB.alsk_host_to_dev(tp, theta_h.data_ptr(), theta_h.nbytes, stream.cuda_stream))
+            als.step()
+            xoff = 0 if xb else rb * f * 4
+            A._check(N.LIB.alsk_dev_to_host(x_out.data_ptr(), xp + xoff, x_out.nbytes, stream.cuda_stream))
+            A._check(N.LIB.alsk_dev_to_host(t_out.data_ptr(), tp + cb * f * 4, t_out.nbytes, stream.cuda_stream))
+            als.check()
+        h2d = xi.nbytes + xv.nbytes + ti.nbytes + tv.nbytes + theta_h.nbytes
+        d2h = x_out.nbytes + t_out.nbytes
+        path = (f"multi-GPU iteration on {world} GPUs from pinned host buffers (each rank: its CSR slices and the "
+                "starting Theta H2D, its X and Theta slices D2H), wall clock, max over ranks")
     for _ in range(max(1, args.warmup // 2)):
         step()
     steps = max(2, args.steps // 2)
-    t = time.perf_counter()
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
     for _ in range(steps):
         step()
-    sec = (time.perf_counter() - t) / steps
-    h2d = (rp.numel() * 8 + ci.numel() * 4 + vv.numel() * 4 + T.numel() * 4) + \
-          (cp.numel() * 8 + ri.numel() * 4 + cv.numel() * 4 + X.numel() * 4)
-    d2h = X.numel() * 4 + T.numel() * 4
-    return {"value": sec, "unit": "s/ALS-iter", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-            "path": "alsk_update_x + alsk_update_theta (host buffers, pinned), wall clock per step", "steps": steps}
+    torch.cuda.synchronize()
+    sec = (time.perf_counter() - t0) / steps
+    v = torch.tensor([sec, float(h2d), float(d2h)], dtype=torch.float64)
+    if world > 1:
+        mx = v[:1].clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        dist.all_reduce(v)
+        v[0] = mx[0]
+    return {"value": float(v[0]), "unit": "s/ALS-iter", "h2d_bytes_per_step": int(v[1]),
+            "d2h_bytes_per_step": int(v[2]), "path": path, "steps": steps}
 
 
 def main():
     args = parse()
+    rank, world, _ = dist_env()
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        sys.exit(spawn(args))
+    if world != args.gpus and not (args.impl == "reference" and args.cpu_sample):
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    if args.dry_run:
+        dry_run(args)
+        return
     if args.impl == "reference":
         run_reference(args)
         return
-    out = run_ours(args)
-    rank, world, _ = dist_env()
+    result = run_ours(args)
     if rank != 0:
         return
-    result, train, test = out
-    if not args.no_e2e and world == 1 and "e2e" not in result:
-        result["e2e"] = run_e2e(args, train, test)
     if not args.no_cpu and world == 1:
-        result["cpu_baseline"] = cpu_reference_sample(train, test, args.config)
+        result["cpu_baseline"] = cpu_baseline_subprocess(args)
     print(json.dumps(result))
 
 

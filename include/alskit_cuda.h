@@ -113,6 +113,10 @@ void alsk_profile_end(double* total_ms, uint64_t* launches);
 /* Per-phase kernel time of the tensor-core engine since alsk_profile_begin: the
  * tensor-core Hermitian launches and the batched Cholesky launches. */
 void alsk_profile_phases(double* herm_ms, uint64_t* herm_launches, double* solve_ms, uint64_t* solve_launches);
+/* Any phase: 0 Hermitian, 1 batched solve, 2 fused half-sweep kernel, 3 collectives
+ * (all-gather / reduce-scatter of a model-parallel session). Events are resolved here, so
+ * profiling adds no host synchronisation to the timed calls. */
+void alsk_profile_phase(int phase, double* ms, uint64_t* launches);
 /* Measured FP32 FFMA throughput of the current device in TFLOP/s (roofline denominator). */
 double alsk_fp32_peak_probe(void);
 /* TFLOP/s of the Hermitian register-blocked inner loop alone (operands resident in shared
@@ -297,6 +301,7 @@ alsk_status alsk_block_stream_next(void* block_stream, void* stream, int* has_bl
 void alsk_block_stream_close(void* block_stream);
 /* Utility: synchronous device-to-host copy on `stream`. */
 alsk_status alsk_dev_to_host(void* dst, const void* src, size_t bytes, void* stream);
+alsk_status alsk_host_to_dev(void* dst, const void* src, size_t bytes, void* stream);
 
 /* Device loss/rmse; result written to *out (host) after a stream sync. */
 alsk_status alsk_dev_loss(const alsk_csr* r, const int64_t* col_nnz, const float* x,
@@ -382,6 +387,77 @@ alsk_status alsk_dev_split_mask(const alsk_csr* r, const uint32_t* d_mask, int64
  * (rows+1) and *nnz_out only. */
 alsk_status alsk_dev_filter_columns(const alsk_csr* r, int64_t col_begin, int64_t col_end, int64_t* row_ptr_out,
                                     int32_t* col_idx_out, float* values_out, int64_t* nnz_out, void* stream);
+
+/* ---- multi-GPU (replaces su_als_update_x's worker loop, parallel.hpp:487-583,
+ * with one GPU per worker) ------------------------------------------------------------------ */
+/* NCCL communicators. NCCL is loaded at run time; alsk_comm_available() is 0 when it is not
+ * installed (the single-GPU entry points do not need it). One process per GPU: rank 0 makes a
+ * 128-byte id (alsk_comm_unique_id), the caller ships it to every rank, and each rank calls
+ * alsk_comm_init_rank. One process driving several GPUs: alsk_comm_init_all. */
+typedef struct alsk_comm alsk_comm;
+#define ALSK_COMM_ID_BYTES 128
+enum { ALSK_DTYPE_F32 = 0, ALSK_DTYPE_F64 = 1 };
+int alsk_comm_available(void);
+int alsk_nccl_version(void);
+alsk_status alsk_comm_unique_id(uint8_t* id_out /* ALSK_COMM_ID_BYTES */);
+alsk_status alsk_comm_init_rank(const uint8_t* id, int nranks, int rank, int device, alsk_comm** out);
+alsk_status alsk_comm_init_all(int ndev, const int* devices, alsk_comm** comms_out /* ndev */);
+/* A communicator whose collectives go through caller-supplied functions (same semantics as
+ * alsk_comm_allgather / alsk_comm_reduce_scatter, return 0 on success). Used by the tests to
+ * run several ranks' sessions on one GPU over a host transport; NCCL is the product path. */
+typedef struct alsk_comm_ops {
+    int (*allgather)(void* user, void* buf, int64_t chunk_elems, int dtype, void* stream);
+    int (*reduce_scatter)(void* user, const void* in, void* out, int64_t chunk_elems, int dtype, void* stream);
+    void* user;
+} alsk_comm_ops;
+alsk_status alsk_comm_init_custom(int nranks, int rank, const alsk_comm_ops* ops, alsk_comm** out);
+void alsk_comm_destroy(alsk_comm* comm);
+int alsk_comm_rank(const alsk_comm* comm);
+int alsk_comm_size(const alsk_comm* comm);
+/* In-place all-gather: rank r's chunk sits at buf + r*chunk_elems; afterwards buf holds all. */
+alsk_status alsk_comm_allgather(alsk_comm* comm, void* buf, int64_t chunk_elems, int dtype, void* stream);
+/* Sum-reduce-scatter: in holds nranks*chunk_elems, out receives this rank's summed chunk. */
+alsk_status alsk_comm_reduce_scatter(alsk_comm* comm, const void* in, void* out, int64_t chunk_elems, int dtype,
+                                     void* stream);
+alsk_status alsk_comm_allreduce_max(alsk_comm* comm, double* buf, int64_t count, void* stream);
+/* Wait for the stream while polling NCCL's asynchronous error state; on an error or after
+ * timeout_s (> 0) the communicator is aborted and ALSK_ERR_CUDA returned instead of a hang. */
+alsk_status alsk_comm_wait(alsk_comm* comm, void* stream, double timeout_s);
+
+/* Packed-row scratch of the tensor-core half-sweep, owned by the caller (halved on
+ * allocation failure down to 64 MB). Sessions that own one never lock or synchronise. */
+typedef struct alsk_workspace alsk_workspace;
+alsk_status alsk_workspace_create(size_t scratch_bytes, alsk_workspace** out);
+size_t alsk_workspace_bytes(const alsk_workspace* ws);
+void alsk_workspace_destroy(alsk_workspace* ws);
+
+/* One rank's share of a multi-GPU ALS run (a single-GPU run is comm = NULL).
+ *  ALSK_MP_MODEL : x_local = CSR rows [xb, xe) of R (global item ids), t_local = CSR rows
+ *                  [tb, te) of R^T (global user ids); slices are equal-count:
+ *                  xb = rank*ceil(m/P), tb = rank*ceil(n/P). Each half solves the rank's slice
+ *                  and all-gathers the factor in place (bit-identical to one GPU for any P).
+ *  ALSK_MP_HYBRID: x_local as above; t_local = every item's ratings from this rank's users
+ *                  (n rows, user ids local to the slab). The Theta half reduce-scatters
+ *                  per-item partial Hermitians (lambda n_v^local, parallel.hpp:408-411), solves
+ *                  the item slice and all-gathers Theta; X stays in per-rank slabs.
+ * x0 (m*f) / theta0 (n*f) are device pointers (NULL = zeros). ws = NULL allocates a private
+ * workspace. Half-sweeps are asynchronous on `stream`: columns are validated once here and
+ * breakdowns are raised by alsk_mp_check (which also polls NCCL errors). */
+typedef struct alsk_mp alsk_mp;
+enum { ALSK_MP_MODEL = 0, ALSK_MP_HYBRID = 1 };
+alsk_status alsk_mp_create(alsk_comm* comm, int mode, int64_t m, int64_t n, int f, double lambda,
+                           alsk_precision precision, const alsk_csr* x_local, const alsk_csr* t_local,
+                           const float* x0, const float* theta0, alsk_workspace* ws, void* stream, alsk_mp** out);
+alsk_status alsk_mp_half_x(alsk_mp* mp, void* stream);
+alsk_status alsk_mp_half_theta(alsk_mp* mp, void* stream);
+alsk_status alsk_mp_check(alsk_mp* mp, void* stream);
+/* Device factors: X (MODEL: all m rows after the all-gather; HYBRID: the slab starting at
+ * global row *x_row_begin) and Theta (all n rows). Padded rows follow the real ones. */
+alsk_status alsk_mp_factors(alsk_mp* mp, float** x, int64_t* x_row_begin, float** theta);
+void alsk_mp_slices(const alsk_mp* mp, int64_t* x_begin, int64_t* x_end, int64_t* t_begin, int64_t* t_end);
+/* Bytes this rank moved through collectives ((P-1)/P of each buffer) and the call count. */
+void alsk_mp_collective_stats(const alsk_mp* mp, int64_t* bytes, int64_t* calls);
+void alsk_mp_destroy(alsk_mp* mp);
 
 #ifdef __cplusplus
 }

@@ -325,6 +325,44 @@ class Reference(_Lib):
         return st, p.value, q.value, fp.value
 
 
+    # ---- bench.py's reference arm (ref_bench_*: the reference's own train_run iteration) ----
+    def bench_write_cache(self, m, n, nnz, seed, path) -> int:
+        return self.call("bench_write_cache", C.c_int64(m), C.c_int64(n), C.c_int64(nnz), C.c_uint64(seed),
+                         str(path).encode())
+
+    def bench_prepare(self, path, holdout, seed, f, lam):
+        tn, tc = C.c_int64(), C.c_int64()
+        setup = (C.c_double * 4)()
+        st = self.call("bench_prepare", str(path).encode(), C.c_double(holdout), C.c_uint64(seed), f,
+                       C.c_double(lam), C.byref(tn), C.byref(tc), setup)
+        return st, tn.value, tc.value, list(setup)
+
+    def bench_iteration(self):
+        xs, ts = C.c_double(), C.c_double()
+        st = self.call("bench_iteration", C.byref(xs), C.byref(ts))
+        return st, xs.value, ts.value
+
+    def bench_sample(self, kx, kt):
+        xs, ts, nx, nt = C.c_double(), C.c_double(), C.c_int64(), C.c_int64()
+        st = self.call("bench_sample", C.c_int64(kx), C.c_int64(kt), C.byref(xs), C.byref(ts), C.byref(nx),
+                       C.byref(nt))
+        return st, xs.value, ts.value, nx.value, nt.value
+
+    def bench_eval(self):
+        lo, rm, ls, rs = C.c_double(), C.c_double(), C.c_double(), C.c_double()
+        st = self.call("bench_eval", C.byref(lo), C.byref(rm), C.byref(ls), C.byref(rs))
+        return st, lo.value, rm.value, ls.value, rs.value
+
+    def bench_factors(self, m, n, f):
+        x = np.zeros(m * f, np.float32)
+        t = np.zeros(n * f, np.float32)
+        st = self.call("bench_factors", _p(x), _p(t))
+        return st, x, t
+
+    def bench_release(self) -> None:
+        self.call("bench_release", restype=None)
+
+
 def oracle() -> Oracle:
     return Oracle()
 

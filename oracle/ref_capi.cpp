@@ -14,6 +14,7 @@
 
 #include "alskit/alskit.hpp"  // from /root/reference/proj/include, namespace alskit_ref
 #include "../include/alskit_cuda.h"  // our C ABI types only (by path: -I points at the reference)
+#include "../paper_1603_03820_b200/csrc/synth_host.hpp"  // the bench's data generator (CUDA-free, shared)
 
 namespace R = alskit_ref;
 
@@ -320,6 +321,147 @@ alsk_status ref_restore_latest_iteration(const char* dir, int* iteration, int* w
             *which = static_cast<int>(cp->which);
         }
     });
+}
+
+}  // extern "C"
+
+// ---- bench.py's reference arm -------------------------------------------------------------
+// The reference's own train_run iteration (driver.hpp:113-115, 178-181, 256-258), run in a
+// process that never loads libalskit_cuda.so:
+//   load_binary_cache -> split_train_test(R, holdout, mix_seed(seed, 2)) ->
+//   rt = transpose_of(csr_to_csc(train)); x = random_factor(m, f, seed),
+//   theta = random_factor(n, f, mix_seed(seed, 1)); per iteration
+//   x = update_x(train, theta, cfg); theta = update_x(rt, x, cfg)   (threads = 0).
+// The cache is written once by ref_bench_write_cache (the shared synthetic generator,
+// synth_host.hpp, through the reference's own save_binary_cache).
+namespace {
+struct BenchState {
+    R::CsrMatrix train, rt;
+    std::vector<R::Triplet> test;
+    R::FactorMatrix x, theta;
+    R::SolverConfig cfg;
+};
+BenchState* g_bench = nullptr;
+
+double seconds_since(std::chrono::steady_clock::time_point t0) {
+    return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
+
+R::CsrMatrix prefix_rows(const R::CsrMatrix& a, int64_t k) {
+    R::CsrMatrix s;
+    s.rows = k;
+    s.cols = a.cols;
+    s.col_offset = a.col_offset;
+    s.row_ptr.assign(a.row_ptr.begin(), a.row_ptr.begin() + k + 1);
+    const int64_t nz = s.row_ptr.back();
+    s.col_idx.assign(a.col_idx.begin(), a.col_idx.begin() + nz);
+    s.values.assign(a.values.begin(), a.values.begin() + nz);
+    return s;
+}
+}  // namespace
+
+extern "C" {
+
+alsk_status ref_bench_write_cache(int64_t m, int64_t n, int64_t nnz, uint64_t seed, const char* path) {
+    return guarded([&] {
+        R::CsrMatrix a;
+        a.rows = m;
+        a.cols = n;
+        a.row_ptr.resize(static_cast<size_t>(m) + 1);
+        a.col_idx.resize(static_cast<size_t>(nnz));
+        a.values.resize(static_cast<size_t>(nnz));
+        if (alsk_synth::synth_csr(m, n, nnz, seed, 0, a.row_ptr.data(), a.col_idx.data(), a.values.data()) != 0)
+            throw R::InputError("invalid synthetic shape");
+        R::save_binary_cache(a, path);
+    });
+}
+
+// Load + split + transpose + init; seconds of each setup stage into setup_s[0..3].
+alsk_status ref_bench_prepare(const char* cache, double holdout, uint64_t seed, int f, double lambda,
+                              int64_t* train_nnz, int64_t* test_count, double* setup_s) {
+    return guarded([&] {
+        delete g_bench;
+        g_bench = new BenchState();
+        auto t0 = std::chrono::steady_clock::now();
+        const R::CsrMatrix r = R::load_binary_cache(cache);
+        setup_s[0] = seconds_since(t0);
+        t0 = std::chrono::steady_clock::now();
+        R::SplitResult split = R::split_train_test(r, holdout, R::detail::mix_seed(seed, 2));
+        setup_s[1] = seconds_since(t0);
+        t0 = std::chrono::steady_clock::now();
+        g_bench->rt = R::transpose_of(R::csr_to_csc(split.train));
+        setup_s[2] = seconds_since(t0);
+        g_bench->train = std::move(split.train);
+        g_bench->test = std::move(split.test);
+        t0 = std::chrono::steady_clock::now();
+        g_bench->x = R::random_factor(g_bench->train.rows, f, seed);
+        g_bench->theta = R::random_factor(g_bench->train.cols, f, R::detail::mix_seed(seed, 1));
+        setup_s[3] = seconds_since(t0);
+        g_bench->cfg.f = f;
+        g_bench->cfg.lambda = lambda;
+        g_bench->cfg.threads = 0;  // hardware_concurrency (thread_pool.hpp:20-24)
+        *train_nnz = g_bench->train.nnz();
+        *test_count = static_cast<int64_t>(g_bench->test.size());
+    });
+}
+
+// One full ALS iteration exactly as train_run does it (driver.hpp:256-258).
+alsk_status ref_bench_iteration(double* x_half_s, double* theta_half_s) {
+    return guarded([&] {
+        if (!g_bench) throw R::InputError("ref_bench_prepare first");
+        auto t0 = std::chrono::steady_clock::now();
+        g_bench->x = R::update_x(g_bench->train, g_bench->theta, g_bench->cfg);
+        *x_half_s = seconds_since(t0);
+        t0 = std::chrono::steady_clock::now();
+        g_bench->theta = R::update_x(g_bench->rt, g_bench->x, g_bench->cfg);
+        *theta_half_s = seconds_since(t0);
+    });
+}
+
+// A bounded sample: update_x on the first kx rows of train and the first kt rows of rt,
+// timed separately, plus their nonzero counts (for extrapolation by nnz).
+alsk_status ref_bench_sample(int64_t kx, int64_t kt, double* x_s, double* t_s, int64_t* nzx, int64_t* nzt) {
+    return guarded([&] {
+        if (!g_bench) throw R::InputError("ref_bench_prepare first");
+        kx = std::min<int64_t>(kx, g_bench->train.rows);
+        kt = std::min<int64_t>(kt, g_bench->rt.rows);
+        const R::CsrMatrix sx = prefix_rows(g_bench->train, kx), st = prefix_rows(g_bench->rt, kt);
+        *nzx = sx.nnz();
+        *nzt = st.nnz();
+        auto t0 = std::chrono::steady_clock::now();
+        (void)R::update_x(sx, g_bench->theta, g_bench->cfg);
+        *x_s = seconds_since(t0);
+        t0 = std::chrono::steady_clock::now();
+        (void)R::update_x(st, g_bench->x, g_bench->cfg);
+        *t_s = seconds_since(t0);
+    });
+}
+
+// train_J and test RMSE of the current factors (the reference's serial eval, timed apart).
+alsk_status ref_bench_eval(double* loss_out, double* rmse_out, double* loss_s, double* rmse_s) {
+    return guarded([&] {
+        if (!g_bench) throw R::InputError("ref_bench_prepare first");
+        auto t0 = std::chrono::steady_clock::now();
+        *loss_out = R::loss(g_bench->train, g_bench->x, g_bench->theta, g_bench->cfg.lambda);
+        *loss_s = seconds_since(t0);
+        t0 = std::chrono::steady_clock::now();
+        *rmse_out = g_bench->test.empty() ? 0.0 : R::rmse(g_bench->test, g_bench->x, g_bench->theta);
+        *rmse_s = seconds_since(t0);
+    });
+}
+
+// Copies of the current factors (x: rows*f, theta: cols*f).
+alsk_status ref_bench_factors(float* x, float* theta) {
+    return guarded([&] {
+        if (!g_bench) throw R::InputError("ref_bench_prepare first");
+        std::memcpy(x, g_bench->x.entries.data(), sizeof(float) * g_bench->x.entries.size());
+        std::memcpy(theta, g_bench->theta.entries.data(), sizeof(float) * g_bench->theta.entries.size());
+    });
+}
+
+void ref_bench_release(void) {
+    delete g_bench;
+    g_bench = nullptr;
 }
 
 }  // extern "C"

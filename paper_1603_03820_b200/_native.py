@@ -85,6 +85,7 @@ _SIGS = {
     "alsk_block_stream_next": (C.c_int, [vp, vp, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int), CsrP]),
     "alsk_block_stream_close": (None, [vp]),
     "alsk_dev_to_host": (C.c_int, [vp, vp, C.c_size_t, vp]),
+    "alsk_host_to_dev": (C.c_int, [vp, vp, C.c_size_t, vp]),
     "alsk_dev_split_train_test": (C.c_int, [CsrP, C.c_double, C.c_uint64, C.POINTER(i64), vp, vp, vp, vp, vp]),
     "alsk_checkpoint_write": (C.c_int, [C.c_char_p, C.c_int, C.c_int, i64, C.c_int, C.c_uint64, vp]),
     "alsk_checkpoint_path": (C.c_int, [C.c_char_p, C.c_int, C.c_int, C.c_char_p, C.c_size_t]),
@@ -113,7 +114,42 @@ _SIGS = {
     "alsk_mask_count": (i64, [vp, i64, i64]),
     "alsk_dev_split_mask": (C.c_int, [CsrP, vp, i64, i64, vp, vp, vp, vp, i64p, vp]),
     "alsk_dev_filter_columns": (C.c_int, [CsrP, i64, i64, vp, vp, vp, i64p, vp]),
+    "alsk_profile_phase": (None, [C.c_int, f64p, C.POINTER(u64)]),
+    # multi-GPU (multigpu.cu)
+    "alsk_comm_available": (C.c_int, []),
+    "alsk_nccl_version": (C.c_int, []),
+    "alsk_comm_unique_id": (C.c_int, [vp]),
+    "alsk_comm_init_rank": (C.c_int, [vp, C.c_int, C.c_int, C.c_int, C.POINTER(vp)]),
+    "alsk_comm_init_all": (C.c_int, [C.c_int, vp, vp]),
+    "alsk_comm_init_custom": (C.c_int, [C.c_int, C.c_int, vp, C.POINTER(vp)]),
+    "alsk_comm_destroy": (None, [vp]),
+    "alsk_comm_rank": (C.c_int, [vp]),
+    "alsk_comm_size": (C.c_int, [vp]),
+    "alsk_comm_allgather": (C.c_int, [vp, vp, i64, C.c_int, vp]),
+    "alsk_comm_reduce_scatter": (C.c_int, [vp, vp, vp, i64, C.c_int, vp]),
+    "alsk_comm_allreduce_max": (C.c_int, [vp, vp, i64, vp]),
+    "alsk_comm_wait": (C.c_int, [vp, vp, C.c_double]),
+    "alsk_workspace_create": (C.c_int, [C.c_size_t, C.POINTER(vp)]),
+    "alsk_workspace_bytes": (C.c_size_t, [vp]),
+    "alsk_workspace_destroy": (None, [vp]),
+    "alsk_mp_create": (C.c_int, [vp, C.c_int, i64, i64, C.c_int, C.c_double, C.c_int, CsrP, CsrP, vp, vp, vp, vp,
+                                 C.POINTER(vp)]),
+    "alsk_mp_half_x": (C.c_int, [vp, vp]),
+    "alsk_mp_half_theta": (C.c_int, [vp, vp]),
+    "alsk_mp_check": (C.c_int, [vp, vp]),
+    "alsk_mp_factors": (C.c_int, [vp, C.POINTER(vp), C.POINTER(i64), C.POINTER(vp)]),
+    "alsk_mp_slices": (None, [vp, C.POINTER(i64), C.POINTER(i64), C.POINTER(i64), C.POINTER(i64)]),
+    "alsk_mp_collective_stats": (None, [vp, C.POINTER(i64), C.POINTER(i64)]),
+    "alsk_mp_destroy": (None, [vp]),
 }
+
+# transport callbacks of alsk_comm_init_custom (alsk_comm_ops)
+ALLGATHER_FN = C.CFUNCTYPE(C.c_int, vp, vp, i64, C.c_int, vp)
+REDUCE_SCATTER_FN = C.CFUNCTYPE(C.c_int, vp, vp, vp, i64, C.c_int, vp)
+
+
+class CommOpsT(C.Structure):
+    _fields_ = [("allgather", ALLGATHER_FN), ("reduce_scatter", REDUCE_SCATTER_FN), ("user", vp)]
 
 
 def _load() -> C.CDLL:

@@ -8,6 +8,7 @@
 #include <cstdio>
 #include <cstring>
 #include <limits>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -32,41 +33,49 @@ struct Profile {
     bool on = false;
     double ms = 0.0;
     uint64_t launches = 0;
-    double phase_ms[PHASE_COUNT] = {0.0, 0.0};
-    uint64_t phase_n[PHASE_COUNT] = {0, 0};
+    double phase_ms[PHASE_COUNT] = {};
+    uint64_t phase_n[PHASE_COUNT] = {};
 } g_prof;
 
 }  // namespace
 
 // For the host-only entry points (host_data.cpp), which return a status without a guard.
 void set_last_error(const char* msg) { t_error = msg; }
+void set_breakdown_index(int64_t k) { t_breakdown = k; }
 
 bool prof_on() { return g_prof.on; }
 void prof_add(int phase, float ms) {
     g_prof.phase_ms[phase] += ms;
     g_prof.phase_n[phase] += 1;
 }
-
 namespace {
-
-template <class Fn>
-alsk_status guard(Fn&& fn) {
-    t_error.clear();
-    t_breakdown = -1;
-    try {
-        fn();
-        return ALSK_OK;
-    } catch (const Failure& e) {
-        t_error = e.what();
-        return e.status;
-    } catch (const std::bad_alloc&) {
-        t_error = "host allocation failed";
-        return ALSK_ERR_CAPACITY;
-    } catch (const std::exception& e) {
-        t_error = e.what();
-        return ALSK_ERR_CUDA;
+struct Deferred {
+    int phase;
+    cudaEvent_t e0, e1;
+};
+std::mutex g_defer_mu;
+std::vector<Deferred> g_deferred;
+void resolve_deferred() {
+    std::vector<Deferred> d;
+    {
+        std::lock_guard<std::mutex> lk(g_defer_mu);
+        d.swap(g_deferred);
+    }
+    for (auto& e : d) {
+        cudaEventSynchronize(e.e1);
+        float ms = 0.f;
+        if (cudaEventElapsedTime(&ms, e.e0, e.e1) == cudaSuccess) prof_add(e.phase, ms);
+        cudaEventDestroy(e.e0);
+        cudaEventDestroy(e.e1);
     }
 }
+}  // namespace
+void prof_defer(int phase, cudaEvent_t e0, cudaEvent_t e1) {
+    std::lock_guard<std::mutex> lk(g_defer_mu);
+    g_deferred.push_back({phase, e0, e1});
+}
+
+namespace {
 
 // check_update_shapes (solver.hpp:76-81)
 void check_update_shapes(const alsk_csr* r, int64_t theta_rows, int f) {
@@ -178,15 +187,9 @@ void update_rows_device(const DevCsr& r, const float* theta, int64_t theta_rows,
                                       : update_fused_fp32(r, theta, theta_rows, f, static_cast<float>(lambda), rb,
                                                           re, x_out, sb.st, s));
     if (fused) {
-        if (g_prof.on) {
+        if (e0) {
             ALSK_CUDA(cudaEventRecord(e1, s));
-            ALSK_CUDA(cudaEventSynchronize(e1));
-            float ms = 0.f;
-            ALSK_CUDA(cudaEventElapsedTime(&ms, e0, e1));
-            g_prof.ms += ms;
-            g_prof.launches += 1;
-            cudaEventDestroy(e0);
-            cudaEventDestroy(e1);
+            prof_defer(PHASE_FUSED, e0, e1);
         }
         sb.raise_if_broken(s, br, rb);
         return;
@@ -224,6 +227,14 @@ void update_rows_device(const DevCsr& r, const float* theta, int64_t theta_rows,
 cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
 
 }  // namespace
+
+// The synchronous half-sweep (column check, breakdown raised with the reference's text) for
+// the other translation units (multigpu.cu's FP64-exact path).
+void update_rows_sync(const DevCsr& r, const float* theta, int64_t theta_rows, int f, double lambda,
+                      alsk_precision prec, int64_t batch_rows, int64_t rb, int64_t re, float* x_out, cudaStream_t s) {
+    update_rows_device(r, theta, theta_rows, f, lambda, prec, batch_rows, rb, re, x_out, s);
+}
+bool fp32_uses_tensor_cores(alsk_precision prec, int f) { return use_tensor_cores(prec, f); }
 }  // namespace alsk
 
 using namespace alsk;
@@ -239,16 +250,27 @@ int alsk_device_available(void) {
 uint64_t alsk_kernel_launch_count(void) { return g_launches.load(); }
 void alsk_set_fp32_engine(int engine) { g_fp32_engine.store(engine); }
 int alsk_fp32_engine(void) { return g_fp32_engine.load(); }
-void alsk_profile_begin(void) { g_prof = Profile{true, 0.0, 0}; }
+void alsk_profile_begin(void) {
+    resolve_deferred();  // events recorded before this window are not counted in it
+    g_prof = Profile{true, 0.0, 0};
+}
+void alsk_profile_phase(int phase, double* ms, uint64_t* launches) {
+    resolve_deferred();
+    const bool ok = phase >= 0 && phase < PHASE_COUNT;
+    *ms = ok ? g_prof.phase_ms[phase] : 0.0;
+    *launches = ok ? g_prof.phase_n[phase] : 0;
+}
 void alsk_profile_phases(double* herm_ms, uint64_t* herm_launches, double* solve_ms, uint64_t* solve_launches) {
+    resolve_deferred();
     *herm_ms = g_prof.phase_ms[PHASE_HERMITIAN];
     *herm_launches = g_prof.phase_n[PHASE_HERMITIAN];
     *solve_ms = g_prof.phase_ms[PHASE_SOLVE];
     *solve_launches = g_prof.phase_n[PHASE_SOLVE];
 }
 void alsk_profile_end(double* total_ms, uint64_t* launches) {
-    *total_ms = g_prof.ms;
-    *launches = g_prof.launches;
+    resolve_deferred();
+    *total_ms = g_prof.phase_ms[PHASE_FUSED];
+    *launches = g_prof.phase_n[PHASE_FUSED];
     g_prof.on = false;
 }
 const char* alsk_build_info(void) {
@@ -818,16 +840,26 @@ alsk_status alsk_dev_partial_hermitian(const alsk_csr* r, const float* theta, in
     });
 }
 
-int64_t alsk_packed_stride(int f) { return f < 1 ? 0 : packed_stride(f); }
+int64_t alsk_packed_stride(int f) {
+    if (f < 1) return 0;
+    return f <= 15 ? static_cast<int64_t>(f) * (f + 1) / 2 + f : packed_stride(f);
+}
 
 alsk_status alsk_dev_partial_hermitian_f32(const alsk_csr* r, const float* theta, int64_t theta_rows, int f,
                                            double lambda, int64_t row_begin, int64_t row_end, float* out_packed,
                                            void* stream) {
     return guard([&] {
-        if (!tc_supported(f)) fail_input("FP32 partial Hermitians need 16 <= f <= 119 (tensor-core engine)");
+        if (f < 1) fail_input("rank must be >= 1");
+        if (f > 15 && !tc_supported(f))
+            fail_input("FP32 partial Hermitians need f <= 15 (register kernel) or 16 <= f <= 119 (tensor cores)");
         require_device();
         const DevCsr v = dev_view(r);
         check_columns(v, row_begin, row_end, r->col_offset, r->col_offset + theta_rows, as_stream(stream));
+        if (f <= 15) {
+            partial_small_fp32(v, theta, theta_rows, f, static_cast<float>(lambda), row_begin, row_end, out_packed,
+                               as_stream(stream));
+            return;
+        }
         if (!hermitian_packed_tc(v, theta, theta_rows, f, static_cast<float>(lambda), row_begin, row_end, out_packed,
                                  as_stream(stream)))
             fail_input("tensor-core Hermitian unavailable for this rank");
@@ -841,7 +873,10 @@ alsk_status alsk_dev_solve_packed_f32(const float* packed, int64_t count, int f,
         require_device();
         cudaStream_t s = as_stream(stream);
         StatusBufs sb(count, s);
-        packed_solve(packed, count, f, x_out, sb.st, 0, s);
+        if (f <= 15)
+            solve_small_packed(packed, count, f, x_out, sb.st, s);
+        else
+            packed_solve(packed, count, f, x_out, sb.st, 0, s);
         sb.raise_if_broken(s, 0);
     });
 }
@@ -1241,6 +1276,14 @@ alsk_status alsk_dev_to_host(void* dst, const void* src, size_t bytes, void* str
     return guard([&] {
         require_device();
         ALSK_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, as_stream(stream)));
+        ALSK_CUDA(cudaStreamSynchronize(as_stream(stream)));
+    });
+}
+
+alsk_status alsk_host_to_dev(void* dst, const void* src, size_t bytes, void* stream) {
+    return guard([&] {
+        require_device();
+        ALSK_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, as_stream(stream)));
         ALSK_CUDA(cudaStreamSynchronize(as_stream(stream)));
     });
 }

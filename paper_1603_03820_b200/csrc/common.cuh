@@ -6,6 +6,7 @@
 
 #include <atomic>
 #include <cstdint>
+#include <new>
 #include <stdexcept>
 #include <string>
 
@@ -35,12 +36,37 @@ inline void count_launch(uint64_t n = 1) { g_launches.fetch_add(n, std::memory_o
 #define ALSK_LAUNCHED() do { ::alsk::count_launch(); ::alsk::cuda_check(cudaGetLastError(), "kernel launch"); } while (0)
 
 void set_breakdown_index(int64_t k);
+void set_last_error(const char* msg);
+
+// Run fn, converting library exceptions to an alsk_status plus the thread's last-error text
+// (the C boundary of every entry point).
+template <class Fn>
+alsk_status guard(Fn&& fn) {
+    set_last_error("");
+    set_breakdown_index(-1);
+    try {
+        fn();
+        return ALSK_OK;
+    } catch (const Failure& e) {
+        set_last_error(e.what());
+        return e.status;
+    } catch (const std::bad_alloc&) {
+        set_last_error("host allocation failed");
+        return ALSK_ERR_CAPACITY;
+    } catch (const std::exception& e) {
+        set_last_error(e.what());
+        return ALSK_ERR_CUDA;
+    }
+}
 
 // Kernel-phase timing for the bench (alsk_profile_begin / alsk_profile_phases): when on,
 // launches are bracketed by CUDA events on their stream and accumulated per phase.
-enum ProfPhase { PHASE_HERMITIAN = 0, PHASE_SOLVE = 1, PHASE_COUNT = 2 };
+enum ProfPhase { PHASE_HERMITIAN = 0, PHASE_SOLVE = 1, PHASE_FUSED = 2, PHASE_COLLECTIVE = 3, PHASE_COUNT = 4 };
 bool prof_on();
 void prof_add(int phase, float ms);
+// The pair of events is handed to the profile when the timer closes and resolved only when
+// the profile is read (alsk_profile_phases), so timing adds no host synchronisation.
+void prof_defer(int phase, cudaEvent_t e0, cudaEvent_t e1);
 class PhaseTimer {  // no-op unless profiling is on
 public:
     PhaseTimer(int phase, cudaStream_t s) : phase_(phase), s_(s) {
@@ -52,12 +78,7 @@ public:
     ~PhaseTimer() {
         if (!e0_) return;
         cudaEventRecord(e1_, s_);
-        cudaEventSynchronize(e1_);
-        float ms = 0.f;
-        cudaEventElapsedTime(&ms, e0_, e1_);
-        prof_add(phase_, ms);
-        cudaEventDestroy(e0_);
-        cudaEventDestroy(e1_);
+        prof_defer(phase_, e0_, e1_);
     }
 private:
     int phase_;

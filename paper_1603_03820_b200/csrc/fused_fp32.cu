@@ -428,74 +428,18 @@ void strided_theta(StridedTheta& t, const float* theta, int64_t theta_rows, int 
 // B in registers (FP32), adds lambda n_u, and runs the Cholesky and both triangular solves
 // in registers. Same results contract as the fused kernel (FP32 tolerance; all-zero A ->
 // x = 0, solver.hpp:215-220; first non-positive pivot reported, solver.hpp:230-235).
-template <int F, bool WARP>
-__global__ void __launch_bounds__(128)
-small_update_kernel(const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col_idx,
-                    const float* __restrict__ values, int64_t col_lo, const float* __restrict__ theta, int ldt,
-                    float lambda, int64_t rb, int64_t count, float* __restrict__ x,
-                    unsigned long long* __restrict__ min_row, int32_t* __restrict__ column,
-                    double* __restrict__ pivot, int64_t status_base) {
-    const int64_t gt = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    const int64_t t = WARP ? gt >> 5 : gt;
-    const int lane = WARP ? static_cast<int>(threadIdx.x & 31) : 0;
-    if (t >= count) return;  // warp-uniform in the WARP variant
-    const int64_t u = rb + t;
+// Cholesky of the packed lower triangle a (lambda term included) and both triangular solves
+// of b, in registers; x row t written by `writer`. All-zero A -> x = 0 (solver.hpp:215-220);
+// the first non-positive pivot is reported (solver.hpp:230-235).
+template <int F>
+__device__ __forceinline__ void small_chol_solve(float* a, float* b, bool writer, int64_t t, float* __restrict__ x,
+                                                 unsigned long long* __restrict__ min_row,
+                                                 int32_t* __restrict__ column, double* __restrict__ pivot,
+                                                 int64_t status_base) {
     constexpr int NA = F * (F + 1) / 2;
-    constexpr int NQ = (F + 3) / 4;
-    float a[NA], b[F];
-#pragma unroll
-    for (int q = 0; q < NA; ++q) a[q] = 0.f;
-#pragma unroll
-    for (int q = 0; q < F; ++q) b[q] = 0.f;
-    const int64_t k0 = row_ptr[u], k1 = row_ptr[u + 1];
-    for (int64_t k = k0 + lane; k < k1; k += (WARP ? 32 : 1)) {
-        const int v = col_idx[k] - static_cast<int>(col_lo);
-        const float r = values[k];
-        // the caller's rows in place (no padded copy): 16-, 8- or 4-byte loads by F's alignment
-        const float* src = theta + static_cast<int64_t>(v) * ldt;
-        float th[4 * NQ];
-        if constexpr (F % 4 == 0) {
-#pragma unroll
-            for (int q = 0; q < NQ; ++q) {
-                const float4 w = __ldg(reinterpret_cast<const float4*>(src) + q);
-                th[4 * q] = w.x, th[4 * q + 1] = w.y, th[4 * q + 2] = w.z, th[4 * q + 3] = w.w;
-            }
-        } else if constexpr (F % 2 == 0) {
-#pragma unroll
-            for (int q = 0; q < F / 2; ++q) {
-                const float2 w = __ldg(reinterpret_cast<const float2*>(src) + q);
-                th[2 * q] = w.x, th[2 * q + 1] = w.y;
-            }
-        } else {
-#pragma unroll
-            for (int q = 0; q < F; ++q) th[q] = __ldg(src + q);
-        }
-#pragma unroll
-        for (int i = 0; i < F; ++i) {
-            b[i] = fmaf(r, th[i], b[i]);
-#pragma unroll
-            for (int j = 0; j <= i; ++j) a[i * (i + 1) / 2 + j] = fmaf(th[i], th[j], a[i * (i + 1) / 2 + j]);
-        }
-    }
-    if constexpr (WARP) {  // every lane ends with the same sums (fixed butterfly order)
-#pragma unroll
-        for (int q = 0; q < NA; ++q)
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) a[q] += __shfl_xor_sync(0xffffffffu, a[q], o);
-#pragma unroll
-        for (int q = 0; q < F; ++q)
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) b[q] += __shfl_xor_sync(0xffffffffu, b[q], o);
-    }
-    const bool writer = lane == 0;
-    const float reg = lambda * static_cast<float>(k1 - k0);  // float arithmetic as solver.hpp:141,152
     bool nz = false;
 #pragma unroll
-    for (int i = 0; i < F; ++i) {
-        a[i * (i + 1) / 2 + i] += reg;
-#pragma unroll
-        for (int j = 0; j <= i; ++j) nz |= a[i * (i + 1) / 2 + j] != 0.f;
-    }
+    for (int q = 0; q < NA; ++q) nz |= a[q] != 0.f;
     float* xr = x + t * F;
     if (!nz) {
         if (writer) {
@@ -563,7 +507,104 @@ small_update_kernel(const int64_t* __restrict__ row_ptr, const int32_t* __restri
     }
 }
 
-template <bool WARP>
+
+template <int F, bool WARP, bool PARTIAL>
+__global__ void __launch_bounds__(128)
+small_update_kernel(const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col_idx,
+                    const float* __restrict__ values, int64_t col_lo, const float* __restrict__ theta, int ldt,
+                    float lambda, int64_t rb, int64_t count, float* __restrict__ x,
+                    unsigned long long* __restrict__ min_row, int32_t* __restrict__ column,
+                    double* __restrict__ pivot, int64_t status_base) {
+    const int64_t gt = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int64_t t = WARP ? gt >> 5 : gt;
+    const int lane = WARP ? static_cast<int>(threadIdx.x & 31) : 0;
+    if (t >= count) return;  // warp-uniform in the WARP variant
+    const int64_t u = rb + t;
+    constexpr int NA = F * (F + 1) / 2;
+    constexpr int NQ = (F + 3) / 4;
+    float a[NA], b[F];
+#pragma unroll
+    for (int q = 0; q < NA; ++q) a[q] = 0.f;
+#pragma unroll
+    for (int q = 0; q < F; ++q) b[q] = 0.f;
+    const int64_t k0 = row_ptr[u], k1 = row_ptr[u + 1];
+    for (int64_t k = k0 + lane; k < k1; k += (WARP ? 32 : 1)) {
+        const int v = col_idx[k] - static_cast<int>(col_lo);
+        const float r = values[k];
+        // the caller's rows in place (no padded copy): 16-, 8- or 4-byte loads by F's alignment
+        const float* src = theta + static_cast<int64_t>(v) * ldt;
+        float th[4 * NQ];
+        if constexpr (F % 4 == 0) {
+#pragma unroll
+            for (int q = 0; q < NQ; ++q) {
+                const float4 w = __ldg(reinterpret_cast<const float4*>(src) + q);
+                th[4 * q] = w.x, th[4 * q + 1] = w.y, th[4 * q + 2] = w.z, th[4 * q + 3] = w.w;
+            }
+        } else if constexpr (F % 2 == 0) {
+#pragma unroll
+            for (int q = 0; q < F / 2; ++q) {
+                const float2 w = __ldg(reinterpret_cast<const float2*>(src) + q);
+                th[2 * q] = w.x, th[2 * q + 1] = w.y;
+            }
+        } else {
+#pragma unroll
+            for (int q = 0; q < F; ++q) th[q] = __ldg(src + q);
+        }
+#pragma unroll
+        for (int i = 0; i < F; ++i) {
+            b[i] = fmaf(r, th[i], b[i]);
+#pragma unroll
+            for (int j = 0; j <= i; ++j) a[i * (i + 1) / 2 + j] = fmaf(th[i], th[j], a[i * (i + 1) / 2 + j]);
+        }
+    }
+    if constexpr (WARP) {  // every lane ends with the same sums (fixed butterfly order)
+#pragma unroll
+        for (int q = 0; q < NA; ++q)
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) a[q] += __shfl_xor_sync(0xffffffffu, a[q], o);
+#pragma unroll
+        for (int q = 0; q < F; ++q)
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) b[q] += __shfl_xor_sync(0xffffffffu, b[q], o);
+    }
+    const bool writer = lane == 0;
+    const float reg = lambda * static_cast<float>(k1 - k0);  // float arithmetic as solver.hpp:141,152
+#pragma unroll
+    for (int i = 0; i < F; ++i) a[i * (i + 1) / 2 + i] += reg;
+    if constexpr (PARTIAL) {
+        // data-parallel partial (parallel.hpp:408-411): packed [lower(A) row-major | b],
+        // lambda n_u^local on the diagonal, reduced across ranks before the solve
+        if (writer) {
+            float* o = x + t * (NA + F);
+#pragma unroll
+            for (int q = 0; q < NA; ++q) o[q] = a[q];
+#pragma unroll
+            for (int q = 0; q < F; ++q) o[NA + q] = b[q];
+        }
+    } else {
+        small_chol_solve<F>(a, b, writer, t, x, min_row, column, pivot, status_base);
+    }
+}
+
+// Solve of reduced small-rank packed rows ([lower(A) | b], NA + F floats): a thread per row.
+template <int F>
+__global__ void __launch_bounds__(128)
+small_solve_packed_kernel(const float* __restrict__ packed, int64_t count, float* __restrict__ x,
+                          unsigned long long* __restrict__ min_row, int32_t* __restrict__ column,
+                          double* __restrict__ pivot) {
+    constexpr int NA = F * (F + 1) / 2;
+    const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (t >= count) return;
+    float a[NA], b[F];
+    const float* p = packed + t * (NA + F);
+#pragma unroll
+    for (int q = 0; q < NA; ++q) a[q] = p[q];
+#pragma unroll
+    for (int q = 0; q < F; ++q) b[q] = p[NA + q];
+    small_chol_solve<F>(a, b, true, t, x, min_row, column, pivot, 0);
+}
+
+template <bool WARP, bool PARTIAL = false>
 bool launch_small(const DevCsr& r, const float* theta, int f, int ldt, float lambda, int64_t rb, int64_t re,
                   float* x, const SolveStatus& st, cudaStream_t s) {
     const int64_t count = re - rb;
@@ -571,9 +612,9 @@ bool launch_small(const DevCsr& r, const float* theta, int f, int ldt, float lam
     const unsigned grid = static_cast<unsigned>((threads + 127) / 128);
 #define ALSK_SMALL_CASE(FV)                                                                                  \
     case FV:                                                                                                 \
-        small_update_kernel<FV, WARP><<<grid, 128, 0, s>>>(r.row_ptr, r.col_idx, r.values, r.col_offset, theta, \
-                                                           ldt, lambda, rb, count, x, st.min_row, st.column,    \
-                                                           st.pivot, 0);                                        \
+        small_update_kernel<FV, WARP, PARTIAL><<<grid, 128, 0, s>>>(r.row_ptr, r.col_idx, r.values, r.col_offset, \
+                                                                    theta, ldt, lambda, rb, count, x, st.min_row, \
+                                                                    st.column, st.pivot, 0);                      \
         ALSK_LAUNCHED();                                                                                     \
         return true;
     switch (f) {
@@ -646,6 +687,56 @@ bool update_fused_fp32(const DevCsr& r, const float* theta, int64_t theta_rows, 
         if (ok) return true;
     }
     return dispatch<true>(r, theta, theta_rows, f, lambda, rb, re, x_out, nullptr, nullptr, &st, s);
+}
+
+// Data-parallel partial Hermitians for small ranks (f <= 15): packed [lower(A) | b] rows of
+// f(f+1)/2 + f floats with lambda n_u^local on the diagonal (parallel.hpp:408-411).
+bool partial_small_fp32(const DevCsr& r, const float* theta, int64_t theta_rows, int f, float lambda, int64_t rb,
+                        int64_t re, float* out, cudaStream_t s) {
+    if (f < 1 || f > 15) return false;
+    if (re <= rb) return true;
+    const uintptr_t need = f % 4 == 0 ? 15 : (f % 2 == 0 ? 7 : 3);
+    const float* tp = theta;
+    int ldt = f;
+    StridedTheta th;
+    if (reinterpret_cast<uintptr_t>(theta) & need) {
+        strided_theta(th, theta, theta_rows, f, s);
+        tp = th.ptr;
+        ldt = th.ldt;
+    }
+    SolveStatus none{};
+    return r.nnz < 32 * r.rows ? launch_small<false, true>(r, tp, f, ldt, lambda, rb, re, out, none, s)
+                               : launch_small<true, true>(r, tp, f, ldt, lambda, rb, re, out, none, s);
+}
+
+bool solve_small_packed(const float* packed, int64_t count, int f, float* x, const SolveStatus& st, cudaStream_t s) {
+    if (count <= 0) return true;
+    const unsigned grid = static_cast<unsigned>((count + 127) / 128);
+#define ALSK_SMALL_SOLVE(FV)                                                                               \
+    case FV:                                                                                               \
+        small_solve_packed_kernel<FV><<<grid, 128, 0, s>>>(packed, count, x, st.min_row, st.column, st.pivot); \
+        ALSK_LAUNCHED();                                                                                   \
+        return true;
+    switch (f) {
+        ALSK_SMALL_SOLVE(1)
+        ALSK_SMALL_SOLVE(2)
+        ALSK_SMALL_SOLVE(3)
+        ALSK_SMALL_SOLVE(4)
+        ALSK_SMALL_SOLVE(5)
+        ALSK_SMALL_SOLVE(6)
+        ALSK_SMALL_SOLVE(7)
+        ALSK_SMALL_SOLVE(8)
+        ALSK_SMALL_SOLVE(9)
+        ALSK_SMALL_SOLVE(10)
+        ALSK_SMALL_SOLVE(11)
+        ALSK_SMALL_SOLVE(12)
+        ALSK_SMALL_SOLVE(13)
+        ALSK_SMALL_SOLVE(14)
+        ALSK_SMALL_SOLVE(15)
+        default:
+            return false;
+    }
+#undef ALSK_SMALL_SOLVE
 }
 
 bool hermitian_fused_fp32(const DevCsr& r, const float* theta, int64_t theta_rows, int f, float lambda, int64_t rb,

@@ -55,6 +55,9 @@ bool update_fused_fp32(const DevCsr& r, const float* theta, int64_t theta_rows, 
                        int64_t rb, int64_t re, float* x_out, const SolveStatus& st, cudaStream_t s);
 
 // FP32 register-blocked assembly only (materialised output) — the hermitian timed alone.
+bool partial_small_fp32(const DevCsr& r, const float* theta, int64_t theta_rows, int f, float lambda, int64_t rb,
+                        int64_t re, float* out, cudaStream_t s);
+bool solve_small_packed(const float* packed, int64_t count, int f, float* x, const SolveStatus& st, cudaStream_t s);
 bool hermitian_fused_fp32(const DevCsr& r, const float* theta, int64_t theta_rows, int f, float lambda,
                           int64_t rb, int64_t re, float* A, float* B, cudaStream_t s);
 
@@ -62,8 +65,15 @@ bool hermitian_fused_fp32(const DevCsr& r, const float* theta, int64_t theta_row
 // SM (tc_update.cu), followed by the batched TMEM Cholesky (tc_solve.cu).
 // tc_supported: 16 <= f <= 119.
 bool tc_supported(int f);
+// Caller-owned packed-row scratch (a workspace): used stream-ordered, without locking or
+// host synchronisation; nullptr selects the per-device default scratch.
+struct Scratch {
+    float* ptr = nullptr;
+    size_t bytes = 0;
+};
+constexpr int kMaxDevices = 64;
 bool update_tc(const DevCsr& r, const float* theta, int64_t theta_rows, int f, float lambda, int64_t rb,
-               int64_t re, float* x_out, const SolveStatus& st, cudaStream_t s);
+               int64_t re, float* x_out, const SolveStatus& st, cudaStream_t s, const Scratch* scratch = nullptr);
 // Packed (panel-blocked) rows [rb, re) of A_u + lambda n_u I and B_u on the tensor cores into
 // out_packed (packed_stride(f) floats per row): the data-parallel split's FP32 partials.
 bool hermitian_packed_tc(const DevCsr& r, const float* theta, int64_t theta_rows, int f, float lambda, int64_t rb,
@@ -96,12 +106,6 @@ bool packed_solve16(const float* packed, int64_t count, int f, float* x, const S
                     int64_t status_off, cudaStream_t s);
 bool packed_solve_tiles(const float* packed, int64_t count, int f, float* x, const SolveStatus& st,
                         int64_t status_off, cudaStream_t s);
-
-// Packed-lower double partial Hermitian (data-parallel split) and its solve.
-void partial_hermitian_packed(const DevCsr& r, const float* theta, int f, double lambda,
-                              int64_t rb, int64_t re, double* out, cudaStream_t s);
-void solve_packed(const double* packed, int64_t count, int f, float* X, const SolveStatus& st,
-                  cudaStream_t s);
 
 // Evaluation (solver.hpp:358-406). Deterministic two-level double reductions.
 double loss_device(const DevCsr& r, const int64_t* col_nnz, const float* x, const float* theta,

@@ -685,45 +685,65 @@ void strided(Strided& t, const float* theta, int64_t rows, int f, cudaStream_t s
 // batches (MODE_PACKED into a device scratch) each followed by the batched packed solve.
 template <int MODE>
 bool dispatch_tc(const DevCsr& r, const float* theta, int64_t theta_rows, int f, float lambda, int64_t rb, int64_t re,
-                 float* x, float* a, float* b, const SolveStatus* st, cudaStream_t s) {
+                 float* x, float* a, float* b, const SolveStatus* st, cudaStream_t s, const Scratch* ext = nullptr) {
     if (!tc_supported(f)) return false;
     if (re <= rb) return true;
     Strided th;
     strided(th, theta, theta_rows, f, s);
     const int nb = (f + 1 + 7) / 8;
     const int64_t pkn = packed_stride(f);
-    // packed rows per batch: the scratch size (ALSK_TC_SCRATCH_MB, default 11264 MB: a
-    // Netflix-shape X half in one batch, 0.5% faster per iteration than 4096 MB in three;
-    // allocated only up to what the half needs) over the row size
+    // Packed-row scratch. A caller-owned workspace (sessions, alsk_workspace_*) is used as
+    // is: stream-ordered, no lock, no host synchronisation. Otherwise the per-device default
+    // scratch (ALSK_TC_SCRATCH_MB, default 4096 MB, grown on demand up to what the half
+    // needs and halved on allocation failure) is shared by all callers of that device; they
+    // are serialised on it until the stream has drained the batches that use it.
     static const int64_t scratch_mb = [] {
         const char* e = std::getenv("ALSK_TC_SCRATCH_MB");
-        return e ? std::max<int64_t>(64, std::atoll(e)) : int64_t(11264);
+        return e ? std::max<int64_t>(64, std::atoll(e)) : int64_t(4096);
     }();
-    const int64_t batch = std::min<int64_t>(re - rb, std::max<int64_t>(1, (scratch_mb << 20) / (pkn * 4)));
-    // packed-row scratch kept for the process (grow-only, never freed): a per-call ~1 GB
-    // allocation would otherwise sit on every host-API half-sweep. Callers are serialised on
-    // it: the lock is held until the stream has drained the batches that use it.
-    static float* scratch_ptr = nullptr;
-    static size_t scratch_bytes = 0;
-    static std::mutex scratch_mu;
-    std::unique_lock<std::mutex> lock(scratch_mu, std::defer_lock);
+    struct DefaultScratch {
+        float* ptr = nullptr;
+        size_t bytes = 0;
+        std::mutex mu;
+    };
+    static DefaultScratch defaults[kMaxDevices];
+    std::unique_lock<std::mutex> lock;
+    float* scratch_p = nullptr;
+    int64_t batch = re - rb;
+    if (MODE == MODE_PACKED) {
+        if (ext) {
+            scratch_p = ext->ptr;
+            batch = std::min<int64_t>(re - rb, std::max<int64_t>(1, static_cast<int64_t>(ext->bytes / (pkn * 4))));
+        } else {
+            int dev = 0;
+            ALSK_CUDA(cudaGetDevice(&dev));
+            DefaultScratch& d = defaults[dev % kMaxDevices];
+            lock = std::unique_lock<std::mutex>(d.mu);
+            int64_t want = std::min<int64_t>(re - rb, std::max<int64_t>(1, (scratch_mb << 20) / (pkn * 4)));
+            if (d.bytes < sizeof(float) * want * pkn) {
+                ALSK_CUDA(cudaStreamSynchronize(s));
+                if (d.ptr) cudaFree(d.ptr);
+                d.ptr = nullptr;
+                d.bytes = 0;
+                for (;;) {
+                    const size_t need = sizeof(float) * want * pkn;
+                    if (cudaMalloc(&d.ptr, need) == cudaSuccess) {
+                        d.bytes = need;
+                        break;
+                    }
+                    (void)cudaGetLastError();
+                    if (want == 1) ALSK_CUDA(cudaErrorMemoryAllocation);
+                    want = std::max<int64_t>(1, want / 2);  // retry with a smaller batch
+                }
+            }
+            scratch_p = d.ptr;
+            batch = std::min<int64_t>(re - rb, std::max<int64_t>(1, static_cast<int64_t>(d.bytes / (pkn * 4))));
+        }
+    }
     struct {
         float* p;
         float* as() const { return p; }
-    } scratch{nullptr};
-    if (MODE == MODE_PACKED) {
-        lock.lock();
-        const size_t need = sizeof(float) * batch * pkn;
-        if (scratch_bytes < need) {
-            ALSK_CUDA(cudaStreamSynchronize(s));
-            if (scratch_ptr) cudaFree(scratch_ptr);
-            scratch_ptr = nullptr;
-            scratch_bytes = 0;
-            ALSK_CUDA(cudaMalloc(&scratch_ptr, need));
-            scratch_bytes = need;
-        }
-        scratch.p = scratch_ptr;
-    }
+    } scratch{scratch_p};
 #define ALSK_TC_CASE(NBV)                                                                              \
     if (nb <= NBV) {                                                                                   \
         if (MODE == MODE_FULL) {                                                                       \
@@ -740,7 +760,7 @@ bool dispatch_tc(const DevCsr& r, const float* theta, int64_t theta_rows, int f,
                 PhaseTimer pt(PHASE_SOLVE, s);                                                         \
                 packed_solve(scratch.as(), b1 - b0, f, x + (b0 - rb) * f, *st, b0 - rb, s);      \
             }                                                                                          \
-            ALSK_CUDA(cudaStreamSynchronize(s)); /* the shared scratch is free again */              \
+            if (!ext) ALSK_CUDA(cudaStreamSynchronize(s)); /* the shared scratch is free again */    \
         }                                                                                              \
         return true;                                                                                   \
     }
@@ -759,8 +779,8 @@ bool dispatch_tc(const DevCsr& r, const float* theta, int64_t theta_rows, int f,
 bool tc_supported(int f) { return f >= 16 && f <= 119; }  // 2*round16(f+1) <= 256, tiles <= 128
 
 bool update_tc(const DevCsr& r, const float* theta, int64_t theta_rows, int f, float lambda, int64_t rb, int64_t re,
-               float* x_out, const SolveStatus& st, cudaStream_t s) {
-    return dispatch_tc<MODE_PACKED>(r, theta, theta_rows, f, lambda, rb, re, x_out, nullptr, nullptr, &st, s);
+               float* x_out, const SolveStatus& st, cudaStream_t s, const Scratch* scratch) {
+    return dispatch_tc<MODE_PACKED>(r, theta, theta_rows, f, lambda, rb, re, x_out, nullptr, nullptr, &st, s, scratch);
 }
 
 bool hermitian_packed_tc(const DevCsr& r, const float* theta, int64_t theta_rows, int f, float lambda, int64_t rb,

@@ -18,6 +18,6 @@ if [[ $STEP == all || $STEP == ncu ]]; then
      --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu > gpurun_out/ncu_bench.log 2>&1
   echo "ncu launches exit $?" >> gpurun_out/status.txt
   timeout 900 /usr/local/cuda/bin/ncu --set full --clock-control none --import-source on -k regex:"tc_update|tc_solve" -c 2 \
-     -o gpurun_out/prof_tc python scripts/prof_step.py 2 1 > gpurun_out/ncu_full.log 2>&1
+     -o gpurun_out/prof_tc python scripts/prof_step.py netflix 1 > gpurun_out/ncu_full.log 2>&1
   echo "ncu full exit $?" >> gpurun_out/status.txt
 fi

@@ -1,21 +1,29 @@
-"""One Netflix-shape ALS iteration (X-half then Theta-half) through alsk_dev_update with the
-chosen precision, for ncu captures: python scripts/prof_step.py [precision] [iters]."""
+"""The benched iteration for ncu captures: bench.py's single-GPU path (the C++ session
+alsk_mp with its own packed-row workspace, the same data builder), without bench.py's
+extra legs. usage: python scripts/prof_step.py [config=netflix] [iters=1] [precision=fp32]"""
 import sys
-sys.path.insert(0, '.')
-import torch
-import bench
-from paper_1603_03820_b200 import alskit as A
-from paper_1603_03820_b200.session import DeviceCsr, dev_update
-prec = int(sys.argv[1]) if len(sys.argv) > 1 else 2
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+import torch  # noqa: E402
+
+import bench  # noqa: E402
+from paper_1603_03820_b200 import alskit as A  # noqa: E402
+from paper_1603_03820_b200 import datagen as G  # noqa: E402
+from paper_1603_03820_b200.distributed import MODEL, MultiGpuALS  # noqa: E402
+from paper_1603_03820_b200.session import PREC_FP32, PREC_FP64_EXACT  # noqa: E402
+
+cfg = sys.argv[1] if len(sys.argv) > 1 else "netflix"
 iters = int(sys.argv[2]) if len(sys.argv) > 2 else 1
-train, test = bench.make_data('netflix')
-dev = torch.device('cuda')
-R = DeviceCsr.from_host(train, dev); RT = R.transpose()
-m, n, f = 480189, 17770, 100
-X = torch.from_numpy(A.random_factor(m, f, 42).entries).to(dev)
-T = torch.from_numpy(A.random_factor(n, f, A.mix_seed(42, 1)).entries).to(dev)
-for it in range(iters):
-    dev_update(R, T, n, f, 0.05, prec, X)
-    dev_update(RT, X, m, f, 0.05, prec, T)
+prec = PREC_FP64_EXACT if (len(sys.argv) > 3 and sys.argv[3] == "fp64") else PREC_FP32
+m, n, nnz, f, lam = bench.CONFIGS[cfg]
+dev = torch.device("cuda", 0)
+mask = G.holdout_mask(nnz, 0.1, G.split_seed())
+rd = G.build_rank_data(cfg, 0, 1, dev, mask)
+theta0 = torch.from_numpy(A.random_factor(n, f, A.mix_seed(42, 1)).entries).to(dev)
+als = MultiGpuALS(None, MODEL, m, n, f, lam, prec, rd.x, rd.t, None, theta0)
+for _ in range(iters):
+    als.step()
+als.check()
 torch.cuda.synchronize()
 print("done")

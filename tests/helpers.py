@@ -38,3 +38,14 @@ def instance(orc, seed, m, n, nnz, f):
 def csr(m, n, arrs, col_offset=0):
     rp, ci, vv = arrs
     return binding.csr_struct(m, n, rp, ci, vv, col_offset)
+
+
+def synth_split(cfg: str):
+    """The bench's input on the host: the shared synthetic generator's matrix for a named
+    shape (bench.CONFIGS) and the reference driver's split (driver.hpp:113)."""
+    import bench
+    from paper_1603_03820_b200 import alskit as A
+    m, n, nnz, f, lam = bench.CONFIGS[cfg]
+    R = A.synth_csr(m, n, nnz, bench.data_seed(cfg))
+    sp = A.split_train_test(R, 0.1, A.mix_seed(42, 2))
+    return sp.train, sp.test

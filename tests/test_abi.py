@@ -62,10 +62,12 @@ def test_synthetic_generator_shape_and_determinism(A):
 
 
 def test_packed_stride_matches_the_python_layout():
-    """alsk_packed_stride (C ABI, no device needed) and distributed.packed_stride agree: the
-    panel-blocked packed row of kernels.cuh, one 8-float row segment per (block, row)."""
+    """alsk_packed_stride (C ABI, no device needed) and distributed.packed_stride agree: for
+    f <= 15 the compact [lower(A) | b] row of the register kernels, otherwise the panel-blocked
+    packed row of kernels.cuh, one 8-float row segment per (block, row)."""
     from paper_1603_03820_b200 import _native as N
     from paper_1603_03820_b200.distributed import packed_stride
     for f in range(1, 131):
         nb = (f + 7) // 8
-        assert N.LIB.alsk_packed_stride(f) == packed_stride(f) == sum(8 * (f + 1 - 8 * b) for b in range(nb))
+        want = f * (f + 1) // 2 + f if f <= 15 else sum(8 * (f + 1 - 8 * b) for b in range(nb))
+        assert N.LIB.alsk_packed_stride(f) == packed_stride(f) == want

@@ -1,5 +1,6 @@
-"""Multi-GPU host logic on CPU: world_size-2 gloo runs of paper_1603_03820_b200.distributed with
-the compute steps replaced by CPU stand-ins (the oracle for update_x, numpy for the packed
+"""Multi-GPU host logic on CPU: world_size-2 gloo runs of the partitioning model
+(tests/mp_model.py, the Python restatement of libalskit_cuda's alsk_mp slicing and
+collectives) with the compute steps replaced by CPU stand-ins (the oracle for update_x, numpy for the packed
 partial Hermitians). Checks the partitioning, padding, all-gather and reduce-scatter
 plumbing: model-parallel halves are bit-identical to one process; the data-parallel
 Theta-half matches the single-process update within 1e-6 normwise (double reassociation,
@@ -47,7 +48,7 @@ def _problem():
 
 def _cpu_compute():
     from oracle import binding
-    from paper_1603_03820_b200.distributed import Compute
+    from mp_model import Compute
     orc = binding.oracle()
 
     def update_rows(R, theta, theta_rows, f, lam, precision, rb, re, out):
@@ -94,7 +95,7 @@ def _cpu_compute():
             xs = X[R.ci[k0:k1]]
             a = xs.T @ xs + lam * (k1 - k0) * np.eye(f)
             b = xs.T @ R.vv[k0:k1].astype(np.float64)
-            out[(v - rb) * per:(v - rb + 1) * per] = torch.from_numpy(pack_panel_blocked(a, b, f))
+            out[(v - rb) * per:(v - rb + 1) * per] = torch.from_numpy(pack_row(a, b, f))
 
     def solve_packed_f32(packed, count, f, out):
         from paper_1603_03820_b200.distributed import packed_stride
@@ -103,12 +104,32 @@ def _cpu_compute():
         A = np.zeros((count, f, f), np.float32)
         B = np.zeros((count, f), np.float32)
         for v in range(count):
-            A[v], B[v] = unpack_panel_blocked(p[v], f)
+            A[v], B[v] = unpack_row(p[v], f)
         st, x = orc.batch_solve(np.ascontiguousarray(A.reshape(-1)), np.ascontiguousarray(B.reshape(-1)), count, f)
         assert st == 0
         out[: count * f].copy_(torch.from_numpy(x))
 
     return Compute(update_rows, partial_hermitian, solve_packed, partial_hermitian_f32, solve_packed_f32)
+
+
+def pack_row(a, b, f):
+    """The FP32 packed partial row (distributed.packed_stride): compact [lower(A) | b] for
+    f <= 15, panel-blocked otherwise."""
+    if f <= 15:
+        il = np.tril_indices(f)
+        return np.concatenate([a[il[0], il[1]], b]).astype(np.float32)
+    return pack_panel_blocked(a, b, f)
+
+
+def unpack_row(row, f):
+    if f <= 15:
+        na = f * (f + 1) // 2
+        il = np.tril_indices(f)
+        a = np.zeros((f, f), np.float32)
+        a[il[0], il[1]] = row[:na]
+        a[il[1], il[0]] = row[:na]
+        return a, np.asarray(row[na:na + f], np.float32)
+    return unpack_panel_blocked(row, f)
 
 
 def pack_panel_blocked(a, b, f):
@@ -148,7 +169,8 @@ def _worker(rank, world, port, q):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        from paper_1603_03820_b200.distributed import DataParallelThetaHalf, ModelParallelALS, even_slices
+        from mp_model import DataParallelThetaHalf, ModelParallelALS
+        from paper_1603_03820_b200.distributed import even_slices
         orc, m, n, f, lam, R, RT, x0, t0 = _problem()
         comp = _cpu_compute()
         mp_als = ModelParallelALS(R, RT, m, n, f, lam, 0, torch.from_numpy(x0), torch.from_numpy(t0), compute=comp)
@@ -212,13 +234,13 @@ def test_model_and_data_parallel_gloo_world2():
 def test_panel_blocked_pack_round_trip():
     from paper_1603_03820_b200.distributed import packed_stride
     rng = np.random.default_rng(3)
-    for f in (1, 5, 8, 9, 16, 100):
+    for f in (1, 5, 8, 9, 15, 16, 17, 100):
         m = rng.standard_normal((f, f))
         a = (m @ m.T).astype(np.float32)
         b = rng.standard_normal(f).astype(np.float32)
-        row = pack_panel_blocked(a, b, f)
+        row = pack_row(a, b, f)
         assert row.size == packed_stride(f)
-        a2, b2 = unpack_panel_blocked(row, f)
+        a2, b2 = unpack_row(row, f)
         il = np.tril_indices(f)
         assert np.array_equal(a2[il], a[il]) and np.array_equal(b2, b)
 

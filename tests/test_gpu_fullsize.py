@@ -27,8 +27,8 @@ pytestmark = pytest.mark.gpu
 
 @pytest.fixture(scope="module")
 def netflix_split(A, gpu):
-    import bench
-    return bench.make_data("netflix")
+    from helpers import synth_split
+    return synth_split("netflix")
 
 
 @pytest.fixture(scope="module")
@@ -102,8 +102,10 @@ def _rmse(N, test, X, T, m, n, f, dev):
     cols = torch.from_numpy(tt["col"].copy()).to(dev)
     vals = torch.from_numpy(tt["value"].copy()).to(dev)
     out = C.c_double()
-    st = N.LIB.alsk_dev_rmse(rows.data_ptr(), cols.data_ptr(), vals.data_ptr(), len(tt), X.data_ptr(), m,
-                             T.data_ptr(), n, f, C.byref(out), torch.cuda.current_stream().cuda_stream)
+    xp = X if isinstance(X, int) else X.data_ptr()
+    tp = T if isinstance(T, int) else T.data_ptr()
+    st = N.LIB.alsk_dev_rmse(rows.data_ptr(), cols.data_ptr(), vals.data_ptr(), len(tt), xp, m,
+                             tp, n, f, C.byref(out), torch.cuda.current_stream().cuda_stream)
     assert st == 0
     return out.value
 
@@ -113,7 +115,7 @@ def test_fullsize_ten_iterations_rmse_parity(A, netflix, netflix_split):
     initial factors, the tensor-core engine's test RMSE is within 1e-4 of the reference-order
     FP64 mode's (driver.hpp:255-262 iteration order)."""
     from paper_1603_03820_b200 import _native as N
-    from paper_1603_03820_b200.distributed import ModelParallelALS
+    from paper_1603_03820_b200.distributed import MODEL, MultiGpuALS
     from paper_1603_03820_b200.session import PREC_FP32, PREC_FP64_EXACT
     train, R, dev = netflix
     _, test = netflix_split
@@ -124,9 +126,11 @@ def test_fullsize_ten_iterations_rmse_parity(A, netflix, netflix_split):
     out = {}
     for name, prec in (("tc", PREC_FP32), ("fp64", PREC_FP64_EXACT)):
         with A.use_fp32_engine("tensor"):
-            als = ModelParallelALS(R, RT, m, n, f, lam, prec, x0, t0)
+            als = MultiGpuALS(None, MODEL, m, n, f, lam, prec, R, RT, x0, t0)
             for _ in range(10):
                 als.step()
-            X, T = als.factors()
+            als.check()
+            X, _, T = als.pointers()
             out[name] = _rmse(N, test, X, T, m, n, f, dev)
+            als.close()
     assert abs(out["tc"] - out["fp64"]) <= 1e-4, out

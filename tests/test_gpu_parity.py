@@ -395,33 +395,31 @@ def test_als_train_ml1m_shape_rmse_parity(A, orc, gpu):
 
 # ------------------------------------------------------------------ multi-GPU paths, 1 device
 def test_distributed_paths_single_device(A, orc, gpu):
-    """ModelParallelALS and DataParallelThetaHalf with the CUDA compute at world size 1:
-    the model-parallel step equals update_x/update_theta; the data-parallel Theta-half
-    (double partials -> round once -> reference-order solve) is bit-identical to the FP64
-    update_x of R^T."""
+    """The C++ multi-GPU session (alsk_mp) at world size 1 on the full device CSRs: the
+    MODEL iteration equals update_x/update_theta bit for bit (FP64 exact); the HYBRID session's
+    data-parallel Theta half (double partials -> round once -> reference-order solve) is
+    bit-identical too, and its FP32 variant (tensor-core panel-blocked partials + TMEM
+    Cholesky) lands within the FP32 bar."""
     import torch
-    from paper_1603_03820_b200.distributed import DataParallelThetaHalf, ModelParallelALS
-    from paper_1603_03820_b200.session import DeviceCsr, PREC_FP64_EXACT
+    from paper_1603_03820_b200.distributed import HYBRID, MODEL, MultiGpuALS
+    from paper_1603_03820_b200.session import DeviceCsr, PREC_FP32, PREC_FP64_EXACT
     r, th = rand_csr(A, orc, 777, 300, 120, 6000, 16)
     dev = torch.device("cuda")
     R = DeviceCsr.from_host(r, dev)
     RT = R.transpose()
-    x0 = A.random_factor(300, 16, 42)
-    als = ModelParallelALS(R, RT, 300, 120, 16, 0.05, PREC_FP64_EXACT, torch.from_numpy(x0.entries).to(dev),
-                           torch.from_numpy(th.entries).to(dev))
-    als.step()
-    X, T = als.factors()
     cfg = A.SolverConfig(f=16, lambda_=0.05)
     x1 = A.update_x(r, th, cfg)
     t1 = A.update_theta(A.csr_to_csc(r), x1, cfg)
-    assert np.array_equal(X.cpu().numpy(), x1.entries) and np.array_equal(T.cpu().numpy(), t1.entries)
-    dp = DataParallelThetaHalf(RT, 300, 120, 16, 0.05)
-    T2 = torch.zeros(120 * 16, dtype=torch.float32, device=dev)
-    dp.half_theta(X, T2)
-    assert np.array_equal(T2.cpu().numpy(), t1.entries)
-    # FP32 variant: tensor-core panel-blocked partials + TMEM Cholesky, within the FP32 bar
-    dp32 = DataParallelThetaHalf(RT, 300, 120, 16, 0.05, fp32=True)
-    T3 = torch.zeros(120 * 16, dtype=torch.float32, device=dev)
-    dp32.half_theta(X, T3)
-    gap = normwise_gap(T3.cpu().numpy(), t1.entries)
+    t0 = torch.from_numpy(th.entries).to(dev)
+    for mode in (MODEL, HYBRID):
+        als = MultiGpuALS(None, mode, 300, 120, 16, 0.05, PREC_FP64_EXACT, R, RT, None, t0)
+        als.step()
+        X, T = als.factors_host()
+        als.close()
+        assert np.array_equal(X, x1.entries) and np.array_equal(T, t1.entries), mode
+    als = MultiGpuALS(None, HYBRID, 300, 120, 16, 0.05, PREC_FP32, R, RT, None, t0)
+    als.step()
+    X, T = als.factors_host()
+    als.close()
+    gap = max(normwise_gap(X, x1.entries), normwise_gap(T, t1.entries))
     assert gap <= FP32_TOL and gap <= 5e-5, gap
