@@ -9,7 +9,9 @@
 //  * grid_partition (sparse.hpp:250-314): per-row binary search of the column cuts.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 #include <string>
 #include <vector>
 
@@ -227,6 +229,217 @@ int bits_for(int64_t count) {  // bits to represent values in [0, count)
     return b;
 }
 
+
+// ------------------------------------------------- single-pass counting-sort transpose ---
+// csr_to_csc as the reference does it (a stable counting sort, sparse.hpp:185-207), spread
+// over C chunks of consecutive nonzeros (one CTA each, one wave):
+//  tr_tile_rows  row of the first nonzero of every 2048-nonzero tile (binary search);
+//  tr_count      per-chunk column histogram in shared memory -> H[chunk][col];
+//  tr_colscan    per column, exclusive prefix of H over the chunks (in place) and the
+//                column totals -> col_ptr;
+//  tr_scatter    each chunk's running offsets off[c] = col_ptr[c] + H[chunk][c] live in
+//                shared memory; a staged tile is stably partitioned by owner warp
+//                (c mod 16), and each warp ranks its own columns in order (__match_any_sync,
+//                one read-modify-write of off[c] per distinct column), so entries of a
+//                column are placed in nonzero order, i.e. by ascending row — exactly the
+//                reference's output. Algorithmic traffic: col_idx read twice, values once,
+//                row_idx + values written once (~20 B per nonzero).
+constexpr int kTrThreads = 512;
+constexpr int kTrWarps = kTrThreads / 32;  // owners: column mod 16
+constexpr int kTrSub = 4;                  // staged elements per thread per tile
+constexpr int kTrTile = kTrThreads * kTrSub;
+constexpr int kTrSpan = 1024;              // row_ptr entries staged per tile (else global search)
+constexpr int kTrMaxCols = 44 * 1024;      // shared-memory offset table limit
+
+__global__ void tr_tile_rows_kernel(const int64_t* __restrict__ row_ptr, int64_t rows, int64_t nnz,
+                                    int64_t ntiles, int32_t* __restrict__ tile_row) {
+    for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t <= ntiles;
+         t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t e = std::min<int64_t>(t * kTrTile, nnz - 1);
+        int64_t lo = 0, hi = rows - 1;  // largest r with row_ptr[r] <= e
+        while (lo < hi) {
+            const int64_t mid = (lo + hi + 1) >> 1;
+            if (row_ptr[mid] <= e) lo = mid; else hi = mid - 1;
+        }
+        tile_row[t] = static_cast<int32_t>(t == ntiles ? rows - 1 : lo);
+    }
+}
+
+__global__ void __launch_bounds__(kTrThreads)
+tr_count_kernel(const int32_t* __restrict__ col_idx, int64_t nnz, int64_t chunk, int n, uint32_t* __restrict__ H) {
+    extern __shared__ uint32_t hist[];
+    for (int c = threadIdx.x; c < n; c += blockDim.x) hist[c] = 0;
+    __syncthreads();
+    const int64_t e0 = blockIdx.x * chunk, e1 = std::min<int64_t>(nnz, e0 + chunk);
+    int64_t e = e0 + threadIdx.x;
+    for (; e + 3 * kTrThreads < e1; e += 4 * kTrThreads) {
+        const int c0 = __ldcs(col_idx + e), c1 = __ldcs(col_idx + e + kTrThreads);
+        const int c2 = __ldcs(col_idx + e + 2 * kTrThreads), c3 = __ldcs(col_idx + e + 3 * kTrThreads);
+        atomicAdd(hist + c0, 1u);
+        atomicAdd(hist + c1, 1u);
+        atomicAdd(hist + c2, 1u);
+        atomicAdd(hist + c3, 1u);
+    }
+    for (; e < e1; e += kTrThreads) atomicAdd(hist + col_idx[e], 1u);
+    __syncthreads();
+    uint32_t* out = H + static_cast<int64_t>(blockIdx.x) * n;
+    for (int c = threadIdx.x; c < n; c += blockDim.x) out[c] = hist[c];
+}
+
+// block (32 columns, 32 chunk groups)
+__global__ void tr_colscan_kernel(uint32_t* __restrict__ H, int nchunks, int n,
+                                  unsigned long long* __restrict__ totals) {
+    __shared__ uint32_t part[32][33];
+    const int col = blockIdx.x * 32 + threadIdx.x;
+    const int g = threadIdx.y;
+    const int per = (nchunks + 31) / 32;
+    const int k0 = std::min(nchunks, g * per), k1 = std::min(nchunks, (g + 1) * per);
+    uint32_t sum = 0;
+    if (col < n)
+        for (int k = k0; k < k1; ++k) sum += H[static_cast<int64_t>(k) * n + col];
+    part[g][threadIdx.x] = sum;
+    __syncthreads();
+    if (g == 0) {
+        uint32_t run = 0;
+        for (int i = 0; i < 32; ++i) {
+            const uint32_t v = part[i][threadIdx.x];
+            part[i][threadIdx.x] = run;
+            run += v;
+        }
+        if (col < n) totals[col] = run;
+    }
+    __syncthreads();
+    if (col < n) {
+        uint32_t run = part[g][threadIdx.x];
+        for (int k = k0; k < k1; ++k) {
+            const int64_t i = static_cast<int64_t>(k) * n + col;
+            const uint32_t v = H[i];
+            H[i] = run;
+            run += v;
+        }
+    }
+}
+
+__device__ __forceinline__ int tr_row_search(const int64_t* __restrict__ rp, int lo, int hi, int64_t e) {
+    while (lo < hi) {  // largest r in [lo, hi] with rp[r] <= e
+        const int mid = (lo + hi + 1) >> 1;
+        if (rp[mid] <= e) lo = mid; else hi = mid - 1;
+    }
+    return lo;
+}
+
+__global__ void __launch_bounds__(kTrThreads)
+tr_scatter_kernel(const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col_idx,
+                  const float* __restrict__ values, int64_t nnz, int64_t chunk, int n,
+                  const uint32_t* __restrict__ H, const int64_t* __restrict__ col_ptr,
+                  const int32_t* __restrict__ tile_row, int32_t* __restrict__ out_rows,
+                  float* __restrict__ out_vals) {
+    extern __shared__ __align__(16) unsigned char tr_smem[];
+    uint32_t* off = reinterpret_cast<uint32_t*>(tr_smem);                  // n
+    int32_t* s_col = reinterpret_cast<int32_t*>(off + ((n + 3) & ~3));     // kTrTile
+    int32_t* s_row = s_col + kTrTile;                                      // kTrTile
+    float* s_val = reinterpret_cast<float*>(s_row + kTrTile);              // kTrTile
+    int64_t* s_rp = reinterpret_cast<int64_t*>(s_val + kTrTile);           // kTrSpan + 1
+    __shared__ int s_cnt[kTrSub][kTrWarps][kTrWarps];  // [sub][warp][owner]
+    __shared__ int s_olen[kTrWarps], s_ooff[kTrWarps];
+
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const unsigned lt = (1u << lane) - 1u;
+    const uint32_t* Hrow = H + static_cast<int64_t>(blockIdx.x) * n;
+    for (int c = threadIdx.x; c < n; c += blockDim.x) off[c] = static_cast<uint32_t>(col_ptr[c]) + Hrow[c];
+    const int64_t e0 = blockIdx.x * chunk, e1 = std::min<int64_t>(nnz, e0 + chunk);
+    __syncthreads();
+    for (int64_t tb = e0; tb < e1; tb += kTrTile) {
+        const int64_t t = tb / kTrTile;
+        const int ra = tile_row[t], rb = tile_row[t + 1];
+        const bool staged = rb - ra <= kTrSpan;
+        if (staged)
+            for (int i = threadIdx.x; i <= rb - ra + 1 && i <= kTrSpan; i += blockDim.x)
+                s_rp[i] = row_ptr[ra + i];
+        int c[kTrSub], o[kTrSub];
+        float v[kTrSub];
+#pragma unroll
+        for (int k = 0; k < kTrSub; ++k) {
+            const int64_t e = tb + k * kTrThreads + threadIdx.x;
+            const bool ok = e < e1;
+            c[k] = ok ? __ldcs(col_idx + e) : -1;
+            v[k] = ok ? __ldcs(values + e) : 0.f;
+            o[k] = ok ? (c[k] & (kTrWarps - 1)) : kTrWarps;
+        }
+        // per (sub-tile, warp) counts of every owner; stable rank within the warp
+        int rank[kTrSub];
+#pragma unroll
+        for (int k = 0; k < kTrSub; ++k) {
+            const unsigned peers = __match_any_sync(0xffffffffu, o[k]);
+            rank[k] = __popc(peers & lt);
+#pragma unroll
+            for (int w = 0; w < kTrWarps; ++w) {
+                const unsigned b = __ballot_sync(0xffffffffu, o[k] == w);
+                if (lane == w) s_cnt[k][warp][w] = __popc(b);
+            }
+        }
+        __syncthreads();
+        if (threadIdx.x < kTrWarps) {  // owner ow: exclusive scan over (sub-tile, warp) in element order
+            const int ow = threadIdx.x;
+            int run = 0;
+            for (int k = 0; k < kTrSub; ++k)
+                for (int w = 0; w < kTrWarps; ++w) {
+                    const int x = s_cnt[k][w][ow];
+                    s_cnt[k][w][ow] = run;
+                    run += x;
+                }
+            s_olen[ow] = run;
+        }
+        __syncthreads();
+        if (warp == 0) {
+            const int x = lane < kTrWarps ? s_olen[lane] : 0;
+            int inc = x;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, inc, d);
+                if (lane >= d) inc += y;
+            }
+            if (lane < kTrWarps) s_ooff[lane] = inc - x;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < kTrSub; ++k) {
+            if (o[k] < kTrWarps) {
+                const int64_t e = tb + k * kTrThreads + threadIdx.x;
+                const int r = staged ? ra + tr_row_search(s_rp, 0, rb - ra, e)
+                                     : tr_row_search(row_ptr, ra, rb, e);  // (tr_row_search on global)
+                const int p = s_ooff[o[k]] + s_cnt[k][warp][o[k]] + rank[k];
+                s_col[p] = c[k];
+                s_row[p] = r;
+                s_val[p] = v[k];
+            }
+        }
+        __syncthreads();
+        // warp `warp` places its columns, in element order
+        const int len = s_olen[warp], base = s_ooff[warp];
+        for (int j = 0; j < len; j += 32) {
+            const int idx = j + lane;
+            const bool ok = idx < len;
+            const int cc = ok ? s_col[base + idx] : -1 - lane;
+            const unsigned peers = __match_any_sync(0xffffffffu, cc);
+            const int leader = __ffs(peers) - 1;
+            uint32_t old = 0;
+            if (ok && lane == leader) {
+                old = off[cc];
+                off[cc] = old + __popc(peers);
+            }
+            old = __shfl_sync(0xffffffffu, old, leader);
+            if (ok) {
+                const uint32_t pos = old + __popc(peers & lt);
+                out_rows[pos] = s_row[base + idx];
+                out_vals[pos] = s_val[base + idx];
+            }
+            __syncwarp();
+        }
+        __syncthreads();
+    }
+}
+
 // --------------------------------------------------------------- helpers -------------
 // Per nonzero: key = column, payload = (row << 32) | value bits.
 __global__ void csr_pack_kernel(const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col_idx,
@@ -378,8 +591,8 @@ void csr_from_triplets_device(int64_t m, int64_t n, const int64_t* rows, const i
     exclusive_scan_ptr<unsigned long long>(cnt.as<unsigned long long>(), m, row_ptr, s);
 }
 
-void csr_to_csc_device(const DevCsr& a, int64_t* col_ptr, int32_t* row_idx, float* values,
-                       cudaStream_t s) {
+void csr_to_csc_radix(const DevCsr& a, int64_t* col_ptr, int32_t* row_idx, float* values,
+                      cudaStream_t s) {
     const int64_t n = a.nnz;
     if (a.rows > 0xffffffffLL) fail_input("row count exceeds the device transpose range");
     DevBuf cnt(sizeof(unsigned long long) * std::max<int64_t>(a.cols, 1), s);
@@ -400,6 +613,55 @@ void csr_to_csc_device(const DevCsr& a, int64_t* col_ptr, int32_t* row_idx, floa
                                p1.as<uint64_t>(), n, bits_for(a.cols), s);
     unpack_kernel<<<grid_for(n), 256, 0, s>>>(p0.as<uint64_t>(), n, row_idx, values);
     ALSK_LAUNCHED();
+}
+
+// Single-pass counting-sort transpose when the column table fits shared memory and every
+// position fits 32 bits (all the named shapes' CSR -> CSC); the two-pass radix sort otherwise.
+bool csr_to_csc_counting(const DevCsr& a, int64_t* col_ptr, int32_t* row_idx, float* values, cudaStream_t s) {
+    const int64_t n = a.cols, nnz = a.nnz;
+    if (n < 1 || n > kTrMaxCols || nnz >= (int64_t(1) << 32) || a.rows >= (int64_t(1) << 31) || nnz == 0)
+        return false;
+    const size_t smem_scatter = sizeof(uint32_t) * ((n + 3) & ~3) + sizeof(int32_t) * 3 * kTrTile +
+                                sizeof(int64_t) * (kTrSpan + 2);
+    static bool attr = false;
+    if (!attr) {
+        ALSK_CUDA(cudaFuncSetAttribute(tr_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+        ALSK_CUDA(cudaFuncSetAttribute(tr_count_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+        attr = true;
+    }
+    int occ = 0;
+    ALSK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, tr_scatter_kernel, kTrThreads, smem_scatter));
+    if (occ < 1) return false;
+    const int64_t ntiles_total = (nnz + kTrTile - 1) / kTrTile;
+    const int64_t want = static_cast<int64_t>(num_sms()) * occ;
+    const int64_t tiles_per_chunk = std::max<int64_t>(1, (ntiles_total + want - 1) / want);
+    const int64_t chunk = tiles_per_chunk * kTrTile;
+    const int nchunks = static_cast<int>((nnz + chunk - 1) / chunk);
+    DevBuf tile_row(sizeof(int32_t) * (ntiles_total + 1), s);
+    DevBuf H(sizeof(uint32_t) * static_cast<size_t>(nchunks) * n, s);
+    DevBuf totals(sizeof(unsigned long long) * n, s);
+    tr_tile_rows_kernel<<<grid_for(ntiles_total + 1), 256, 0, s>>>(a.row_ptr, a.rows, nnz, ntiles_total,
+                                                                   tile_row.as<int32_t>());
+    ALSK_LAUNCHED();
+    tr_count_kernel<<<nchunks, kTrThreads, sizeof(uint32_t) * n, s>>>(a.col_idx, nnz, chunk, static_cast<int>(n),
+                                                                     H.as<uint32_t>());
+    ALSK_LAUNCHED();
+    tr_colscan_kernel<<<static_cast<unsigned>((n + 31) / 32), dim3(32, 32), 0, s>>>(
+        H.as<uint32_t>(), nchunks, static_cast<int>(n), totals.as<unsigned long long>());
+    ALSK_LAUNCHED();
+    exclusive_scan_ptr<unsigned long long>(totals.as<unsigned long long>(), n, col_ptr, s);
+    tr_scatter_kernel<<<nchunks, kTrThreads, smem_scatter, s>>>(a.row_ptr, a.col_idx, a.values, nnz, chunk,
+                                                                static_cast<int>(n), H.as<uint32_t>(), col_ptr,
+                                                                tile_row.as<int32_t>(), row_idx, values);
+    ALSK_LAUNCHED();
+    return true;
+}
+
+void csr_to_csc_device(const DevCsr& a, int64_t* col_ptr, int32_t* row_idx, float* values,
+                       cudaStream_t s) {
+    static const bool radix_only = std::getenv("ALSK_TRANSPOSE_RADIX") != nullptr;  // A/B switch
+    if (!radix_only && csr_to_csc_counting(a, col_ptr, row_idx, values, s)) return;
+    csr_to_csc_radix(a, col_ptr, row_idx, values, s);
 }
 
 }  // namespace alsk
