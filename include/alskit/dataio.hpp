@@ -32,8 +32,33 @@ inline CsrMatrix load_binary_cache(const std::filesystem::path& path) {
     a.row_ptr.resize(static_cast<std::size_t>(rows) + 1);
     a.col_idx.resize(static_cast<std::size_t>(nnz));
     a.values.resize(static_cast<std::size_t>(nnz));
-    detail::check(alsk_load_cache(path.c_str(), a.row_ptr.data(), a.col_idx.data(), a.values.data()));
+    detail::check(alsk_load_cache(path.c_str(), rows, nnz, a.row_ptr.data(), a.col_idx.data(), a.values.data()));
     return a;
+}
+
+/// dataio.hpp:240-244
+struct SplitResult {
+    CsrMatrix train;
+    std::vector<Triplet> test;
+};
+
+/// dataio.hpp:251-290: floor(nnz * holdout) nonzeros held out by a partial Fisher-Yates over
+/// positions (the same mt19937_64 draws, so the split is the reference's bit for bit).
+inline SplitResult split_train_test(const CsrMatrix& r, double holdout_fraction, std::uint64_t seed) {
+    const alsk_csr v = detail::view(r);
+    std::int64_t k = 0;
+    detail::check(alsk_split_train_test(&v, holdout_fraction, seed, &k, nullptr, nullptr, nullptr, nullptr));
+    SplitResult out;
+    out.train.rows = r.rows;
+    out.train.cols = r.cols;
+    out.train.row_ptr.resize(static_cast<std::size_t>(r.rows) + 1);
+    out.train.col_idx.resize(static_cast<std::size_t>(r.nnz() - k));
+    out.train.values.resize(static_cast<std::size_t>(r.nnz() - k));
+    out.test.resize(static_cast<std::size_t>(k));
+    detail::check(alsk_split_train_test(&v, holdout_fraction, seed, &k, out.train.row_ptr.data(),
+                                        out.train.col_idx.data(), out.train.values.data(),
+                                        reinterpret_cast<alsk_triplet*>(out.test.data())));
+    return out;
 }
 
 // ---- grid persistence and streaming (dataio.hpp:352-540) ----
@@ -170,7 +195,8 @@ inline Checkpoint read_checkpoint(const std::filesystem::path& path) {
     cp.which = static_cast<FactorKind>(which);
     cp.factor = FactorMatrix(rows, f);
     cp.digest = digest;
-    detail::check(alsk_checkpoint_read(path.c_str(), cp.factor.entries.data()));
+    detail::check(alsk_checkpoint_read(path.c_str(), static_cast<int64_t>(cp.factor.entries.size()),
+                                       cp.factor.entries.data()));
     return cp;
 }
 

@@ -252,9 +252,12 @@ alsk_status alsk_dev_solve_packed_f32(const float* packed, int64_t count, int f,
  * upload). */
 alsk_status alsk_cache_header(const char* path, int64_t* rows, int64_t* cols, int64_t* nnz);
 alsk_status alsk_save_cache(const alsk_csr* r, const char* path);
-alsk_status alsk_load_cache(const char* path, int64_t* row_ptr, int32_t* col_idx, float* values);
-alsk_status alsk_dev_load_cache(const char* path, int64_t* row_ptr, int32_t* col_idx, float* values,
-                                void* stream);
+/* cap_rows / cap_nnz: the capacity of the caller's buffers (row_ptr holds cap_rows+1); a file
+ * whose header grew since the caller read it is an IoError, never an overrun. */
+alsk_status alsk_load_cache(const char* path, int64_t cap_rows, int64_t cap_nnz, int64_t* row_ptr, int32_t* col_idx,
+                            float* values);
+alsk_status alsk_dev_load_cache(const char* path, int64_t cap_rows, int64_t cap_nnz, int64_t* row_ptr,
+                                int32_t* col_idx, float* values, void* stream);
 
 /* Factor checkpoints (replace write_checkpoint / read_checkpoint / restore_latest /
  * CheckpointWriter, dataio.hpp:546-786): same file format (56-byte header: magic "ALSKCPKT",
@@ -265,8 +268,8 @@ alsk_status alsk_checkpoint_write(const char* dir, int iteration, int which, int
 alsk_status alsk_checkpoint_path(const char* dir, int iteration, int which, char* out, size_t cap);
 alsk_status alsk_checkpoint_header(const char* path, int* iteration, int* which, int64_t* rows, int* f,
                                    uint64_t* digest);
-alsk_status alsk_checkpoint_read(const char* path, float* entries);
-alsk_status alsk_dev_checkpoint_read(const char* path, float* d_entries, void* stream);
+alsk_status alsk_checkpoint_read(const char* path, int64_t cap_entries, float* entries);
+alsk_status alsk_dev_checkpoint_read(const char* path, int64_t cap_entries, float* d_entries, void* stream);
 /* which = -1: newest of either kind (theta outranks x at the same iteration); 0 / 1: that
  * kind only. *found = 0 when the directory holds none. */
 alsk_status alsk_checkpoint_latest(const char* dir, int which, char* out, size_t cap, int* found);
@@ -334,6 +337,8 @@ alsk_status alsk_session_half_theta(alsk_session* s);  /* Theta = update_x(R^T, 
 alsk_status alsk_session_loss(alsk_session* s, double* out);
 alsk_status alsk_session_rmse(alsk_session* s, double* out); /* NaN when there is no test set */
 alsk_status alsk_session_factors(alsk_session* s, float* x_out, float* theta_out);
+/* The session's device factors and its stream (for device-side snapshots). */
+alsk_status alsk_session_device(alsk_session* s, float** x, float** theta, void** stream);
 void alsk_session_destroy(alsk_session* s);
 
 /* ---- host data helpers (dataio/factor restatements used by the drivers) ------------ */

@@ -465,3 +465,32 @@ void ref_bench_release(void) {
 }
 
 }  // extern "C"
+
+// The reference's own train_run (driver.hpp:107-268) on a binary cache, for the C++ driver
+// parity test (tests/test_train_run.py): factors out, metrics / checkpoints on disk.
+// stop_after > 0: the callback stops the run after that iteration (a killed run).
+extern "C" alsk_status ref_train_run(const char* cache, int f, double lambda, int iterations, uint64_t seed,
+                                     int acc_double, const char* ckpt_dir, const char* metrics, int resume,
+                                     int stop_after, float* x_out, float* theta_out, int* start_iteration,
+                                     uint64_t* digest) {
+    return guarded([&] {
+        R::RunConfig cfg;
+        cfg.data = cache;
+        cfg.format = R::RatingsFormat::binary_cache;
+        cfg.f = f;
+        cfg.lambda = lambda;
+        cfg.iterations = iterations;
+        cfg.seed = seed;
+        cfg.accumulate_double = acc_double != 0;
+        cfg.checkpoint_dir = ckpt_dir ? ckpt_dir : "";
+        cfg.metrics = metrics ? metrics : "";
+        cfg.resume = resume != 0;
+        R::IterationCallback cb;
+        if (stop_after > 0) cb = [&](int t, const R::FactorMatrix&, const R::FactorMatrix&) { return t < stop_after; };
+        const R::TrainResult r = R::train_run(cfg, cb);
+        std::memcpy(x_out, r.x.entries.data(), sizeof(float) * r.x.entries.size());
+        std::memcpy(theta_out, r.theta.entries.data(), sizeof(float) * r.theta.entries.size());
+        *start_iteration = r.start_iteration;
+        *digest = r.digest;
+    });
+}

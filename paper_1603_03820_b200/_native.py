@@ -75,8 +75,8 @@ _SIGS = {
     "alsk_packed_stride": (i64, [C.c_int]),
     "alsk_cache_header": (C.c_int, [C.c_char_p, C.POINTER(i64), C.POINTER(i64), C.POINTER(i64)]),
     "alsk_save_cache": (C.c_int, [CsrP, C.c_char_p]),
-    "alsk_load_cache": (C.c_int, [C.c_char_p, vp, vp, vp]),
-    "alsk_dev_load_cache": (C.c_int, [C.c_char_p, vp, vp, vp, vp]),
+    "alsk_load_cache": (C.c_int, [C.c_char_p, i64, i64, vp, vp, vp]),
+    "alsk_dev_load_cache": (C.c_int, [C.c_char_p, i64, i64, vp, vp, vp, vp]),
     "alsk_persist_grid_meta": (C.c_int, [C.c_char_p, C.c_int, C.c_int, i64, i64, vp, vp]),
     "alsk_block_path": (C.c_int, [C.c_char_p, C.c_int, C.c_int, C.c_char_p, C.c_size_t]),
     "alsk_grid_meta": (C.c_int, [C.c_char_p, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(i64), C.POINTER(i64),
@@ -91,8 +91,8 @@ _SIGS = {
     "alsk_checkpoint_path": (C.c_int, [C.c_char_p, C.c_int, C.c_int, C.c_char_p, C.c_size_t]),
     "alsk_checkpoint_header": (C.c_int, [C.c_char_p, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(i64),
                                          C.POINTER(C.c_int), C.POINTER(C.c_uint64)]),
-    "alsk_checkpoint_read": (C.c_int, [C.c_char_p, vp]),
-    "alsk_dev_checkpoint_read": (C.c_int, [C.c_char_p, vp, vp]),
+    "alsk_checkpoint_read": (C.c_int, [C.c_char_p, i64, vp]),
+    "alsk_dev_checkpoint_read": (C.c_int, [C.c_char_p, i64, vp, vp]),
     "alsk_checkpoint_latest": (C.c_int, [C.c_char_p, C.c_int, C.c_char_p, C.c_size_t, C.POINTER(C.c_int)]),
     "alsk_ckpt_writer_create": (C.c_int, [C.c_char_p, C.POINTER(vp)]),
     "alsk_ckpt_writer_submit_device": (C.c_int, [vp, C.c_int, C.c_int, i64, C.c_int, C.c_uint64, vp, vp]),
@@ -115,6 +115,7 @@ _SIGS = {
     "alsk_dev_split_mask": (C.c_int, [CsrP, vp, i64, i64, vp, vp, vp, vp, i64p, vp]),
     "alsk_dev_filter_columns": (C.c_int, [CsrP, i64, i64, vp, vp, vp, i64p, vp]),
     "alsk_profile_phase": (None, [C.c_int, f64p, C.POINTER(u64)]),
+    "alsk_session_device": (C.c_int, [vp, C.POINTER(vp), C.POINTER(vp), C.POINTER(vp)]),
     # multi-GPU (multigpu.cu)
     "alsk_comm_available": (C.c_int, []),
     "alsk_nccl_version": (C.c_int, []),

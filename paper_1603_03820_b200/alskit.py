@@ -513,7 +513,7 @@ def load_binary_cache(path) -> CsrMatrix:
     rp = np.empty(rows + 1, np.int64)
     ci = np.empty(nnz, np.int32)
     va = np.empty(nnz, np.float32)
-    _check(LIB.alsk_load_cache(os.fsencode(path), _p(rp), _p(ci), _p(va)))
+    _check(LIB.alsk_load_cache(os.fsencode(path), rows, nnz, _p(rp), _p(ci), _p(va)))
     return CsrMatrix(rows, cols, 0, rp, ci, va)
 
 
@@ -610,7 +610,7 @@ def read_checkpoint(path) -> Checkpoint:
     """dataio.hpp:627-651: bit-identical to what was written."""
     it, wh, rows, f, dg = checkpoint_header(path)
     e = np.empty(rows * f, np.float32)
-    _check(LIB.alsk_checkpoint_read(os.fsencode(path), _p(e)))
+    _check(LIB.alsk_checkpoint_read(os.fsencode(path), e.size, _p(e)))
     return Checkpoint(it, wh, FactorMatrix(rows, f, e), dg)
 
 

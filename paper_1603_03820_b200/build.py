@@ -26,6 +26,11 @@ NVCC_FLAGS = ARCH + [
     "--expt-relaxed-constexpr", f"-I{INCLUDE}", f"-I{CSRC}",
 ]
 CXX_FLAGS = ["-O3", "-std=c++17", "-fPIC", "-pthread", f"-I{INCLUDE}", f"-I{CSRC}"]
+# ALSK_MEASURE=1 builds the measurement library (profiling counters, dry runs, A/B variants
+# read from the environment; csrc/measure.cuh). The product build ignores those switches.
+if os.environ.get("ALSK_MEASURE") == "1":
+    NVCC_FLAGS.append("-DALSK_MEASURE")
+    CXX_FLAGS.append("-DALSK_MEASURE")
 
 
 def _headers_mtime() -> float:
@@ -71,7 +76,7 @@ def build(verbose: bool = False) -> Path:
     return LIB
 
 
-CPP_TESTS = [ROOT / "tests" / "cpp" / "dropin_test.cpp"]
+CPP_TESTS = [ROOT / "tests" / "cpp" / "dropin_test.cpp", ROOT / "tests" / "cpp" / "train_run_cli.cpp"]
 
 
 def build_cpp_tests(verbose: bool = False) -> list[Path]:

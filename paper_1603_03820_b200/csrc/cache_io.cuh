@@ -123,6 +123,9 @@ struct Validator {
     int32_t last = 0;   // col_idx[k0 - 1] of the chunk being fed
     [[noreturn]] void bad(const std::string& m) const { fail_io(path + ": corrupt cache (" + m + ")"); }
     void ends() const {
+        // check_dims first, as validate() does (sparse.hpp:88-92, 106)
+        if (cols > 2147483647LL)
+            bad("column count " + std::to_string(cols) + " exceeds the 32-bit index range");
         if (rp[0] != 0 || rp[rows] != nnz) bad("row_ptr must start at 0 and end at nnz");
     }
     void feed(const int32_t* ci, int64_t k0, int64_t k1) {

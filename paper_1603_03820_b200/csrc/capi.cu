@@ -1015,6 +1015,14 @@ alsk_status alsk_session_factors(alsk_session* S, float* x_out, float* theta_out
     });
 }
 
+alsk_status alsk_session_device(alsk_session* S, float** x, float** theta, void** stream) {
+    return guard([&] {
+        if (x) *x = S->X.as<float>();
+        if (theta) *theta = S->T.as<float>();
+        if (stream) *stream = S->stream;
+    });
+}
+
 void alsk_session_destroy(alsk_session* S) {
     if (!S) return;
     cudaStream_t s = S->stream;
@@ -1051,12 +1059,25 @@ alsk_status alsk_save_cache(const alsk_csr* r, const char* path) {
     });
 }
 
-// Host buffers (sizes from alsk_cache_header).
-alsk_status alsk_load_cache(const char* path, int64_t* row_ptr, int32_t* col_idx, float* values) {
+namespace alsk {
+// The caller sized its buffers from an earlier header read; a file replaced since then (a
+// re-persisted grid, a new cache) must not be loaded past them.
+inline void check_capacity(const char* path, int64_t have_rows, int64_t have_nnz, int64_t cap_rows, int64_t cap_nnz) {
+    if (have_rows > cap_rows || have_nnz > cap_nnz)
+        fail_io(std::string(path) + ": file changed since its header was read (" + std::to_string(have_rows) +
+                " rows / " + std::to_string(have_nnz) + " entries exceed the caller's " + std::to_string(cap_rows) +
+                " / " + std::to_string(cap_nnz) + ")");
+}
+}  // namespace alsk
+
+// Host buffers of capacity cap_rows+1 / cap_nnz (sizes from alsk_cache_header).
+alsk_status alsk_load_cache(const char* path, int64_t cap_rows, int64_t cap_nnz, int64_t* row_ptr, int32_t* col_idx,
+                            float* values) {
     return guard([&] {
         File in(path, "rb");
         const Header h = read_header(in);
         const int64_t rows = static_cast<int64_t>(h.rows), nnz = static_cast<int64_t>(h.nnz);
+        check_capacity(path, rows, nnz, cap_rows, cap_nnz);
         in.read(row_ptr, sizeof(int64_t) * (rows + 1), "row_ptr");
         in.read(col_idx, sizeof(int32_t) * nnz, "col_idx");
         in.read(values, sizeof(float) * nnz, "values");
@@ -1067,13 +1088,15 @@ alsk_status alsk_load_cache(const char* path, int64_t* row_ptr, int32_t* col_idx
 }
 
 // Device buffers: row_ptr[rows+1], col_idx[nnz], values[nnz] (sizes from alsk_cache_header).
-alsk_status alsk_dev_load_cache(const char* path, int64_t* row_ptr, int32_t* col_idx, float* values, void* stream) {
+alsk_status alsk_dev_load_cache(const char* path, int64_t cap_rows, int64_t cap_nnz, int64_t* row_ptr,
+                                int32_t* col_idx, float* values, void* stream) {
     return guard([&] {
         require_device();
         cudaStream_t s = static_cast<cudaStream_t>(stream);
         File in(path, "rb");
         const Header h = read_header(in);
         const int64_t rows = static_cast<int64_t>(h.rows), nnz = static_cast<int64_t>(h.nnz);
+        check_capacity(path, rows, nnz, cap_rows, cap_nnz);
         std::vector<int64_t> rp(static_cast<size_t>(rows) + 1);
         in.read(rp.data(), sizeof(int64_t) * rp.size(), "row_ptr");
         Validator val{rp.data(), rows, static_cast<int64_t>(h.cols), nnz, in.path};
@@ -1146,20 +1169,22 @@ alsk_status alsk_checkpoint_header(const char* path, int* iteration, int* which,
     });
 }
 
-alsk_status alsk_checkpoint_read(const char* path, float* entries) {
+alsk_status alsk_checkpoint_read(const char* path, int64_t cap_entries, float* entries) {
     return guard([&] {
         File in(path, "rb");
         const CkptHeader h = read_checkpoint_header(in);
+        check_capacity(path, 0, static_cast<int64_t>(h.rows) * h.f, 0, cap_entries);
         in.read(entries, sizeof(float) * static_cast<size_t>(h.rows) * h.f, "payload");
     });
 }
 
 // Restore a factor straight into HBM (rows*f floats at d_entries), through pinned staging.
-alsk_status alsk_dev_checkpoint_read(const char* path, float* d_entries, void* stream) {
+alsk_status alsk_dev_checkpoint_read(const char* path, int64_t cap_entries, float* d_entries, void* stream) {
     return guard([&] {
         require_device();
         File in(path, "rb");
         const CkptHeader h = read_checkpoint_header(in);
+        check_capacity(path, 0, static_cast<int64_t>(h.rows) * h.f, 0, cap_entries);
         const size_t bytes = sizeof(float) * static_cast<size_t>(h.rows) * h.f;
         if (!bytes) return;
         void* stage = nullptr;

@@ -31,6 +31,7 @@
 #include <cstdlib>
 
 #include "kernels.cuh"
+#include "measure.cuh"
 
 namespace alsk {
 namespace {
@@ -668,7 +669,7 @@ bool dispatch(const DevCsr& r, const float* theta, int64_t theta_rows, int f, fl
 bool update_fused_fp32(const DevCsr& r, const float* theta, int64_t theta_rows, int f, float lambda, int64_t rb,
                        int64_t re, float* x_out, const SolveStatus& st, cudaStream_t s) {
     // small ranks: a thread per row when rows average under 32 ratings, else a warp per row
-    static const bool no_small = std::getenv("ALSK_NO_SMALL_F") != nullptr;  // A/B switch
+    static const bool no_small = measure_env("ALSK_NO_SMALL_F") != nullptr;  // A/B switch
     if (!no_small && f <= 15 && r.rows > 0) {
         if (re <= rb) return true;
         // rows read in place at stride f (a factor is never copied: at SparkALS scale X is

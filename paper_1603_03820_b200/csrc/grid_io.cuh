@@ -123,12 +123,8 @@ class DeviceBlockStream {
 
     DeviceBlockStream(std::string dir, std::vector<int> order)
         : dir_(std::move(dir)), meta_(read_grid_meta(dir_)), order_(std::move(order)) {
-        for (size_t k = 0; k + 1 < order_.size(); k += 2) {
-            const int i = order_[k], j = order_[k + 1];
-            if (i < 0 || i >= meta_.p || j < 0 || j >= meta_.q)
-                fail_input("block (" + std::to_string(i) + ", " + std::to_string(j) + ") lies outside the " +
-                           std::to_string(meta_.p) + "x" + std::to_string(meta_.q) + " grid");
-        }
+        // an out-of-range block is reported by the next() that would return it, after the
+        // blocks before it in the plan (as BlockStream::next does, dataio.hpp:498-506)
         ALSK_CUDA(cudaGetDevice(&device_));
         ALSK_CUDA(cudaStreamCreateWithFlags(&upload_, cudaStreamNonBlocking));
         for (Slot& s : slots_) {
@@ -145,6 +141,10 @@ class DeviceBlockStream {
         }
         cv_.notify_all();
         loader_.join();
+        // the block still handed out may be in use by work the consumer queued after the last
+        // next(): release it on the consumer's stream and order the frees after that
+        if (in_use_ >= 0 && consumer_) cudaEventRecord(slots_[in_use_].released, consumer_);
+        for (Slot& s : slots_) cudaStreamWaitEvent(upload_, s.released, 0);
         cudaStreamSynchronize(upload_);
         for (Slot& s : slots_) {
             cudaEventSynchronize(s.released);
@@ -160,6 +160,7 @@ class DeviceBlockStream {
     // block would have been returned
     bool next(cudaStream_t consumer, Out& out) {
         std::unique_lock<std::mutex> lock(mu_);
+        consumer_ = consumer;
         if (in_use_ >= 0) {  // the consumer is done issuing work on the previous block
             ALSK_CUDA(cudaEventRecord(slots_[in_use_].released, consumer));
             slots_[in_use_].busy = false;
@@ -267,7 +268,11 @@ class DeviceBlockStream {
                         if (!slots_[t].busy) slot = t;
                     slots_[slot].busy = true;
                 }
-                load(slots_[slot], order_[k], order_[k + 1]);
+                const int bi = order_[k], bj = order_[k + 1];
+                if (bi < 0 || bi >= meta_.p || bj < 0 || bj >= meta_.q)
+                    fail_input("block (" + std::to_string(bi) + ", " + std::to_string(bj) + ") lies outside the " +
+                               std::to_string(meta_.p) + "x" + std::to_string(meta_.q) + " grid");
+                load(slots_[slot], bi, bj);
                 {
                     std::lock_guard<std::mutex> lock(mu_);
                     queue_.push_back(slot);
@@ -295,6 +300,7 @@ class DeviceBlockStream {
     std::vector<int> order_;  // i0, j0, i1, j1, ...
     int device_ = 0;
     cudaStream_t upload_ = nullptr;
+    cudaStream_t consumer_ = nullptr;  // stream of the last next(): the in-use block's user
     Slot slots_[3];
     std::mutex mu_;
     std::condition_variable cv_;

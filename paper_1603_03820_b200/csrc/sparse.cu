@@ -16,6 +16,7 @@
 #include <vector>
 
 #include "kernels.cuh"
+#include "measure.cuh"
 
 namespace alsk {
 namespace {
@@ -623,12 +624,13 @@ bool csr_to_csc_counting(const DevCsr& a, int64_t* col_ptr, int32_t* row_idx, fl
         return false;
     const size_t smem_scatter = sizeof(uint32_t) * ((n + 3) & ~3) + sizeof(int32_t) * 3 * kTrTile +
                                 sizeof(int64_t) * (kTrSpan + 2);
-    static bool attr = false;
-    if (!attr) {
-        ALSK_CUDA(cudaFuncSetAttribute(tr_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-        ALSK_CUDA(cudaFuncSetAttribute(tr_count_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-        attr = true;
-    }
+    cudaFuncAttributes fa{};
+    ALSK_CUDA(cudaFuncGetAttributes(&fa, tr_scatter_kernel));
+    if (smem_scatter + fa.sharedSizeBytes > 227 * 1024) return false;
+    ALSK_CUDA(cudaFuncSetAttribute(tr_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   static_cast<int>(smem_scatter)));
+    ALSK_CUDA(cudaFuncSetAttribute(tr_count_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   static_cast<int>(sizeof(uint32_t) * n)));
     int occ = 0;
     ALSK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, tr_scatter_kernel, kTrThreads, smem_scatter));
     if (occ < 1) return false;
@@ -659,7 +661,7 @@ bool csr_to_csc_counting(const DevCsr& a, int64_t* col_ptr, int32_t* row_idx, fl
 
 void csr_to_csc_device(const DevCsr& a, int64_t* col_ptr, int32_t* row_idx, float* values,
                        cudaStream_t s) {
-    static const bool radix_only = std::getenv("ALSK_TRANSPOSE_RADIX") != nullptr;  // A/B switch
+    static const bool radix_only = measure_env("ALSK_TRANSPOSE_RADIX") != nullptr;  // A/B switch
     if (!radix_only && csr_to_csc_counting(a, col_ptr, row_idx, values, s)) return;
     csr_to_csc_radix(a, col_ptr, row_idx, values, s);
 }

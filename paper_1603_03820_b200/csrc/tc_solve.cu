@@ -34,6 +34,7 @@
 #include <vector>
 
 #include "kernels.cuh"
+#include "measure.cuh"
 #include "tc_common.cuh"
 
 namespace alsk {
@@ -475,10 +476,10 @@ void launch_solve(const float* packed, int64_t count, int f, float* x, const Sol
     // on an SM, so no CTA waits in tcgen05.alloc for another to finish
     const int smem = static_cast<int>(std::max<size_t>(P.total, 46 * 1024));
     static const int per_sm = [] {  // CTAs per SM (A/B switch for latency measurements; at most 4)
-        const char* e = std::getenv("ALSK_TS_CTAS");
+        const char* e = measure_env("ALSK_TS_CTAS");
         return e ? std::max(1, std::min(4, std::atoi(e))) : 4;
     }();
-    static const bool want_prof = std::getenv("ALSK_TS_PROF") != nullptr;
+    static const bool want_prof = measure_env("ALSK_TS_PROF") != nullptr;
     // persistent CTAs with a static system assignment: never launch more than are resident
     // at once (large f: shared memory allows only 3 or 2 per SM), or the extra CTAs run as a
     // second wave after the others
@@ -490,7 +491,7 @@ void launch_solve(const float* packed, int64_t count, int f, float* x, const Sol
     resident = static_cast<int>((228 * 1024) / (smem + 2 * 1024));
     const int ctas_per_sm = std::max(1, std::min(per_sm, resident));
     static bool said = false;
-    if (!said && std::getenv("ALSK_TS_VERBOSE")) {
+    if (!said && measure_env("ALSK_TS_VERBOSE")) {
         std::fprintf(stderr, "[tc_solve] f=%d smem=%d resident=%d ctas_per_sm=%d\n", f, smem, resident, ctas_per_sm);
         said = true;
     }
@@ -499,18 +500,18 @@ void launch_solve(const float* packed, int64_t count, int f, float* x, const Sol
     // ALSK_TS_WAITS=mma_first,backsub (ns): first sleep of the MMA wait, back-substitution poll
     static const std::array<uint32_t, 2> tun = [] {
         std::array<uint32_t, 2> v{200u, 1000u};
-        if (const char* e = std::getenv("ALSK_TS_WAITS")) {
+        if (const char* e = measure_env("ALSK_TS_WAITS")) {
             unsigned a = 0, b = 0;
             if (std::sscanf(e, "%u,%u", &a, &b) == 2) v = {a, b};
         }
         return v;
     }();
     static const uint32_t sleep_ns = [] {
-        const char* e = std::getenv("ALSK_TS_SLEEP");
+        const char* e = measure_env("ALSK_TS_SLEEP");
         return e ? static_cast<uint32_t>(std::atoi(e)) : 32u;  // parking (0) measured slower
     }();
     // ALSK_TS_PROF=<factor thread>: whose phases the profile reports
-    const uint32_t opts = want_prof ? static_cast<uint32_t>(std::atoi(std::getenv("ALSK_TS_PROF")) & 127) : 0u;
+    const uint32_t opts = want_prof ? static_cast<uint32_t>(std::atoi(measure_env("ALSK_TS_PROF")) & 127) : 0u;
     if (!want_prof) {
         ALSK_CUDA(cudaFuncSetAttribute(tc_solve_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         tc_solve_kernel<false><<<grid, TS_THREADS, smem, s>>>(packed, count, f, x, st.min_row, st.column + status_off,
@@ -545,11 +546,11 @@ void launch_solve(const float* packed, int64_t count, int f, float* x, const Sol
 
 bool packed_solve(const float* packed, int64_t count, int f, float* x, const SolveStatus& st, int64_t status_off,
                   cudaStream_t s) {
-    static const bool tiles = std::getenv("ALSK_SOLVE_TILES") != nullptr;  // A/B switch for measurements
+    static const bool tiles = measure_env("ALSK_SOLVE_TILES") != nullptr;  // A/B switch for measurements
     if (tiles || f < 8 || f > 127) return packed_solve_tiles(packed, count, f, x, st, status_off, s);
     if (count <= 0) return true;
     static const int bw = [] {  // column-step width of the TMEM Cholesky (A/B switch)
-        const char* e = std::getenv("ALSK_TS_BW");
+        const char* e = measure_env("ALSK_TS_BW");
         return e ? std::atoi(e) : 8;
     }();
     if (bw == 16 && packed_solve16(packed, count, f, x, st, status_off, s)) return true;

@@ -14,6 +14,8 @@
 //      thread issues six negated MMAs (two K halves x Ph Ph^T + Ph Pl^T + Pl Ph^T).
 // The packed rows are read straight from global memory (prefetched into L2 one system
 // ahead), which leaves the shared memory for the 16-wide tiles at 4 CTAs per SM.
+// Measurement build only (ALSK_MEASURE): measured slower than tc_solve.cu;
+// the product library gets the stub at the end of this file.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -23,7 +25,10 @@
 #include <cstdlib>
 
 #include "kernels.cuh"
+#include "measure.cuh"
 #include "tc_common.cuh"
+
+#ifdef ALSK_MEASURE
 
 namespace alsk {
 namespace {
@@ -529,7 +534,7 @@ bool packed_solve16(const float* packed, int64_t count, int f, float* x, const S
     const unsigned grid = static_cast<unsigned>(std::min<int64_t>(count, per_sm * static_cast<int64_t>(num_sms())));
     static const std::array<uint32_t, 3> w = [] {  // poll sleep, MMA first sleep, back-substitution poll (ns)
         std::array<uint32_t, 3> v{32u, 200u, 1000u};
-        if (const char* e = std::getenv("ALSK_TS16_WAITS")) {
+        if (const char* e = measure_env("ALSK_TS16_WAITS")) {
             unsigned a = 0, b = 0, c = 0;
             if (std::sscanf(e, "%u,%u,%u", &a, &b, &c) == 3) v = {a, b, c};
         }
@@ -542,3 +547,11 @@ bool packed_solve16(const float* packed, int64_t count, int f, float* x, const S
 }
 
 }  // namespace alsk
+
+#else  // !ALSK_MEASURE
+
+namespace alsk {
+bool packed_solve16(const float*, int64_t, int, float*, const SolveStatus&, int64_t, cudaStream_t) { return false; }
+}  // namespace alsk
+
+#endif  // ALSK_MEASURE

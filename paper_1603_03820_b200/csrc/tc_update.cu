@@ -51,6 +51,7 @@
 #include <vector>
 
 #include "kernels.cuh"
+#include "measure.cuh"
 #include "tc_common.cuh"
 
 namespace alsk {
@@ -597,11 +598,11 @@ void launch_tc(const DevCsr& r, const float* theta, int64_t theta_rows, int f, i
                int64_t re, float* x, float* a, float* b, const SolveStatus* st, cudaStream_t s) {
     // deepest operand ring first (the MMA is fed by the split through it), then the staging ring
     static const int max_hls = [] {  // A/B switches for measurements
-        const char* e = std::getenv("ALSK_TC_HLS");
+        const char* e = measure_env("ALSK_TC_HLS");
         return e ? std::max(2, std::min(HL_STAGES_MAX, std::atoi(e))) : HL_STAGES_MAX;
     }();
     static const int max_stages = [] {
-        const char* e = std::getenv("ALSK_TC_STAGES");
+        const char* e = measure_env("ALSK_TC_STAGES");
         return e ? std::max(2, std::min(8, std::atoi(e))) : 6;  // 4-6 within noise (6 best with cp.async.ca), 3, 2, 7 slower
     }();
     int hls = max_hls, stages = max_stages;
@@ -616,7 +617,7 @@ void launch_tc(const DevCsr& r, const float* theta, int64_t theta_rows, int f, i
     // warps (ALSK_TC_SLEEP=epi,load,split,mma)
     static const std::array<uint32_t, 4> sleeps = [] {
         std::array<uint32_t, 4> v{128u, 32u, 50u, 20u};
-        if (const char* e = std::getenv("ALSK_TC_SLEEP")) {
+        if (const char* e = measure_env("ALSK_TC_SLEEP")) {
             unsigned a = 0, b = 0, c = 0, d = 0;
             if (std::sscanf(e, "%u,%u,%u,%u", &a, &b, &c, &d) == 4) v = {a, b, c, d};
         }
@@ -625,14 +626,14 @@ void launch_tc(const DevCsr& r, const float* theta, int64_t theta_rows, int f, i
     // ALSK_TC_DRY (measurements only, bit mask): 1 = split warps skip the split, 2 = no
     // MMAs, 4 = the epilogue treats D as zero
     static const uint32_t dry = [] {
-        const char* e = std::getenv("ALSK_TC_DRY");
+        const char* e = measure_env("ALSK_TC_DRY");
         return e ? static_cast<uint32_t>(std::atoi(e)) : 0u;
     }();
     auto k = tc_update_kernel<NB, MODE>;
     ALSK_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(P.total)));
     const int64_t nrows = re - rb;
     const unsigned grid = static_cast<unsigned>(std::min<int64_t>(nrows, num_sms()));
-    static const bool want_prof = std::getenv("ALSK_TC_PROF") != nullptr;
+    static const bool want_prof = measure_env("ALSK_TC_PROF") != nullptr;
     DevBuf prof;
     if (want_prof) {
         prof.alloc(sizeof(long long) * grid * NWARPS * 6, s);

@@ -55,7 +55,7 @@ class DeviceCsr:
         rp = torch.empty(rows + 1, dtype=torch.int64, device=device)
         ci = torch.empty(max(nnz, 1), dtype=torch.int32, device=device)
         va = torch.empty(max(nnz, 1), dtype=torch.float32, device=device)
-        _check(LIB.alsk_dev_load_cache(os.fsencode(path), rp.data_ptr(), ci.data_ptr(), va.data_ptr(),
+        _check(LIB.alsk_dev_load_cache(os.fsencode(path), rows, nnz, rp.data_ptr(), ci.data_ptr(), va.data_ptr(),
                                        stream_handle()))
         return DeviceCsr(rows, cols, rp, ci[:nnz], va[:nnz], device)
 
@@ -175,7 +175,7 @@ class AlsSession:
         if (rows, f) != want:
             raise InputError(f"{path}: checkpoint holds a {rows}x{f} factor, the run needs {want[0]}x{want[1]}")
         dst = self.X if which == FactorKind.x else self.T
-        _check(LIB.alsk_dev_checkpoint_read(os.fsencode(path), dst.data_ptr(), stream_handle()))
+        _check(LIB.alsk_dev_checkpoint_read(os.fsencode(path), rows * f, dst.data_ptr(), stream_handle()))
 
 
 class DeviceCheckpointWriter:

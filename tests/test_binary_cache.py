@@ -92,6 +92,7 @@ def _corrupt_files(A, tmp_path):
     bad = bytearray(raw); bad[ci_at(2):ci_at(2) + 4] = struct.pack("<i", 5); put("col_range", bad)
     bad = bytearray(raw); bad[ci_at(4):ci_at(4) + 4] = struct.pack("<i", -1); put("col_negative", bad)
     bad = bytearray(raw); bad[ci_at(1):ci_at(1) + 4] = struct.pack("<i", 1); put("col_order", bad)
+    bad = bytearray(raw); bad[24:32] = struct.pack("<Q", 1 << 31); put("cols_32bit", bad)
     return out
 
 
@@ -108,7 +109,24 @@ EXPECTED = {
     "col_range": "corrupt cache (column index 5 out of range in row 1)",
     "col_negative": "corrupt cache (column index -1 out of range in row 2)",
     "col_order": "corrupt cache (column indices must be strictly increasing within row 0)",
+    "cols_32bit": "corrupt cache (column count 2147483648 exceeds the 32-bit index range)",
 }
+
+
+def test_loader_never_writes_past_the_callers_buffers(A, tmp_path):
+    """The header is re-read by the load: a file that grew since the caller sized its buffers
+    (a replaced cache) is an IoError instead of an overrun."""
+    import ctypes as C
+    from paper_1603_03820_b200 import _native as N
+    big = random_matrix(A, 3, 40, 30, 300)
+    p = tmp_path / "r.cache"
+    A.save_binary_cache(big, p)
+    rp = np.zeros(11, np.int64)
+    ci = np.zeros(100, np.int32)
+    va = np.zeros(100, np.float32)
+    st = N.LIB.alsk_load_cache(str(p).encode(), 10, 100, rp.ctypes.data, ci.ctypes.data, va.ctypes.data)
+    assert st == 4 and "file changed since its header was read" in N.LIB.alsk_last_error().decode()
+    assert not rp.any() and not ci.any()
 
 
 def test_errors_are_io_errors_naming_the_file(A, tmp_path):

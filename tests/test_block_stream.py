@@ -84,8 +84,14 @@ def test_stream_errors_name_the_block(A, gpu, tmp_path):
     from paper_1603_03820_b200.session import DeviceBlockStream
     _, g, d = _grid(A, tmp_path)
     meta = A.load_grid_meta(d)
+    # an out-of-range block surfaces at the next() that would return it, after the blocks
+    # planned before it (BlockStream::next, dataio.hpp:498-506)
+    got = []
     with pytest.raises(A.InputError, match=r"block \(3, 0\) lies outside the 3x2 grid"):
-        DeviceBlockStream(d, [A.BlockRef(3, 0)])
+        with DeviceBlockStream(d, [A.BlockRef(0, 0), A.BlockRef(3, 0)]) as bs:
+            for ref, _ in bs:
+                got.append(ref)
+    assert got == [A.BlockRef(0, 0)]
     missing = A.block_path(d, 1, 1)
     import os
     os.remove(missing)
