@@ -475,7 +475,21 @@ def roofline(args, f, m, n, nz_x, nz_t, world, herm, solve, fused, coll, coll_by
     hbm = peaks.get("hbm_gbs")
     ffma = fp32_peak_probe() or 148 * 128 * 2 * 1.965e9 / 1e12
     herm_ms, herm_n = herm
-    if herm_n > 0 and f > 15:
+    if args.precision == "fp64":
+        # reference-order FP64 kernels (materialised A/B + exact solve): the Hermitian against
+        # the FP64 FMA peak (148 SMs x 64 DFMA x 2 flop x 1.965 GHz; no measured figure)
+        flops = steps * (nz_x + nz_t) * flops_per_nz
+        fp64 = 148 * 64 * 2 * 1.965e9 / 1e12
+        achieved = flops / (herm_ms * 1e-3) / 1e12 if herm_ms else None
+        roof = {"bound": "fp64", "kernel": "herm_mat_kernel<double> (reference-order FP64 Hermitian + bias)",
+                "achieved": achieved, "peak": fp64, "unit": "TFLOP/s",
+                "frac": achieved / fp64 if achieved else None,
+                "peak_source": "nominal FP64 FMA peak at the max SM clock (MEASURED_PEAKS.json has none)",
+                "traffic": None, "flops_per_launch": flops / max(herm_n, 1), "kernel_ms_avg": herm_ms / max(herm_n, 1),
+                "launches": int(herm_n), "kernel_share_of_step": (herm_ms / steps) / ms,
+                "solve": {"kernel": "solve_exact_kernel (reference-order FP64 Cholesky)",
+                          "ms_per_step": solve[0] / steps, "share_of_step": (solve[0] / steps) / ms}}
+    elif herm_n > 0 and f > 15:
         # tensor-core engine: Hermitian (tc_update_kernel) and batched Cholesky timed apart
         flops = steps * (nz_x + nz_t) * flops_per_nz
         achieved = flops / (herm_ms * 1e-3) / 1e12

@@ -200,12 +200,18 @@ void update_rows_device(const DevCsr& r, const float* theta, int64_t theta_rows,
     DevBuf A(sizeof(float) * chunk * f * f, s), B(sizeof(float) * chunk * f, s);
     for (int64_t b0 = rb; b0 < re; b0 += chunk) {
         const int64_t b1 = std::min(re, b0 + chunk);
-        hermitian_materialize(r, theta, f, lambda, exact, b0, b1, A.as<float>(), B.as<float>(), s);
+        {
+            PhaseTimer pt(PHASE_HERMITIAN, s);
+            hermitian_materialize(r, theta, f, lambda, exact, b0, b1, A.as<float>(), B.as<float>(), s);
+        }
         SolveStatus st = sb.st;
         st.column += (b0 - rb);
         st.pivot += (b0 - rb);
         // solve_exact reports launch-relative rows; shift by the batch offset
-        solve_exact(A.as<float>(), B.as<float>(), b1 - b0, f, false, x_out + (b0 - rb) * f, st, s);
+        {
+            PhaseTimer pt(PHASE_SOLVE, s);
+            solve_exact(A.as<float>(), B.as<float>(), b1 - b0, f, false, x_out + (b0 - rb) * f, st, s);
+        }
         unsigned long long bad = 0;
         d2h(&bad, sb.st.min_row, 1, s);
         ALSK_CUDA(cudaStreamSynchronize(s));

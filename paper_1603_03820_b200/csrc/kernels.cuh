@@ -107,6 +107,7 @@ bool packed_solve16(const float* packed, int64_t count, int f, float* x, const S
 bool packed_solve_tiles(const float* packed, int64_t count, int f, float* x, const SolveStatus& st,
                         int64_t status_off, cudaStream_t s);
 
+
 // Evaluation (solver.hpp:358-406). Deterministic two-level double reductions.
 double loss_device(const DevCsr& r, const int64_t* col_nnz, const float* x, const float* theta,
                    int f, double lambda, cudaStream_t s);

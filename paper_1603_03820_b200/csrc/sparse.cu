@@ -231,26 +231,30 @@ int bits_for(int64_t count) {  // bits to represent values in [0, count)
 }
 
 
-// ------------------------------------------------- single-pass counting-sort transpose ---
-// csr_to_csc as the reference does it (a stable counting sort, sparse.hpp:185-207), spread
-// over C chunks of consecutive nonzeros (one CTA each, one wave):
-//  tr_tile_rows  row of the first nonzero of every 2048-nonzero tile (binary search);
-//  tr_count      per-chunk column histogram in shared memory -> H[chunk][col];
-//  tr_colscan    per column, exclusive prefix of H over the chunks (in place) and the
-//                column totals -> col_ptr;
-//  tr_scatter    each chunk's running offsets off[c] = col_ptr[c] + H[chunk][c] live in
-//                shared memory; a staged tile is stably partitioned by owner warp
-//                (c mod 16), and each warp ranks its own columns in order (__match_any_sync,
-//                one read-modify-write of off[c] per distinct column), so entries of a
-//                column are placed in nonzero order, i.e. by ascending row — exactly the
-//                reference's output. Algorithmic traffic: col_idx read twice, values once,
-//                row_idx + values written once (~20 B per nonzero).
+// ------------------------------------------------ chunked counting-sort transpose ---
+// csr_to_csc as a stable LSD sort of the nonzeros by column in 8-bit digits (one pass when
+// n <= 256, two when n <= 65536), each pass a counting sort spread over C chunks of
+// consecutive elements (one CTA each, one wave):
+//  tr_tile_rows  row of the first nonzero of every tile (binary search), so pass 1 reads the
+//                CSR arrays directly (no packed copy of the matrix);
+//  tr_count      per-chunk digit histogram -> H[chunk][256] (pass 1 also counts the columns
+//                for col_ptr);
+//  tr_colscan    per digit, exclusive prefix of H over the chunks (in place) and the totals;
+//  tr_scatter    each chunk's running offsets live in shared memory; a staged tile is stably
+//                partitioned by owner warp (digit mod 16) and each warp ranks its digits in
+//                element order (__match_any_sync, one read-modify-write per distinct digit),
+//                so every pass is stable and the result is the reference's (rows ascending
+//                within a column). Each (chunk, digit) pair writes one contiguous run, so at
+//                most C x 256 partially written lines are live in L2 (a full-column counting
+//                sort would keep C x n of them and turn every write into a read-modify-write).
+// Pass 1 writes (next key byte, row, value) = 9 bytes per nonzero; pass 2 the final arrays.
 constexpr int kTrThreads = 512;
-constexpr int kTrWarps = kTrThreads / 32;  // owners: column mod 16
+constexpr int kTrWarps = kTrThreads / 32;  // owners: digit mod 16
 constexpr int kTrSub = 4;                  // staged elements per thread per tile
 constexpr int kTrTile = kTrThreads * kTrSub;
 constexpr int kTrSpan = 1024;              // row_ptr entries staged per tile (else global search)
-constexpr int kTrMaxCols = 44 * 1024;      // shared-memory offset table limit
+constexpr int kTrColHist = 44 * 1024;      // column histogram in shared memory up to this n
+constexpr int kDig = 256;
 
 __global__ void tr_tile_rows_kernel(const int64_t* __restrict__ row_ptr, int64_t rows, int64_t nnz,
                                     int64_t ntiles, int32_t* __restrict__ tile_row) {
@@ -266,28 +270,42 @@ __global__ void tr_tile_rows_kernel(const int64_t* __restrict__ row_ptr, int64_t
     }
 }
 
+// KEY8: keys are the u8 digits of a previous pass; else int32 columns (digit = low byte, and
+// with COLS the column histogram for col_ptr: shared memory when n fits, else global atomics)
+template <bool KEY8, bool COLS>
 __global__ void __launch_bounds__(kTrThreads)
-tr_count_kernel(const int32_t* __restrict__ col_idx, int64_t nnz, int64_t chunk, int n, uint32_t* __restrict__ H) {
-    extern __shared__ uint32_t hist[];
-    for (int c = threadIdx.x; c < n; c += blockDim.x) hist[c] = 0;
+tr_count_kernel(const void* __restrict__ keys, int64_t nnz, int64_t chunk, int n, uint32_t* __restrict__ H,
+                unsigned long long* __restrict__ colcnt) {
+    extern __shared__ uint32_t colhist[];
+    __shared__ uint32_t dig[kDig];
+    const bool smem_cols = COLS && n <= kTrColHist;
+    for (int d = threadIdx.x; d < kDig; d += blockDim.x) dig[d] = 0;
+    if (smem_cols)
+        for (int c = threadIdx.x; c < n; c += blockDim.x) colhist[c] = 0;
     __syncthreads();
     const int64_t e0 = blockIdx.x * chunk, e1 = std::min<int64_t>(nnz, e0 + chunk);
-    int64_t e = e0 + threadIdx.x;
-    for (; e + 3 * kTrThreads < e1; e += 4 * kTrThreads) {
-        const int c0 = __ldcs(col_idx + e), c1 = __ldcs(col_idx + e + kTrThreads);
-        const int c2 = __ldcs(col_idx + e + 2 * kTrThreads), c3 = __ldcs(col_idx + e + 3 * kTrThreads);
-        atomicAdd(hist + c0, 1u);
-        atomicAdd(hist + c1, 1u);
-        atomicAdd(hist + c2, 1u);
-        atomicAdd(hist + c3, 1u);
+    for (int64_t e = e0 + threadIdx.x; e < e1; e += kTrThreads) {
+        if constexpr (KEY8) {
+            atomicAdd(dig + __ldcs(static_cast<const uint8_t*>(keys) + e), 1u);
+        } else {
+            const int c = __ldcs(static_cast<const int32_t*>(keys) + e);
+            atomicAdd(dig + (c & (kDig - 1)), 1u);
+            if constexpr (COLS) {
+                if (smem_cols) atomicAdd(colhist + c, 1u);
+                else atomicAdd(colcnt + c, 1ull);
+            }
+        }
     }
-    for (; e < e1; e += kTrThreads) atomicAdd(hist + col_idx[e], 1u);
     __syncthreads();
-    uint32_t* out = H + static_cast<int64_t>(blockIdx.x) * n;
-    for (int c = threadIdx.x; c < n; c += blockDim.x) out[c] = hist[c];
+    uint32_t* out = H + static_cast<int64_t>(blockIdx.x) * kDig;
+    for (int d = threadIdx.x; d < kDig; d += blockDim.x) out[d] = dig[d];
+    if (smem_cols)
+        for (int c = threadIdx.x; c < n; c += blockDim.x)
+            if (colhist[c]) atomicAdd(colcnt + c, static_cast<unsigned long long>(colhist[c]));
 }
 
-// block (32 columns, 32 chunk groups)
+// block (32 digits, 32 chunk groups): per digit, exclusive prefix over the chunks in place
+// and the digit totals
 __global__ void tr_colscan_kernel(uint32_t* __restrict__ H, int nchunks, int n,
                                   unsigned long long* __restrict__ totals) {
     __shared__ uint32_t part[32][33];
@@ -321,6 +339,23 @@ __global__ void tr_colscan_kernel(uint32_t* __restrict__ H, int nchunks, int n,
     }
 }
 
+// exclusive scan of the 256 digit totals (one block)
+__global__ void tr_digit_base_kernel(const unsigned long long* __restrict__ totals, uint32_t* __restrict__ base) {
+    __shared__ unsigned long long v[kDig];
+    v[threadIdx.x] = totals[threadIdx.x];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long run = 0;
+        for (int d = 0; d < kDig; ++d) {
+            const unsigned long long x = v[d];
+            v[d] = run;
+            run += x;
+        }
+    }
+    __syncthreads();
+    base[threadIdx.x] = static_cast<uint32_t>(v[threadIdx.x]);
+}
+
 __device__ __forceinline__ int tr_row_search(const int64_t* __restrict__ rp, int lo, int hi, int64_t e) {
     while (lo < hi) {  // largest r in [lo, hi] with rp[r] <= e
         const int mid = (lo + hi + 1) >> 1;
@@ -329,43 +364,61 @@ __device__ __forceinline__ int tr_row_search(const int64_t* __restrict__ rp, int
     return lo;
 }
 
+// FROM_CSR: read (column, value) and the row (tile search) from the CSR arrays, digit = the
+// column's low byte; else read (key byte, row, value) of the previous pass. TO_FINAL: write
+// (row, value) to the CSC arrays; else (column's next byte, row, value) for the next pass.
+template <bool FROM_CSR, bool TO_FINAL>
 __global__ void __launch_bounds__(kTrThreads)
 tr_scatter_kernel(const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col_idx,
-                  const float* __restrict__ values, int64_t nnz, int64_t chunk, int n,
-                  const uint32_t* __restrict__ H, const int64_t* __restrict__ col_ptr,
-                  const int32_t* __restrict__ tile_row, int32_t* __restrict__ out_rows,
-                  float* __restrict__ out_vals) {
-    extern __shared__ __align__(16) unsigned char tr_smem[];
-    uint32_t* off = reinterpret_cast<uint32_t*>(tr_smem);                  // n
-    int32_t* s_col = reinterpret_cast<int32_t*>(off + ((n + 3) & ~3));     // kTrTile
-    int32_t* s_row = s_col + kTrTile;                                      // kTrTile
-    float* s_val = reinterpret_cast<float*>(s_row + kTrTile);              // kTrTile
-    int64_t* s_rp = reinterpret_cast<int64_t*>(s_val + kTrTile);           // kTrSpan + 1
+                  const uint8_t* __restrict__ key_in, const int32_t* __restrict__ row_in,
+                  const float* __restrict__ val_in, int64_t nnz, int64_t chunk, const uint32_t* __restrict__ H,
+                  const uint32_t* __restrict__ digit_base, const int32_t* __restrict__ tile_row,
+                  uint8_t* __restrict__ key_out, int32_t* __restrict__ row_out, float* __restrict__ val_out) {
+    __shared__ uint32_t off[kDig];
+    __shared__ uint8_t s_dig[kTrTile];
+    __shared__ uint8_t s_key[kTrTile];
+    __shared__ int32_t s_row[kTrTile];
+    __shared__ float s_val[kTrTile];
+    __shared__ int64_t s_rp[FROM_CSR ? kTrSpan + 2 : 1];
     __shared__ int s_cnt[kTrSub][kTrWarps][kTrWarps];  // [sub][warp][owner]
     __shared__ int s_olen[kTrWarps], s_ooff[kTrWarps];
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const unsigned lt = (1u << lane) - 1u;
-    const uint32_t* Hrow = H + static_cast<int64_t>(blockIdx.x) * n;
-    for (int c = threadIdx.x; c < n; c += blockDim.x) off[c] = static_cast<uint32_t>(col_ptr[c]) + Hrow[c];
+    const uint32_t* Hrow = H + static_cast<int64_t>(blockIdx.x) * kDig;
+    for (int d = threadIdx.x; d < kDig; d += blockDim.x) off[d] = digit_base[d] + Hrow[d];
     const int64_t e0 = blockIdx.x * chunk, e1 = std::min<int64_t>(nnz, e0 + chunk);
     __syncthreads();
     for (int64_t tb = e0; tb < e1; tb += kTrTile) {
         const int64_t t = tb / kTrTile;
-        const int ra = tile_row[t], rb = tile_row[t + 1];
-        const bool staged = rb - ra <= kTrSpan;
-        if (staged)
-            for (int i = threadIdx.x; i <= rb - ra + 1 && i <= kTrSpan; i += blockDim.x)
-                s_rp[i] = row_ptr[ra + i];
-        int c[kTrSub], o[kTrSub];
+        int ra = 0, rb = 0;
+        bool staged = false;
+        if constexpr (FROM_CSR) {
+            ra = tile_row[t];
+            rb = tile_row[t + 1];
+            staged = rb - ra <= kTrSpan;
+            if (staged)
+                for (int i = threadIdx.x; i <= rb - ra; i += blockDim.x) s_rp[i] = row_ptr[ra + i];
+        }
+        int d[kTrSub], o[kTrSub], kk[kTrSub], rw[kTrSub];
         float v[kTrSub];
 #pragma unroll
         for (int k = 0; k < kTrSub; ++k) {
             const int64_t e = tb + k * kTrThreads + threadIdx.x;
             const bool ok = e < e1;
-            c[k] = ok ? __ldcs(col_idx + e) : -1;
-            v[k] = ok ? __ldcs(values + e) : 0.f;
-            o[k] = ok ? (c[k] & (kTrWarps - 1)) : kTrWarps;
+            if constexpr (FROM_CSR) {
+                const int c = ok ? __ldcs(col_idx + e) : 0;
+                d[k] = c & (kDig - 1);
+                kk[k] = (c >> 8) & 255;
+                v[k] = ok ? __ldcs(val_in + e) : 0.f;
+                rw[k] = 0;
+            } else {
+                d[k] = ok ? __ldcs(key_in + e) : 0;
+                kk[k] = 0;
+                rw[k] = ok ? __ldcs(row_in + e) : 0;
+                v[k] = ok ? __ldcs(val_in + e) : 0.f;
+            }
+            o[k] = ok ? (d[k] & (kTrWarps - 1)) : kTrWarps;
         }
         // per (sub-tile, warp) counts of every owner; stable rank within the warp
         int rank[kTrSub];
@@ -396,9 +449,9 @@ tr_scatter_kernel(const int64_t* __restrict__ row_ptr, const int32_t* __restrict
             const int x = lane < kTrWarps ? s_olen[lane] : 0;
             int inc = x;
 #pragma unroll
-            for (int d = 1; d < 32; d <<= 1) {
-                const int y = __shfl_up_sync(0xffffffffu, inc, d);
-                if (lane >= d) inc += y;
+            for (int dd = 1; dd < 32; dd <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, inc, dd);
+                if (lane >= dd) inc += y;
             }
             if (lane < kTrWarps) s_ooff[lane] = inc - x;
         }
@@ -407,33 +460,36 @@ tr_scatter_kernel(const int64_t* __restrict__ row_ptr, const int32_t* __restrict
         for (int k = 0; k < kTrSub; ++k) {
             if (o[k] < kTrWarps) {
                 const int64_t e = tb + k * kTrThreads + threadIdx.x;
-                const int r = staged ? ra + tr_row_search(s_rp, 0, rb - ra, e)
-                                     : tr_row_search(row_ptr, ra, rb, e);  // (tr_row_search on global)
+                int r = rw[k];
+                if constexpr (FROM_CSR)
+                    r = staged ? ra + tr_row_search(s_rp, 0, rb - ra, e) : tr_row_search(row_ptr, ra, rb, e);
                 const int p = s_ooff[o[k]] + s_cnt[k][warp][o[k]] + rank[k];
-                s_col[p] = c[k];
+                s_dig[p] = static_cast<uint8_t>(d[k]);
+                s_key[p] = static_cast<uint8_t>(kk[k]);
                 s_row[p] = r;
                 s_val[p] = v[k];
             }
         }
         __syncthreads();
-        // warp `warp` places its columns, in element order
+        // warp `warp` places its digits, in element order
         const int len = s_olen[warp], base = s_ooff[warp];
         for (int j = 0; j < len; j += 32) {
             const int idx = j + lane;
             const bool ok = idx < len;
-            const int cc = ok ? s_col[base + idx] : -1 - lane;
-            const unsigned peers = __match_any_sync(0xffffffffu, cc);
+            const int dd = ok ? s_dig[base + idx] : -1 - lane;
+            const unsigned peers = __match_any_sync(0xffffffffu, dd);
             const int leader = __ffs(peers) - 1;
             uint32_t old = 0;
             if (ok && lane == leader) {
-                old = off[cc];
-                off[cc] = old + __popc(peers);
+                old = off[dd];
+                off[dd] = old + __popc(peers);
             }
             old = __shfl_sync(0xffffffffu, old, leader);
             if (ok) {
                 const uint32_t pos = old + __popc(peers & lt);
-                out_rows[pos] = s_row[base + idx];
-                out_vals[pos] = s_val[base + idx];
+                if constexpr (!TO_FINAL) key_out[pos] = s_key[base + idx];
+                row_out[pos] = s_row[base + idx];
+                val_out[pos] = s_val[base + idx];
             }
             __syncwarp();
         }
@@ -616,46 +672,56 @@ void csr_to_csc_radix(const DevCsr& a, int64_t* col_ptr, int32_t* row_idx, float
     ALSK_LAUNCHED();
 }
 
-// Single-pass counting-sort transpose when the column table fits shared memory and every
-// position fits 32 bits (all the named shapes' CSR -> CSC); the two-pass radix sort otherwise.
+// Counting-sort transpose for n <= 65536 columns and positions below 2^32 (every named
+// shape's CSR -> CSC); the radix sort of (column; row, value) pairs otherwise.
 bool csr_to_csc_counting(const DevCsr& a, int64_t* col_ptr, int32_t* row_idx, float* values, cudaStream_t s) {
     const int64_t n = a.cols, nnz = a.nnz;
-    if (n < 1 || n > kTrMaxCols || nnz >= (int64_t(1) << 32) || a.rows >= (int64_t(1) << 31) || nnz == 0)
-        return false;
-    const size_t smem_scatter = sizeof(uint32_t) * ((n + 3) & ~3) + sizeof(int32_t) * 3 * kTrTile +
-                                sizeof(int64_t) * (kTrSpan + 2);
-    cudaFuncAttributes fa{};
-    ALSK_CUDA(cudaFuncGetAttributes(&fa, tr_scatter_kernel));
-    if (smem_scatter + fa.sharedSizeBytes > 227 * 1024) return false;
-    ALSK_CUDA(cudaFuncSetAttribute(tr_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   static_cast<int>(smem_scatter)));
-    ALSK_CUDA(cudaFuncSetAttribute(tr_count_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   static_cast<int>(sizeof(uint32_t) * n)));
-    int occ = 0;
-    ALSK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, tr_scatter_kernel, kTrThreads, smem_scatter));
-    if (occ < 1) return false;
+    if (n < 1 || n > 65536 || nnz >= (int64_t(1) << 32) || a.rows >= (int64_t(1) << 31) || nnz == 0) return false;
+    const bool two = n > kDig;
     const int64_t ntiles_total = (nnz + kTrTile - 1) / kTrTile;
-    const int64_t want = static_cast<int64_t>(num_sms()) * occ;
+    int occ = 0;
+    ALSK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, tr_scatter_kernel<true, false>, kTrThreads, 0));
+    const int64_t want = static_cast<int64_t>(num_sms()) * std::max(occ, 1);
     const int64_t tiles_per_chunk = std::max<int64_t>(1, (ntiles_total + want - 1) / want);
     const int64_t chunk = tiles_per_chunk * kTrTile;
     const int nchunks = static_cast<int>((nnz + chunk - 1) / chunk);
     DevBuf tile_row(sizeof(int32_t) * (ntiles_total + 1), s);
-    DevBuf H(sizeof(uint32_t) * static_cast<size_t>(nchunks) * n, s);
-    DevBuf totals(sizeof(unsigned long long) * n, s);
+    DevBuf H(sizeof(uint32_t) * static_cast<size_t>(nchunks) * kDig, s);
+    DevBuf totals(sizeof(unsigned long long) * kDig, s), base(sizeof(uint32_t) * kDig, s);
+    DevBuf colcnt(sizeof(unsigned long long) * n, s);
+    ALSK_CUDA(cudaMemsetAsync(colcnt.as<void>(), 0, sizeof(unsigned long long) * n, s));
     tr_tile_rows_kernel<<<grid_for(ntiles_total + 1), 256, 0, s>>>(a.row_ptr, a.rows, nnz, ntiles_total,
                                                                    tile_row.as<int32_t>());
     ALSK_LAUNCHED();
-    tr_count_kernel<<<nchunks, kTrThreads, sizeof(uint32_t) * n, s>>>(a.col_idx, nnz, chunk, static_cast<int>(n),
-                                                                     H.as<uint32_t>());
-    ALSK_LAUNCHED();
-    tr_colscan_kernel<<<static_cast<unsigned>((n + 31) / 32), dim3(32, 32), 0, s>>>(
-        H.as<uint32_t>(), nchunks, static_cast<int>(n), totals.as<unsigned long long>());
-    ALSK_LAUNCHED();
-    exclusive_scan_ptr<unsigned long long>(totals.as<unsigned long long>(), n, col_ptr, s);
-    tr_scatter_kernel<<<nchunks, kTrThreads, smem_scatter, s>>>(a.row_ptr, a.col_idx, a.values, nnz, chunk,
-                                                                static_cast<int>(n), H.as<uint32_t>(), col_ptr,
-                                                                tile_row.as<int32_t>(), row_idx, values);
-    ALSK_LAUNCHED();
+    const size_t colsmem = n <= kTrColHist ? sizeof(uint32_t) * n : 0;
+    ALSK_CUDA(cudaFuncSetAttribute(tr_count_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   static_cast<int>(colsmem)));
+    auto digit_pass = [&](auto count_k, const void* keys, auto scatter_k, const uint8_t* key_in, const int32_t* row_in,
+                          const float* val_in, uint8_t* key_out, int32_t* row_out, float* val_out, size_t csm) {
+        count_k<<<nchunks, kTrThreads, csm, s>>>(keys, nnz, chunk, static_cast<int>(n), H.as<uint32_t>(),
+                                                 colcnt.as<unsigned long long>());
+        ALSK_LAUNCHED();
+        tr_colscan_kernel<<<kDig / 32, dim3(32, 32), 0, s>>>(H.as<uint32_t>(), nchunks, kDig,
+                                                              totals.as<unsigned long long>());
+        ALSK_LAUNCHED();
+        tr_digit_base_kernel<<<1, kDig, 0, s>>>(totals.as<unsigned long long>(), base.as<uint32_t>());
+        ALSK_LAUNCHED();
+        scatter_k<<<nchunks, kTrThreads, 0, s>>>(a.row_ptr, a.col_idx, key_in, row_in, val_in, nnz, chunk,
+                                                 H.as<uint32_t>(), base.as<uint32_t>(), tile_row.as<int32_t>(), key_out,
+                                                 row_out, val_out);
+        ALSK_LAUNCHED();
+    };
+    if (!two) {
+        digit_pass(tr_count_kernel<false, true>, a.col_idx, tr_scatter_kernel<true, true>, nullptr, nullptr, a.values,
+                   nullptr, row_idx, values, colsmem);
+    } else {
+        DevBuf k8(static_cast<size_t>(nnz), s), rw(sizeof(int32_t) * nnz, s), vl(sizeof(float) * nnz, s);
+        digit_pass(tr_count_kernel<false, true>, a.col_idx, tr_scatter_kernel<true, false>, nullptr, nullptr, a.values,
+                   k8.as<uint8_t>(), rw.as<int32_t>(), vl.as<float>(), colsmem);
+        digit_pass(tr_count_kernel<true, false>, k8.as<uint8_t>(), tr_scatter_kernel<false, true>, k8.as<uint8_t>(),
+                   rw.as<int32_t>(), vl.as<float>(), nullptr, row_idx, values, 0);
+    }
+    exclusive_scan_ptr<unsigned long long>(colcnt.as<unsigned long long>(), n, col_ptr, s);
     return true;
 }
 
