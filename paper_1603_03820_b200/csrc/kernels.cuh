@@ -106,6 +106,10 @@ bool packed_solve16(const float* packed, int64_t count, int f, float* x, const S
                     int64_t status_off, cudaStream_t s);
 bool packed_solve_tiles(const float* packed, int64_t count, int f, float* x, const SolveStatus& st,
                         int64_t status_off, cudaStream_t s);
+//  warp_solve         - one system per warp in shared memory, mma.sync Schur updates
+//                       (warp_solve.cu; the default); false if f is outside 1..128.
+bool warp_solve(const float* packed, int64_t count, int f, float* x, const SolveStatus& st, int64_t status_off,
+                cudaStream_t s);
 
 
 // Evaluation (solver.hpp:358-406). Deterministic two-level double reductions.

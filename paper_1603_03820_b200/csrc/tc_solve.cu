@@ -546,8 +546,11 @@ void launch_solve(const float* packed, int64_t count, int f, float* x, const Sol
 
 bool packed_solve(const float* packed, int64_t count, int f, float* x, const SolveStatus& st, int64_t status_off,
                   cudaStream_t s) {
-    static const bool tiles = measure_env("ALSK_SOLVE_TILES") != nullptr;  // A/B switch for measurements
-    if (tiles || f < 8 || f > 127) return packed_solve_tiles(packed, count, f, x, st, status_off, s);
+    static const bool tiles = measure_env("ALSK_SOLVE_TILES") != nullptr;  // A/B switches for measurements
+    static const bool tmem = measure_env("ALSK_SOLVE_TMEM") != nullptr;
+    if (tiles) return packed_solve_tiles(packed, count, f, x, st, status_off, s);
+    if (!tmem && warp_solve(packed, count, f, x, st, status_off, s)) return true;
+    if (f < 8 || f > 127) return packed_solve_tiles(packed, count, f, x, st, status_off, s);
     if (count <= 0) return true;
     static const int bw = [] {  // column-step width of the TMEM Cholesky (A/B switch)
         const char* e = measure_env("ALSK_TS_BW");
