@@ -7,9 +7,13 @@ point reports ALSK_ERR_CUDA when no device is present.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from pathlib import Path
 
-_LIB_PATH = Path(__file__).resolve().parent / "libalskit_cuda.so"
+# ALSK_MEASURE_LIB=1 loads the measurement build (build.py with ALSK_MEASURE=1: profiling
+# counters and A/B switches) instead of the product library.
+_LIB_PATH = Path(__file__).resolve().parent / (
+    "libalskit_cuda_measure.so" if os.environ.get("ALSK_MEASURE_LIB") == "1" else "libalskit_cuda.so")
 
 i64 = C.c_int64
 i32 = C.c_int32

@@ -28,9 +28,13 @@ NVCC_FLAGS = ARCH + [
 CXX_FLAGS = ["-O3", "-std=c++17", "-fPIC", "-pthread", f"-I{INCLUDE}", f"-I{CSRC}"]
 # ALSK_MEASURE=1 builds the measurement library (profiling counters, dry runs, A/B variants
 # read from the environment; csrc/measure.cuh). The product build ignores those switches.
+# It is built next to the product library (libalskit_cuda_measure.so, objects in
+# _build_measure) and loaded with ALSK_MEASURE_LIB=1.
 if os.environ.get("ALSK_MEASURE") == "1":
     NVCC_FLAGS.append("-DALSK_MEASURE")
     CXX_FLAGS.append("-DALSK_MEASURE")
+    BUILD = PKG / "_build_measure"
+    LIB = PKG / "libalskit_cuda_measure.so"
 
 
 def _headers_mtime() -> float:
