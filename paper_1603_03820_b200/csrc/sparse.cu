@@ -238,23 +238,27 @@ int bits_for(int64_t count) {  // bits to represent values in [0, count)
 //  tr_tile_rows  row of the first nonzero of every tile (binary search), so pass 1 reads the
 //                CSR arrays directly (no packed copy of the matrix);
 //  tr_count      per-chunk digit histogram -> H[chunk][256] (pass 1 also counts the columns
-//                for col_ptr);
+//                for col_ptr, and derives the digit histogram from them);
 //  tr_colscan    per digit, exclusive prefix of H over the chunks (in place) and the totals;
-//  tr_scatter    each chunk's running offsets live in shared memory; a staged tile is stably
-//                partitioned by owner warp (digit mod 16) and each warp ranks its digits in
-//                element order (__match_any_sync, one read-modify-write per distinct digit),
-//                so every pass is stable and the result is the reference's (rows ascending
-//                within a column). Each (chunk, digit) pair writes one contiguous run, so at
-//                most C x 256 partially written lines are live in L2 (a full-column counting
-//                sort would keep C x n of them and turn every write into a read-modify-write).
+//  tr_scatter    per tile of 4096 nonzeros (warp w: elements 256w .. 256w+255, lane l every
+//                32nd): every warp ranks its 8 rounds of digits in element order
+//                (__match_any_sync, one counter read-modify-write per distinct digit), one
+//                pass over the per-warp counters turns them into tile positions, the tile is
+//                stably sorted by digit in shared memory and written out in sorted order, so
+//                consecutive threads store consecutive positions of a digit's run. Stable in
+//                every pass: the result is the reference's (rows ascending within a column).
+//                Each (chunk, digit) pair writes one contiguous run, so at most C x 256
+//                partially written lines are live in L2 (a full-column counting sort would
+//                keep C x n of them and turn every write into a read-modify-write).
 // Pass 1 writes (next key byte, row, value) = 9 bytes per nonzero; pass 2 the final arrays.
 constexpr int kTrThreads = 512;
-constexpr int kTrWarps = kTrThreads / 32;  // owners: digit mod 16
-constexpr int kTrSub = 4;                  // staged elements per thread per tile
+constexpr int kTrWarps = kTrThreads / 32;
+constexpr int kTrSub = 8;                  // elements per thread per tile
 constexpr int kTrTile = kTrThreads * kTrSub;
 constexpr int kTrSpan = 1024;              // row_ptr entries staged per tile (else global search)
 constexpr int kTrColHist = 44 * 1024;      // column histogram in shared memory up to this n
 constexpr int kDig = 256;
+constexpr int kTrMaxChunkTiles = 1024;     // tiles per chunk (one wave of chunks: >= 4M nonzeros per chunk)
 
 __global__ void tr_tile_rows_kernel(const int64_t* __restrict__ row_ptr, int64_t rows, int64_t nnz,
                                     int64_t ntiles, int32_t* __restrict__ tile_row) {
@@ -270,35 +274,98 @@ __global__ void tr_tile_rows_kernel(const int64_t* __restrict__ row_ptr, int64_t
     }
 }
 
-// KEY8: keys are the u8 digits of a previous pass; else int32 columns (digit = low byte, and
-// with COLS the column histogram for col_ptr: shared memory when n fits, else global atomics)
-template <bool KEY8, bool COLS>
+// KEY8: keys are the u8 digits of a previous pass (per-warp private histograms); else int32
+// columns: the column histogram (shared memory when n fits, else global atomics) gives both
+// col_ptr's counts and, summed by low byte, the digit histogram
+template <bool KEY8, bool COLS, bool PACKED = false>
 __global__ void __launch_bounds__(kTrThreads)
 tr_count_kernel(const void* __restrict__ keys, int64_t nnz, int64_t chunk, int n, uint32_t* __restrict__ H,
                 unsigned long long* __restrict__ colcnt) {
     extern __shared__ uint32_t colhist[];
-    __shared__ uint32_t dig[kDig];
+    __shared__ uint32_t dig[kTrWarps][kDig];
     const bool smem_cols = COLS && n <= kTrColHist;
-    for (int d = threadIdx.x; d < kDig; d += blockDim.x) dig[d] = 0;
+    const int warp = threadIdx.x >> 5;
+    for (int d = threadIdx.x; d < kTrWarps * kDig; d += blockDim.x) (&dig[0][0])[d] = 0;
     if (smem_cols)
         for (int c = threadIdx.x; c < n; c += blockDim.x) colhist[c] = 0;
     __syncthreads();
     const int64_t e0 = blockIdx.x * chunk, e1 = std::min<int64_t>(nnz, e0 + chunk);
-    for (int64_t e = e0 + threadIdx.x; e < e1; e += kTrThreads) {
-        if constexpr (KEY8) {
-            atomicAdd(dig + __ldcs(static_cast<const uint8_t*>(keys) + e), 1u);
-        } else {
-            const int c = __ldcs(static_cast<const int32_t*>(keys) + e);
-            atomicAdd(dig + (c & (kDig - 1)), 1u);
-            if constexpr (COLS) {
-                if (smem_cols) atomicAdd(colhist + c, 1u);
-                else atomicAdd(colcnt + c, 1ull);
+    if constexpr (PACKED) {  // the key byte is the top byte of each 32-bit word
+        const uint32_t* kw = static_cast<const uint32_t*>(keys);
+        const int64_t a0 = std::min<int64_t>(e1, (e0 + 3) & ~int64_t(3)), a1 = std::max<int64_t>(a0, e1 & ~int64_t(3));
+        for (int64_t e = e0 + threadIdx.x; e < a0; e += kTrThreads) atomicAdd(&dig[warp][__ldcs(kw + e) >> 24], 1u);
+        for (int64_t e = a1 + threadIdx.x; e < e1; e += kTrThreads) atomicAdd(&dig[warp][__ldcs(kw + e) >> 24], 1u);
+        const uint4* k4 = reinterpret_cast<const uint4*>(kw + a0);
+        for (int64_t q = threadIdx.x; q < (a1 - a0) >> 2; q += kTrThreads) {
+            const uint4 w = __ldcs(k4 + q);
+            atomicAdd(&dig[warp][w.x >> 24], 1u);
+            atomicAdd(&dig[warp][w.y >> 24], 1u);
+            atomicAdd(&dig[warp][w.z >> 24], 1u);
+            atomicAdd(&dig[warp][w.w >> 24], 1u);
+        }
+    } else if constexpr (KEY8) {
+        const uint8_t* k8 = static_cast<const uint8_t*>(keys);
+        // 4 keys per 32-bit load where aligned
+        const int64_t a0 = std::min<int64_t>(e1, (e0 + 3) & ~int64_t(3)), a1 = std::max<int64_t>(a0, e1 & ~int64_t(3));
+        for (int64_t e = e0 + threadIdx.x; e < a0; e += kTrThreads) atomicAdd(&dig[warp][__ldcs(k8 + e)], 1u);
+        for (int64_t e = a1 + threadIdx.x; e < e1; e += kTrThreads) atomicAdd(&dig[warp][__ldcs(k8 + e)], 1u);
+        const uint32_t* k32 = reinterpret_cast<const uint32_t*>(k8 + a0);
+        for (int64_t q = threadIdx.x; q < (a1 - a0) >> 2; q += kTrThreads) {
+            const uint32_t w = __ldcs(k32 + q);
+            atomicAdd(&dig[warp][w & 255u], 1u);
+            atomicAdd(&dig[warp][(w >> 8) & 255u], 1u);
+            atomicAdd(&dig[warp][(w >> 16) & 255u], 1u);
+            atomicAdd(&dig[warp][w >> 24], 1u);
+        }
+    } else {
+        const int32_t* cols = static_cast<const int32_t*>(keys);
+        auto add = [&](int c) {
+            if (smem_cols) {
+                atomicAdd(colhist + c, 1u);
+            } else {
+                atomicAdd(&dig[warp][c & (kDig - 1)], 1u);
+                if constexpr (COLS) atomicAdd(colcnt + c, 1ull);
             }
+        };
+        // 16-byte loads, four in flight per thread (chunks start at multiples of the tile)
+        const int64_t a0 = std::min<int64_t>(e1, (e0 + 3) & ~int64_t(3)), a1 = std::max<int64_t>(a0, e1 & ~int64_t(3));
+        for (int64_t e = e0 + threadIdx.x; e < a0; e += kTrThreads) add(__ldcs(cols + e));
+        for (int64_t e = a1 + threadIdx.x; e < e1; e += kTrThreads) add(__ldcs(cols + e));
+        const int4* c4 = reinterpret_cast<const int4*>(cols + a0);
+        const int64_t nq = (a1 - a0) >> 2;
+        int64_t q = threadIdx.x;
+        for (; q + 3 * kTrThreads < nq; q += 4 * kTrThreads) {
+            int4 w[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) w[u] = __ldcs(c4 + q + u * kTrThreads);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                add(w[u].x);
+                add(w[u].y);
+                add(w[u].z);
+                add(w[u].w);
+            }
+        }
+        for (; q < nq; q += kTrThreads) {
+            const int4 w = __ldcs(c4 + q);
+            add(w.x);
+            add(w.y);
+            add(w.z);
+            add(w.w);
         }
     }
     __syncthreads();
     uint32_t* out = H + static_cast<int64_t>(blockIdx.x) * kDig;
-    for (int d = threadIdx.x; d < kDig; d += blockDim.x) out[d] = dig[d];
+    for (int d = threadIdx.x; d < kDig; d += blockDim.x) {
+        uint32_t v = 0;
+        if (!KEY8 && smem_cols) {
+            for (int c = d; c < n; c += kDig) v += colhist[c];
+        } else {
+#pragma unroll
+            for (int w = 0; w < kTrWarps; ++w) v += dig[w][d];
+        }
+        out[d] = v;
+    }
     if (smem_cols)
         for (int c = threadIdx.x; c < n; c += blockDim.x)
             if (colhist[c]) atomicAdd(colcnt + c, static_cast<unsigned long long>(colhist[c]));
@@ -364,134 +431,223 @@ __device__ __forceinline__ int tr_row_search(const int64_t* __restrict__ rp, int
     return lo;
 }
 
+struct TrSmem {
+    uint32_t wcnt[kTrWarps][kDig];  // per-warp digit counters, then their exclusive prefix over warps
+    uint32_t tstart[kDig];          // tile-local start of each digit
+    uint32_t gbase[kDig];           // global position of tile-local sorted index 0 of each digit's run
+    uint32_t off[kDig];             // the chunk's running global offset of each digit
+    uint32_t wsum[kDig / 32];
+    int32_t s_row[kTrTile];         // row (PACK: | next key byte << 24)
+    float s_val[kTrTile];
+    uint8_t s_dig[kTrTile];
+    uint8_t s_key[kTrTile];
+    int64_t s_rp[kTrSpan + 2];
+    int32_t s_trow[kTrMaxChunkTiles + 1];  // first row of each tile of the chunk
+};
+
 // FROM_CSR: read (column, value) and the row (tile search) from the CSR arrays, digit = the
 // column's low byte; else read (key byte, row, value) of the previous pass. TO_FINAL: write
 // (row, value) to the CSC arrays; else (column's next byte, row, value) for the next pass.
-template <bool FROM_CSR, bool TO_FINAL>
-__global__ void __launch_bounds__(kTrThreads)
+// PACK (rows < 2^24): the intermediate carries the key byte in the row's top byte.
+// The next tile's inputs are loaded into registers before the current tile's write-out.
+template <bool FROM_CSR, bool TO_FINAL, bool PACK>
+__global__ void __launch_bounds__(kTrThreads, 2)
 tr_scatter_kernel(const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col_idx,
                   const uint8_t* __restrict__ key_in, const int32_t* __restrict__ row_in,
                   const float* __restrict__ val_in, int64_t nnz, int64_t chunk, const uint32_t* __restrict__ H,
                   const uint32_t* __restrict__ digit_base, const int32_t* __restrict__ tile_row,
                   uint8_t* __restrict__ key_out, int32_t* __restrict__ row_out, float* __restrict__ val_out) {
-    __shared__ uint32_t off[kDig];
-    __shared__ uint8_t s_dig[kTrTile];
-    __shared__ uint8_t s_key[kTrTile];
-    __shared__ int32_t s_row[kTrTile];
-    __shared__ float s_val[kTrTile];
-    __shared__ int64_t s_rp[FROM_CSR ? kTrSpan + 2 : 1];
-    __shared__ int s_cnt[kTrSub][kTrWarps][kTrWarps];  // [sub][warp][owner]
-    __shared__ int s_olen[kTrWarps], s_ooff[kTrWarps];
-
+    extern __shared__ __align__(16) uint8_t tr_smem_raw[];
+    TrSmem& S = *reinterpret_cast<TrSmem*>(tr_smem_raw);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const unsigned lt = (1u << lane) - 1u;
     const uint32_t* Hrow = H + static_cast<int64_t>(blockIdx.x) * kDig;
-    for (int d = threadIdx.x; d < kDig; d += blockDim.x) off[d] = digit_base[d] + Hrow[d];
+    for (int d = threadIdx.x; d < kDig; d += blockDim.x) S.off[d] = digit_base[d] + Hrow[d];
     const int64_t e0 = blockIdx.x * chunk, e1 = std::min<int64_t>(nnz, e0 + chunk);
-    __syncthreads();
+    // this thread's elements of a tile: tb + 256 warp + 32 j + lane
+    int dg[kTrSub], kk[kTrSub], rw[kTrSub];
+    float v[kTrSub];
+    auto load = [&](int64_t tb) {
+        const int tcount = static_cast<int>(std::min<int64_t>(kTrTile, e1 - tb));
+#pragma unroll
+        for (int j = 0; j < kTrSub; ++j) {
+            const int i = 256 * warp + 32 * j + lane;
+            const int64_t e = tb + i;
+            const bool ok = i < tcount;
+            if constexpr (FROM_CSR) {
+                const int c = ok ? __ldcs(col_idx + e) : 0;
+                dg[j] = ok ? (c & (kDig - 1)) : -1 - lane;  // past the end: a digit of its own
+                kk[j] = (c >> 8) & 255;
+                v[j] = ok ? __ldcs(val_in + e) : 0.f;
+                rw[j] = 0;
+            } else if constexpr (PACK) {
+                const int32_t x = ok ? __ldcs(row_in + e) : 0;
+                dg[j] = ok ? static_cast<int>(static_cast<uint32_t>(x) >> 24) : -1 - lane;
+                kk[j] = 0;
+                rw[j] = x & 0xFFFFFF;
+                v[j] = ok ? __ldcs(val_in + e) : 0.f;
+            } else {
+                dg[j] = ok ? static_cast<int>(__ldcs(key_in + e)) : -1 - lane;
+                kk[j] = 0;
+                rw[j] = ok ? __ldcs(row_in + e) : 0;
+                v[j] = ok ? __ldcs(val_in + e) : 0.f;
+            }
+        }
+    };
+    // FROM_CSR: the tiles' first rows in shared memory, and each tile's row_ptr slice loaded
+    // into registers with its elements (two per thread), stored to shared memory at its start
+    constexpr int kRpPer = (kTrSpan + 2 + kTrThreads - 1) / kTrThreads;
+    int64_t rpv[kRpPer];
+    const int64_t t0 = e0 / kTrTile, nt = (e1 - e0 + kTrTile - 1) / kTrTile;
+    if constexpr (FROM_CSR) {
+        for (int64_t i = threadIdx.x; i <= nt; i += blockDim.x) S.s_trow[i] = tile_row[t0 + i];
+        __syncthreads();
+    }
+    auto load_rp = [&](int64_t ti) {
+        if constexpr (FROM_CSR) {
+            const int ra = S.s_trow[ti], rb = S.s_trow[ti + 1];
+#pragma unroll
+            for (int k = 0; k < kRpPer; ++k) {
+                const int i = threadIdx.x + k * kTrThreads;
+                rpv[k] = (rb - ra <= kTrSpan && i <= rb - ra + 1) ? row_ptr[ra + i] : 0;
+            }
+        }
+    };
+    if (e0 < e1) {
+        load(e0);
+        load_rp(0);
+    }
     for (int64_t tb = e0; tb < e1; tb += kTrTile) {
-        const int64_t t = tb / kTrTile;
+        const int tcount = static_cast<int>(std::min<int64_t>(kTrTile, e1 - tb));
         int ra = 0, rb = 0;
         bool staged = false;
         if constexpr (FROM_CSR) {
-            ra = tile_row[t];
-            rb = tile_row[t + 1];
+            const int64_t ti = (tb - e0) / kTrTile;
+            ra = S.s_trow[ti];
+            rb = S.s_trow[ti + 1];
             staged = rb - ra <= kTrSpan;
-            if (staged)
-                for (int i = threadIdx.x; i <= rb - ra; i += blockDim.x) s_rp[i] = row_ptr[ra + i];
-        }
-        int d[kTrSub], o[kTrSub], kk[kTrSub], rw[kTrSub];
-        float v[kTrSub];
+            if (staged) {
 #pragma unroll
-        for (int k = 0; k < kTrSub; ++k) {
-            const int64_t e = tb + k * kTrThreads + threadIdx.x;
-            const bool ok = e < e1;
-            if constexpr (FROM_CSR) {
-                const int c = ok ? __ldcs(col_idx + e) : 0;
-                d[k] = c & (kDig - 1);
-                kk[k] = (c >> 8) & 255;
-                v[k] = ok ? __ldcs(val_in + e) : 0.f;
-                rw[k] = 0;
-            } else {
-                d[k] = ok ? __ldcs(key_in + e) : 0;
-                kk[k] = 0;
-                rw[k] = ok ? __ldcs(row_in + e) : 0;
-                v[k] = ok ? __ldcs(val_in + e) : 0.f;
+                for (int k = 0; k < kRpPer; ++k) {
+                    const int i = threadIdx.x + k * kTrThreads;
+                    if (i <= rb - ra + 1) S.s_rp[i] = rpv[k];
+                }
             }
-            o[k] = ok ? (d[k] & (kTrWarps - 1)) : kTrWarps;
         }
-        // per (sub-tile, warp) counts of every owner; stable rank within the warp
+#pragma unroll
+        for (int d = lane; d < kDig; d += 32) S.wcnt[warp][d] = 0;
+        __syncthreads();  // row_ptr staged, counters zeroed (and the previous tile fully written)
+        // per-warp stable ranks, rounds in element order; peers = lanes with the same digit,
+        // from 8 bit ballots (MATCH.ANY measured as the kernel's main stall)
         int rank[kTrSub];
 #pragma unroll
-        for (int k = 0; k < kTrSub; ++k) {
-            const unsigned peers = __match_any_sync(0xffffffffu, o[k]);
-            rank[k] = __popc(peers & lt);
+        for (int j = 0; j < kTrSub; ++j) {
+            unsigned peers = __ballot_sync(0xffffffffu, dg[j] >= 0);
+            if (dg[j] < 0) peers = 1u << lane;
 #pragma unroll
-            for (int w = 0; w < kTrWarps; ++w) {
-                const unsigned b = __ballot_sync(0xffffffffu, o[k] == w);
-                if (lane == w) s_cnt[k][warp][w] = __popc(b);
+            for (int bit = 0; bit < 8; ++bit) {
+                const bool set = (dg[j] >> bit) & 1;
+                const unsigned bb = __ballot_sync(0xffffffffu, set);
+                peers &= set ? bb : ~bb;
             }
-        }
-        __syncthreads();
-        if (threadIdx.x < kTrWarps) {  // owner ow: exclusive scan over (sub-tile, warp) in element order
-            const int ow = threadIdx.x;
-            int run = 0;
-            for (int k = 0; k < kTrSub; ++k)
-                for (int w = 0; w < kTrWarps; ++w) {
-                    const int x = s_cnt[k][w][ow];
-                    s_cnt[k][w][ow] = run;
-                    run += x;
-                }
-            s_olen[ow] = run;
-        }
-        __syncthreads();
-        if (warp == 0) {
-            const int x = lane < kTrWarps ? s_olen[lane] : 0;
-            int inc = x;
-#pragma unroll
-            for (int dd = 1; dd < 32; dd <<= 1) {
-                const int y = __shfl_up_sync(0xffffffffu, inc, dd);
-                if (lane >= dd) inc += y;
-            }
-            if (lane < kTrWarps) s_ooff[lane] = inc - x;
-        }
-        __syncthreads();
-#pragma unroll
-        for (int k = 0; k < kTrSub; ++k) {
-            if (o[k] < kTrWarps) {
-                const int64_t e = tb + k * kTrThreads + threadIdx.x;
-                int r = rw[k];
-                if constexpr (FROM_CSR)
-                    r = staged ? ra + tr_row_search(s_rp, 0, rb - ra, e) : tr_row_search(row_ptr, ra, rb, e);
-                const int p = s_ooff[o[k]] + s_cnt[k][warp][o[k]] + rank[k];
-                s_dig[p] = static_cast<uint8_t>(d[k]);
-                s_key[p] = static_cast<uint8_t>(kk[k]);
-                s_row[p] = r;
-                s_val[p] = v[k];
-            }
-        }
-        __syncthreads();
-        // warp `warp` places its digits, in element order
-        const int len = s_olen[warp], base = s_ooff[warp];
-        for (int j = 0; j < len; j += 32) {
-            const int idx = j + lane;
-            const bool ok = idx < len;
-            const int dd = ok ? s_dig[base + idx] : -1 - lane;
-            const unsigned peers = __match_any_sync(0xffffffffu, dd);
             const int leader = __ffs(peers) - 1;
             uint32_t old = 0;
-            if (ok && lane == leader) {
-                old = off[dd];
-                off[dd] = old + __popc(peers);
+            if (lane == leader && dg[j] >= 0) {
+                old = S.wcnt[warp][dg[j]];
+                S.wcnt[warp][dg[j]] = old + __popc(peers);
             }
             old = __shfl_sync(0xffffffffu, old, leader);
-            if (ok) {
-                const uint32_t pos = old + __popc(peers & lt);
-                if constexpr (!TO_FINAL) key_out[pos] = s_key[base + idx];
-                row_out[pos] = s_row[base + idx];
-                val_out[pos] = s_val[base + idx];
-            }
+            rank[j] = static_cast<int>(old) + __popc(peers & lt);
             __syncwarp();
+        }
+        __syncthreads();
+        // digit d = thread: exclusive prefix of its counters over the warps, tile start of the
+        // digit (block scan of the totals), global base of its run
+        if (threadIdx.x < kDig) {
+            const int d = threadIdx.x;
+            uint32_t c[kTrWarps];
+#pragma unroll
+            for (int w = 0; w < kTrWarps; ++w) c[w] = S.wcnt[w][d];
+            uint32_t run = 0;
+#pragma unroll
+            for (int w = 0; w < kTrWarps; ++w) {
+                const uint32_t x = c[w];
+                S.wcnt[w][d] = run;
+                run += x;
+            }
+            uint32_t inc = run;  // inclusive scan of the totals over the digits
+#pragma unroll
+            for (int dd = 1; dd < 32; dd <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, inc, dd);
+                if (lane >= dd) inc += y;
+            }
+            if (lane == 31) S.wsum[warp] = inc;
+            S.tstart[d] = inc - run;  // within the warp's 32 digits for now
+        }
+        __syncthreads();
+        if (threadIdx.x < kDig) {
+            const int d = threadIdx.x;
+            uint32_t pre = 0;
+            for (int w = 0; w < warp; ++w) pre += S.wsum[w];
+            const uint32_t st = S.tstart[d] + pre;
+            S.tstart[d] = st;
+            S.gbase[d] = S.off[d] - st;
+        }
+        __syncthreads();
+        // stable sort of the tile by digit in shared memory; rows: the row of each element
+        // follows its predecessor's (+32 elements), two probes then a binary search
+        int r = ra;
+        if constexpr (FROM_CSR) {
+            const int64_t e = tb + 256 * warp + lane;
+            if (256 * warp + lane < tcount)
+                r = staged ? ra + tr_row_search(S.s_rp, 0, rb - ra, e) : tr_row_search(row_ptr, ra, rb, e);
+        }
+#pragma unroll
+        for (int j = 0; j < kTrSub; ++j) {
+            if (dg[j] >= 0) {
+                const int i = 256 * warp + 32 * j + lane;
+                if constexpr (FROM_CSR) {
+                    const int64_t e = tb + i;
+                    if (j > 0) {
+                        if (staged) {
+                            const int lr = r - ra;
+                            if (S.s_rp[lr + 1] <= e)
+                                r = S.s_rp[lr + 2] > e ? r + 1 : ra + tr_row_search(S.s_rp, lr + 2, rb - ra, e);
+                        } else {
+                            r = tr_row_search(row_ptr, r, rb, e);
+                        }
+                    }
+                    rw[j] = r;
+                }
+                const int p = static_cast<int>(S.tstart[dg[j]] + S.wcnt[warp][dg[j]]) + rank[j];
+                S.s_dig[p] = static_cast<uint8_t>(dg[j]);
+                if constexpr (PACK && !TO_FINAL) {
+                    S.s_row[p] = rw[j] | (kk[j] << 24);
+                } else {
+                    S.s_key[p] = static_cast<uint8_t>(kk[j]);
+                    S.s_row[p] = rw[j];
+                }
+                S.s_val[p] = v[j];
+            }
+        }
+        __syncthreads();
+        if (tb + kTrTile < e1) {  // in flight during the write-out
+            load(tb + kTrTile);
+            load_rp((tb - e0) / kTrTile + 1);
+        }
+        // write-out in sorted order: consecutive threads, consecutive positions of a run
+        for (int i = threadIdx.x; i < tcount; i += kTrThreads) {
+            const int d = S.s_dig[i];
+            const uint32_t pos = S.gbase[d] + static_cast<uint32_t>(i);
+            if constexpr (!TO_FINAL && !PACK) key_out[pos] = S.s_key[i];
+            row_out[pos] = S.s_row[i];
+            val_out[pos] = S.s_val[i];
+        }
+        // the chunk's running offsets move past this tile (counts = next digit start - start)
+        if (threadIdx.x < kDig) {
+            const int d = threadIdx.x;
+            const uint32_t nxt = d == kDig - 1 ? static_cast<uint32_t>(tcount) : S.tstart[d + 1];
+            S.off[d] += nxt - S.tstart[d];
         }
         __syncthreads();
     }
@@ -679,10 +835,18 @@ bool csr_to_csc_counting(const DevCsr& a, int64_t* col_ptr, int32_t* row_idx, fl
     if (n < 1 || n > 65536 || nnz >= (int64_t(1) << 32) || a.rows >= (int64_t(1) << 31) || nnz == 0) return false;
     const bool two = n > kDig;
     const int64_t ntiles_total = (nnz + kTrTile - 1) / kTrTile;
+    const int ssm = static_cast<int>(sizeof(TrSmem));
+    const bool pack = a.rows < (int64_t(1) << 24);  // the pass-1 key byte rides in the row's top byte
+    ALSK_CUDA(cudaFuncSetAttribute(tr_scatter_kernel<true, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, ssm));
+    ALSK_CUDA(cudaFuncSetAttribute(tr_scatter_kernel<true, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, ssm));
+    ALSK_CUDA(cudaFuncSetAttribute(tr_scatter_kernel<true, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, ssm));
+    ALSK_CUDA(cudaFuncSetAttribute(tr_scatter_kernel<false, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, ssm));
+    ALSK_CUDA(cudaFuncSetAttribute(tr_scatter_kernel<false, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, ssm));
     int occ = 0;
-    ALSK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, tr_scatter_kernel<true, false>, kTrThreads, 0));
+    ALSK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, tr_scatter_kernel<true, false, false>, kTrThreads, ssm));
     const int64_t want = static_cast<int64_t>(num_sms()) * std::max(occ, 1);
-    const int64_t tiles_per_chunk = std::max<int64_t>(1, (ntiles_total + want - 1) / want);
+    const int64_t tiles_per_chunk = std::min<int64_t>(kTrMaxChunkTiles,
+                                                      std::max<int64_t>(1, (ntiles_total + want - 1) / want));
     const int64_t chunk = tiles_per_chunk * kTrTile;
     const int nchunks = static_cast<int>((nnz + chunk - 1) / chunk);
     DevBuf tile_row(sizeof(int32_t) * (ntiles_total + 1), s);
@@ -706,20 +870,26 @@ bool csr_to_csc_counting(const DevCsr& a, int64_t* col_ptr, int32_t* row_idx, fl
         ALSK_LAUNCHED();
         tr_digit_base_kernel<<<1, kDig, 0, s>>>(totals.as<unsigned long long>(), base.as<uint32_t>());
         ALSK_LAUNCHED();
-        scatter_k<<<nchunks, kTrThreads, 0, s>>>(a.row_ptr, a.col_idx, key_in, row_in, val_in, nnz, chunk,
+        scatter_k<<<nchunks, kTrThreads, ssm, s>>>(a.row_ptr, a.col_idx, key_in, row_in, val_in, nnz, chunk,
                                                  H.as<uint32_t>(), base.as<uint32_t>(), tile_row.as<int32_t>(), key_out,
                                                  row_out, val_out);
         ALSK_LAUNCHED();
     };
     if (!two) {
-        digit_pass(tr_count_kernel<false, true>, a.col_idx, tr_scatter_kernel<true, true>, nullptr, nullptr, a.values,
-                   nullptr, row_idx, values, colsmem);
+        digit_pass(tr_count_kernel<false, true>, a.col_idx, tr_scatter_kernel<true, true, false>, nullptr, nullptr,
+                   a.values, nullptr, row_idx, values, colsmem);
+    } else if (pack) {
+        DevBuf rw(sizeof(int32_t) * nnz, s), vl(sizeof(float) * nnz, s);
+        digit_pass(tr_count_kernel<false, true>, a.col_idx, tr_scatter_kernel<true, false, true>, nullptr, nullptr,
+                   a.values, nullptr, rw.as<int32_t>(), vl.as<float>(), colsmem);
+        digit_pass(tr_count_kernel<true, false, true>, rw.as<int32_t>(), tr_scatter_kernel<false, true, true>, nullptr,
+                   rw.as<int32_t>(), vl.as<float>(), nullptr, row_idx, values, 0);
     } else {
         DevBuf k8(static_cast<size_t>(nnz), s), rw(sizeof(int32_t) * nnz, s), vl(sizeof(float) * nnz, s);
-        digit_pass(tr_count_kernel<false, true>, a.col_idx, tr_scatter_kernel<true, false>, nullptr, nullptr, a.values,
-                   k8.as<uint8_t>(), rw.as<int32_t>(), vl.as<float>(), colsmem);
-        digit_pass(tr_count_kernel<true, false>, k8.as<uint8_t>(), tr_scatter_kernel<false, true>, k8.as<uint8_t>(),
-                   rw.as<int32_t>(), vl.as<float>(), nullptr, row_idx, values, 0);
+        digit_pass(tr_count_kernel<false, true>, a.col_idx, tr_scatter_kernel<true, false, false>, nullptr, nullptr,
+                   a.values, k8.as<uint8_t>(), rw.as<int32_t>(), vl.as<float>(), colsmem);
+        digit_pass(tr_count_kernel<true, false>, k8.as<uint8_t>(), tr_scatter_kernel<false, true, false>,
+                   k8.as<uint8_t>(), rw.as<int32_t>(), vl.as<float>(), nullptr, row_idx, values, 0);
     }
     exclusive_scan_ptr<unsigned long long>(colcnt.as<unsigned long long>(), n, col_ptr, s);
     return true;
