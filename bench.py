@@ -510,9 +510,11 @@ def roofline(args, f, m, n, nz_x, nz_t, world, herm, solve, fused, coll, coll_by
                 "gather": {"bytes_per_launch": hbytes / herm_n, "achieved": hbytes / (herm_ms * 1e-3) / 1e9,
                            "peak": hbm, "unit": "GB/s",
                            "frac": hbytes / (herm_ms * 1e-3) / 1e9 / hbm if hbm else None},
-                "solve": {"kernel": "tc_solve_kernel (TMEM-resident Cholesky, tensor-core rank-8 updates)",
+                "solve": {"kernel": "warp_solve_kernel (one system per warp in shared memory, mma.sync tf32x2 "
+                                    "Schur updates)",
                           "ms_per_step": solve[0] / steps, "launches": int(solve[1]),
                           "achieved_tflops": solve_flops / (solve[0] * 1e-3) / 1e12 if solve[0] else None,
+                          "packed_rows_gbs": steps * rows * pk_row / (solve[0] * 1e-3) / 1e9 if solve[0] else None,
                           "share_of_step": (solve[0] / steps) / ms}}
     else:
         # register/FFMA engines (f <= 15 here): HBM-bound gather, SURVEY.md §8(d)

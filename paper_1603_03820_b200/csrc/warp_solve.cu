@@ -487,11 +487,11 @@ warp_solve_kernel(const float* __restrict__ packed, int64_t count, int f, float*
                     if (32 * q >= k0) break;  // warp-uniform: no lane of this slice is above the block
                     const bool upd = lane + 32 * q < k0;
                     const float* p = buf + (upd ? lbase[q] + 8 * k0 : 0);
-                    float s0 = xv[q], s1 = 0.f;  // two chains
-#pragma unroll
+                    float s0 = xv[q], s1 = 0.f;  // two chains; rows k0+c >= f do not exist
+#pragma unroll                                       // (their cells may hold anything: masked, not 0*x)
                     for (int c = 0; c < 8; c += 2) {
-                        s0 = fmaf(-p[8 * c], xb[c], s0);
-                        s1 = fmaf(-p[8 * c + 8], xb[c + 1], s1);
+                        s0 = fmaf(c < nreal ? -p[8 * c] : 0.f, xb[c], s0);
+                        s1 = fmaf(c + 1 < nreal ? -p[8 * c + 8] : 0.f, xb[c + 1], s1);
                     }
                     xv[q] = upd ? s0 + s1 : xv[q];
                 }
