@@ -13,6 +13,7 @@
 #include <vector>
 
 #include "alskit_cuda.h"
+#include "measure.cuh"
 #include "kernels.cuh"
 #include "cache_io.cuh"
 #include "checkpoint_io.cuh"
@@ -360,7 +361,7 @@ alsk_status alsk_batch_solve(const float* a, const float* b, int64_t count, int 
 }
 
 // update_x on host buffers (solver.hpp:330-345), pipelined: the rows are split into
-// PIPE_BATCHES ranges; each range's col_idx/values go host->device on a copy stream while the
+// ranges (kPipeCuts); each range's col_idx/values go host->device on a copy stream while the
 // previous range computes, and each solved range of X goes back while the next computes.
 // Only row_ptr and the gathered factor must be resident before the first range starts.
 alsk_status alsk_update_x(const alsk_csr* r, const float* theta, int64_t theta_rows, int f,
@@ -397,6 +398,34 @@ alsk_status alsk_update_x(const alsk_csr* r, const float* theta, int64_t theta_r
                 cudaStreamSynchronize(s);
             }
         } drain{c, s};
+#ifdef ALSK_MEASURE
+        // ALSK_E2E_PROF=1: timeline of this call's copy and compute streams (stderr)
+        static const bool e2e_prof = measure_env("ALSK_E2E_PROF") != nullptr;
+        std::vector<std::pair<const char*, cudaEvent_t>> tl;
+        auto mark = [&](const char* what, cudaStream_t on) {
+            if (!e2e_prof) return;
+            cudaEvent_t e;
+            ALSK_CUDA(cudaEventCreate(&e));
+            ALSK_CUDA(cudaEventRecord(e, on));
+            tl.emplace_back(what, e);
+        };
+        mark("start", s);
+        auto dump = [&] {
+            if (!e2e_prof || tl.empty()) return;
+            std::fprintf(stderr, "[e2e-prof m=%lld nnz=%lld]", static_cast<long long>(m), static_cast<long long>(nnz));
+            for (auto& [w, e] : tl) {
+                float ms = 0.f;
+                ALSK_CUDA(cudaEventElapsedTime(&ms, tl[0].second, e));
+                std::fprintf(stderr, " %s@%.2f", w, ms);
+            }
+            for (auto& [w, e] : tl) ALSK_CUDA(cudaEventDestroy(e));
+            tl.clear();
+            std::fprintf(stderr, "\n");
+        };
+#else
+        auto mark = [](const char*, cudaStream_t) {};
+        auto dump = [] {};
+#endif
         cudaEvent_t allocated = evs.make();
         ALSK_CUDA(cudaEventRecord(allocated, s));
         ALSK_CUDA(cudaStreamWaitEvent(c, allocated, 0));
@@ -404,16 +433,30 @@ alsk_status alsk_update_x(const alsk_csr* r, const float* theta, int64_t theta_r
         h2d(T.as<float>(), theta, theta_rows * f, c);
         cudaEvent_t base = evs.make();
         ALSK_CUDA(cudaEventRecord(base, c));
-        constexpr int64_t PIPE_BATCHES = 8;
-        const int64_t nb = std::min<int64_t>(PIPE_BATCHES, m);
+        // Ranges cut at these fractions of the nonzeros (sizes 1,2,3,5,8,12,12,10,6,3,2 / 64):
+        // H2D (~56 GB/s) outruns the compute (~1.7x), so once a range computes the next one is
+        // staged as long as sizes grow by less than that; only the first range's upload and
+        // the last range's download are exposed, and both are small.
+        static constexpr double kPipeCuts[] = {0.0, 1.0 / 64, 3.0 / 64, 6.0 / 64, 11.0 / 64, 19.0 / 64, 31.0 / 64,
+                                               43.0 / 64, 53.0 / 64, 59.0 / 64, 62.0 / 64, 1.0};
+        constexpr int kPipeRanges = sizeof(kPipeCuts) / sizeof(kPipeCuts[0]) - 1;
+        std::vector<int64_t> cut{0};
+        for (int k = 1; k < kPipeRanges; ++k) {
+            const int64_t want = static_cast<int64_t>(kPipeCuts[k] * static_cast<double>(nnz));
+            const int64_t row = std::lower_bound(r->row_ptr, r->row_ptr + m + 1, want) - r->row_ptr;
+            if (row > cut.back() && row < m) cut.push_back(row);
+        }
+        cut.push_back(m);
+        const int64_t nb = static_cast<int64_t>(cut.size()) - 1;
         std::vector<cudaEvent_t> staged(nb);
         for (int64_t k = 0; k < nb; ++k) {
-            const int64_t b0 = m * k / nb, b1 = m * (k + 1) / nb;
+            const int64_t b0 = cut[k], b1 = cut[k + 1];
             const int64_t k0 = r->row_ptr[b0], k1 = r->row_ptr[b1];
             h2d(CI.as<int32_t>() + k0, r->col_idx + k0, k1 - k0, c);
             h2d(V.as<float>() + k0, r->values + k0, k1 - k0, c);
             staged[k] = evs.make();
             ALSK_CUDA(cudaEventRecord(staged[k], c));
+            mark("c:staged", c);
         }
         DevCsr view;
         view.rows = m;
@@ -425,18 +468,82 @@ alsk_status alsk_update_x(const alsk_csr* r, const float* theta, int64_t theta_r
         view.values = V.as<float>();
         ALSK_CUDA(cudaStreamWaitEvent(s, base, 0));
         const alsk_precision prec = cfg->accumulate_double != 0 ? ALSK_PREC_FP64_EXACT : ALSK_PREC_FP32;
+        if (prec == ALSK_PREC_FP32 && use_tensor_cores(prec, f)) {
+            // Tensor-core path without host synchronisation between ranges: a packed-row
+            // scratch owned by this call (stream-ordered pool), the column check running
+            // asynchronously ahead of each range (the Hermitian clamps its gather index, so a
+            // bad column never reads outside Theta), breakdown status per range; errors are
+            // resolved once at the end in the reference's order (batch by batch: a batch's
+            // column check precedes its solve, solver.hpp:120-123 and 230-235).
+            const int64_t br = cfg->batch_rows < 1 ? 1 : cfg->batch_rows;
+            int64_t maxr = 1;
+            for (int64_t k = 0; k < nb; ++k) maxr = std::max(maxr, cut[k + 1] - cut[k]);
+            const size_t pkn = static_cast<size_t>(packed_stride(f)) * 4;
+            const int64_t cap = std::max<int64_t>(1, static_cast<int64_t>((size_t(4096) << 20) / pkn));
+            DevBuf SC(pkn * static_cast<size_t>(std::min(maxr, cap)), s);
+            const Scratch ext{SC.as<float>(), SC.bytes()};
+            DevBuf flag(sizeof(unsigned long long), s), mins(sizeof(unsigned long long) * nb, s);
+            DevBuf col(sizeof(int32_t) * m, s), piv(sizeof(double) * m, s);
+            ALSK_CUDA(cudaMemsetAsync(flag.as<void>(), 0xff, sizeof(unsigned long long), s));
+            ALSK_CUDA(cudaMemsetAsync(mins.as<void>(), 0xff, sizeof(unsigned long long) * nb, s));
+            const int64_t col_lo = r->col_offset, col_hi = r->col_offset + theta_rows;
+            for (int64_t k = 0; k < nb; ++k) {
+                const int64_t b0 = cut[k], b1 = cut[k + 1];
+                ALSK_CUDA(cudaStreamWaitEvent(s, staged[k], 0));
+                mark("s:range-start", s);
+                check_columns_async(view, r->row_ptr[b0], r->row_ptr[b1], col_lo, col_hi,
+                                    flag.as<unsigned long long>(), s);
+                SolveStatus st{mins.as<unsigned long long>() + k, col.as<int32_t>() + b0, piv.as<double>() + b0};
+                update_tc(view, T.as<float>(), theta_rows, f, static_cast<float>(cfg->lambda), b0, b1,
+                          X.as<float>() + b0 * f, st, s, &ext);
+                mark("s:range-end", s);
+                cudaEvent_t solved = evs.make();
+                ALSK_CUDA(cudaEventRecord(solved, s));
+                ALSK_CUDA(cudaStreamWaitEvent(c, solved, 0));
+                d2h(x_out + b0 * f, X.as<float>() + b0 * f, (b1 - b0) * f, c);
+            }
+            unsigned long long bad = 0;
+            std::vector<unsigned long long> mh(nb);
+            d2h(&bad, flag.as<unsigned long long>(), 1, s);
+            d2h(mh.data(), mins.as<unsigned long long>(), nb, s);
+            mark("c:end", c);
+            ALSK_CUDA(cudaStreamSynchronize(c));
+            ALSK_CUDA(cudaStreamSynchronize(s));
+            dump();
+            int64_t rc = -1, rbk = -1;
+            if (bad != ~0ull)  // the row holding the first bad nonzero
+                rc = std::upper_bound(r->row_ptr, r->row_ptr + m + 1, static_cast<int64_t>(bad)) - r->row_ptr - 1;
+            for (int64_t k = 0; k < nb && rbk < 0; ++k)
+                if (mh[k] != ~0ull) rbk = cut[k] + static_cast<int64_t>(mh[k]);
+            if (rc >= 0 && (rbk < 0 || rc / br <= rbk / br)) fail_bad_column(view, bad, col_lo, col_hi, s);
+            if (rbk >= 0) {
+                int32_t cc = 0;
+                double pv = 0.0;
+                d2h(&cc, col.as<int32_t>() + rbk, 1, s);
+                d2h(&pv, piv.as<double>() + rbk, 1, s);
+                ALSK_CUDA(cudaStreamSynchronize(s));
+                t_breakdown = rbk % br;
+                fail_numerical("cholesky breakdown at batch index " + std::to_string(rbk % br) + " (pivot " +
+                               std::to_string(pv) + " at column " + std::to_string(cc - 1) + ")");
+            }
+            return;
+        }
         for (int64_t k = 0; k < nb; ++k) {
-            const int64_t b0 = m * k / nb, b1 = m * (k + 1) / nb;
+            const int64_t b0 = cut[k], b1 = cut[k + 1];
             ALSK_CUDA(cudaStreamWaitEvent(s, staged[k], 0));
+            mark("s:range-start", s);
             update_rows_device(view, T.as<float>(), theta_rows, f, cfg->lambda, prec, cfg->batch_rows, b0, b1,
                                X.as<float>() + b0 * f, s);
+            mark("s:range-end", s);
             cudaEvent_t solved = evs.make();
             ALSK_CUDA(cudaEventRecord(solved, s));
             ALSK_CUDA(cudaStreamWaitEvent(c, solved, 0));
             d2h(x_out + b0 * f, X.as<float>() + b0 * f, (b1 - b0) * f, c);
         }
+        mark("c:end", c);
         ALSK_CUDA(cudaStreamSynchronize(c));
         ALSK_CUDA(cudaStreamSynchronize(s));  // the buffers are freed (stream-ordered) on s
+        dump();
     });
 }
 

@@ -226,6 +226,23 @@ __global__ void solve_exact_kernel(const float* __restrict__ A, const float* __r
 
 }  // namespace
 
+void check_columns_async(const DevCsr& r, int64_t kb, int64_t ke, int64_t col_lo, int64_t col_hi,
+                         unsigned long long* first_bad, cudaStream_t s) {
+    if (ke <= kb) return;
+    const int64_t n = ke - kb;
+    const int grid = static_cast<int>(std::min<int64_t>((n + 255) / 256, num_sms() * 8));
+    check_columns_kernel<<<grid, 256, 0, s>>>(r.row_ptr, r.col_idx, kb, ke, col_lo, col_hi, first_bad);
+    ALSK_LAUNCHED();
+}
+
+void fail_bad_column(const DevCsr& r, unsigned long long entry, int64_t col_lo, int64_t col_hi, cudaStream_t s) {
+    int32_t v = 0;
+    d2h(&v, r.col_idx + entry, 1, s);
+    ALSK_CUDA(cudaStreamSynchronize(s));
+    fail_input("column " + std::to_string(v) + " outside partition [" + std::to_string(col_lo) + ", " +
+               std::to_string(col_hi) + ")");
+}
+
 void check_columns(const DevCsr& r, int64_t rb, int64_t re, int64_t col_lo, int64_t col_hi,
                    cudaStream_t s) {
     if (re <= rb) return;
@@ -244,13 +261,7 @@ void check_columns(const DevCsr& r, int64_t rb, int64_t re, int64_t col_lo, int6
     unsigned long long bad = 0;
     d2h(&bad, flag.as<unsigned long long>(), 1, s);
     ALSK_CUDA(cudaStreamSynchronize(s));
-    if (bad != ~0ull) {
-        int32_t v = 0;
-        d2h(&v, r.col_idx + bad, 1, s);
-        ALSK_CUDA(cudaStreamSynchronize(s));
-        fail_input("column " + std::to_string(v) + " outside partition [" + std::to_string(col_lo) +
-                   ", " + std::to_string(col_hi) + ")");
-    }
+    if (bad != ~0ull) fail_bad_column(r, bad, col_lo, col_hi, s);
 }
 
 namespace {

@@ -31,6 +31,12 @@ struct SolveStatus {
 // reference's message (solver.hpp:120-123) naming the first offending entry.
 void check_columns(const DevCsr& r, int64_t rb, int64_t re, int64_t col_lo, int64_t col_hi,
                    cudaStream_t s);
+// The same check of nonzeros [kb, ke) without host synchronisation: the first offending
+// nonzero is atomicMin'ed into *first_bad (init ~0); fail_bad_column raises its message.
+void check_columns_async(const DevCsr& r, int64_t kb, int64_t ke, int64_t col_lo, int64_t col_hi,
+                         unsigned long long* first_bad, cudaStream_t s);
+[[noreturn]] void fail_bad_column(const DevCsr& r, unsigned long long entry, int64_t col_lo, int64_t col_hi,
+                                  cudaStream_t s);
 
 // Materialised assembly (A full mirrored f*f floats + B f floats per row), rows [rb,re).
 // acc_double: reference-order double accumulation (bit-exact with assemble_mo_rows<double>).

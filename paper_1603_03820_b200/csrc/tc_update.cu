@@ -207,7 +207,7 @@ enum { MODE_FULL = 1, MODE_PACKED = 2 };
 template <int NB, int MODE>
 __global__ void __launch_bounds__(NTHREADS, 1)
 tc_update_kernel(const float* __restrict__ theta, int ldt, const int64_t* __restrict__ row_ptr,
-                 const int32_t* __restrict__ col_idx, const float* __restrict__ values, int64_t col_lo, int f,
+                 const int32_t* __restrict__ col_idx, const float* __restrict__ values, int64_t col_lo, int theta_last, int f,
                  float lambda, int64_t rb, int64_t nrows, int stages, float* __restrict__ out_a,
                  float* __restrict__ out_b, long long* __restrict__ prof, int hls, uint32_t epi_sleep,
                  uint32_t load_sleep, uint32_t split_sleep, uint32_t mma_sleep, uint32_t dry) {
@@ -305,7 +305,9 @@ tc_update_kernel(const float* __restrict__ theta, int ldt, const int64_t* __rest
                 if (done) break;
                 const uint32_t ctr = ctr0 + d;
                 const ChunkInfo ci = qi[d];
-                const int v = qc[d] - static_cast<int>(col_lo);
+                // never gather outside Theta: an out-of-partition column is reported by the
+                // caller's column check (solver.hpp:120-123), possibly after this launch
+                const int v = min(max(qc[d] - static_cast<int>(col_lo), 0), theta_last);
                 const float rv = qv[d];
                 qi[d] = w.info();
                 qc[d] = 0;
@@ -639,7 +641,8 @@ void launch_tc(const DevCsr& r, const float* theta, int64_t theta_rows, int f, i
         prof.alloc(sizeof(long long) * grid * NWARPS * 6, s);
         ALSK_CUDA(cudaMemsetAsync(prof.as<void>(), 0, sizeof(long long) * grid * NWARPS * 6, s));
     }
-    k<<<grid, NTHREADS, P.total, s>>>(theta, ldt, r.row_ptr, r.col_idx, r.values, r.col_offset, f, lambda, rb, nrows, stages,
+    k<<<grid, NTHREADS, P.total, s>>>(theta, ldt, r.row_ptr, r.col_idx, r.values, r.col_offset,
+                                       static_cast<int>(std::max<int64_t>(theta_rows, 1) - 1), f, lambda, rb, nrows, stages,
                                        a, b, want_prof ? prof.as<long long>() : nullptr, hls, sleeps[0], sleeps[1],
                                        sleeps[2], sleeps[3], dry);
     ALSK_LAUNCHED();

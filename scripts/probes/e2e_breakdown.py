@@ -65,3 +65,64 @@ d2h = wall(lambda: X.copy_(dX, non_blocking=True))
 print(f"alsk_update_x {ux:.1f} ms | alsk_update_theta {ut:.1f} ms | sum {ux + ut:.1f} ms")
 print(f"H2D X-half inputs {bx / 1e9:.3f} GB in {cx:.1f} ms ({bx / cx / 1e6:.1f} GB/s); "
       f"Theta-half inputs {bt / 1e9:.3f} GB in {ct:.1f} ms ({bt / ct / 1e6:.1f} GB/s); D2H X {X.nbytes / d2h / 1e6:.1f} GB/s")
+
+# device-resident X half (alsk_dev_update, default scratch), alone, in 9 ranges, and with a
+# concurrent pinned H2D stream of the same bytes
+from paper_1603_03820_b200.session import PREC_FP32, dev_update  # noqa: E402
+
+Td = theta_h.to(dev)
+Xd = torch.empty(m * f, dtype=torch.float32, device=dev)
+cuts = [0] + [int(np.searchsorted(rp.numpy(), c * x.nnz)) for c in (1 / 64, 1 / 16, 3 / 16, 6 / 16, 9 / 16, 12 / 16,
+                                                                      15 / 16, 63 / 64)] + [m]
+one = wall(lambda: dev_update(x, Td, n, f, lam, PREC_FP32, Xd))
+ranged = wall(lambda: [dev_update(x, Td, n, f, lam, PREC_FP32, Xd[a * f:], a, b) for a, b in zip(cuts[:-1], cuts[1:])])
+cs = torch.cuda.Stream()
+
+
+def with_copy():
+    with torch.cuda.stream(cs):
+        h2d([rp, ci, vv], dx)
+    dev_update(x, Td, n, f, lam, PREC_FP32, Xd)
+
+
+both = wall(with_copy)
+print(f"device X half: one call {one:.1f} ms | 9 ranges {ranged:.1f} ms | one call + concurrent H2D {both:.1f} ms")
+
+
+def ranged_with_copy():
+    with torch.cuda.stream(cs):
+        for _ in range(3):
+            h2d([rp, ci, vv], dx)
+    for a, b in zip(cuts[:-1], cuts[1:]):
+        dev_update(x, Td, n, f, lam, PREC_FP32, Xd[a * f:], a, b)
+
+
+def ev_time(fn):
+    ts = []
+    for _ in range(reps + 1):
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        fn(e1)
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    return float(np.median(ts[1:]))
+
+
+def ranged_with_copy_ev(e1):
+    with torch.cuda.stream(cs):
+        for _ in range(3):
+            h2d([rp, ci, vv], dx)
+    for a, b in zip(cuts[:-1], cuts[1:]):
+        dev_update(x, Td, n, f, lam, PREC_FP32, Xd[a * f:], a, b)
+    e1.record()
+
+
+def ranged_ev(e1):
+    for a, b in zip(cuts[:-1], cuts[1:]):
+        dev_update(x, Td, n, f, lam, PREC_FP32, Xd[a * f:], a, b)
+    e1.record()
+
+
+print(f"device X half in 9 ranges, compute stream only: alone {ev_time(ranged_ev):.1f} ms, "
+      f"with 3 concurrent H2D passes {ev_time(ranged_with_copy_ev):.1f} ms")
