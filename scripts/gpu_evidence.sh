@@ -1,7 +1,8 @@
 #!/bin/bash
 # Round-2 evidence in one gpurun call: GPU tests, smoke, the bench (FP32 and the FP64-exact
 # drop-in default), the ncu launch list of the benched step, ncu --set full of the benched
-# tensor-core Hermitian (X and Theta halves) and batched Cholesky, compute-sanitizer logs.
+# tensor-core Hermitian (X and Theta halves) and the warp Cholesky, the transpose launch list
+# and timings, compute-sanitizer logs.
 set -u
 cd "${GRAFT_REPO_ROOT:-$(dirname "$0")/..}"
 mkdir -p gpurun_out
@@ -22,9 +23,14 @@ if [[ $S == *ncu* ]]; then
   timeout 900 $NCU --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 200 --csv \
      --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu > gpurun_out/ncu_bench.log 2>&1
   echo "ncu launches exit $?" >> gpurun_out/status.txt
-  timeout 1200 $NCU --set full --clock-control none --import-source on -k regex:"tc_update|tc_solve" -c 3 \
+  timeout 1200 $NCU --set full --clock-control none --import-source on -k regex:"tc_update|warp_solve" -c 3 \
      -o gpurun_out/prof_tc python scripts/prof_step.py netflix 1 > gpurun_out/ncu_full.log 2>&1
   echo "ncu full exit $?" >> gpurun_out/status.txt
+  timeout 600 $NCU --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
+     -k regex:tr_ --csv --log-file gpurun_out/tr_launches.csv python scripts/probe_transpose.py netflix 1 > /dev/null 2>&1
+  timeout 600 python scripts/probe_transpose.py netflix 5 > gpurun_out/tr_netflix.json 2>&1
+  timeout 900 python scripts/probe_transpose.py hugewiki 3 > gpurun_out/tr_hugewiki.json 2>&1
+  echo "transpose exit $?" >> gpurun_out/status.txt
 fi
 if [[ $S == *san* ]]; then
   for tool in memcheck racecheck synccheck initcheck; do

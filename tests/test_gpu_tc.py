@@ -239,3 +239,32 @@ def test_tc_partial_hermitian_f32_grid_block(A, orc, gpu):
         a, b = unpack_panel_blocked(total[u], f)
         assert np.abs(a - ao[u]).max() <= 1e-5 * max(np.abs(ao[u]).max(), 1e-30), u
         assert np.abs(b - bo[u]).max() <= 1e-5 * max(np.abs(bo[u]).max(), 1e-30), u
+
+
+@pytest.mark.parametrize("batch_rows", [4096, 2])
+def test_tc_error_order_matches_reference(A, ref, gpu, batch_rows):
+    """A bad column and a Cholesky breakdown in one update_x on host buffers: the reference
+    assembles a whole batch (column check, solver.hpp:120-123) before solving it
+    (solver.hpp:230-235), so whichever batch comes first decides the error; the sync-free
+    host path resolves its deferred checks in that order. Row 1 breaks down (one rating,
+    lambda < 0), row 2 holds column 25 outside the block's partition [4, 20)."""
+    f = 16
+    th = np.eye(f, dtype=np.float32)
+    rp = np.array([0, f, f + 1, f + 3, 2 * f + 3], np.int64)
+    ci = np.concatenate([np.arange(4, 20), [5], [6, 25], np.arange(4, 20)]).astype(np.int32)
+    vals = np.ones(len(ci), np.float32)
+    r = A.CsrMatrix(4, 30, 4, rp, ci, vals)
+    cfg = A.SolverConfig(f=f, lambda_=-0.05, accumulate_double=False, batch_rows=batch_rows)
+    st, _ = ref.update_x(binding.csr_struct(4, 30, rp, ci, vals, 4), th.ravel(), f, f, -0.05, acc_double=0,
+                         batch_rows=batch_rows)
+    assert st != 0
+    msg = ref.last_error()
+    with A.use_fp32_engine("tensor"):
+        with pytest.raises(A.Error) as e:
+            A.update_x(r, A.FactorMatrix(f, f, th.ravel()), cfg)
+    if batch_rows == 4096:
+        assert "column 25 outside partition [4, 20)" in msg and isinstance(e.value, A.InputError)
+        assert str(e.value) == msg
+    else:
+        assert "cholesky breakdown at batch index 1" in msg and isinstance(e.value, A.NumericalError)
+        assert str(e.value).startswith("cholesky breakdown at batch index 1")
