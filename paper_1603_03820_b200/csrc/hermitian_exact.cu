@@ -141,6 +141,7 @@ __global__ void solve_exact_kernel(const float* __restrict__ A, const float* __r
     double* L = sm;                        // f(f+1)/2
     double* s = L + f * (f + 1) / 2;       // f
     float* xs = reinterpret_cast<float*>(s + f);
+    uint8_t* tri = reinterpret_cast<uint8_t*>(xs + f);  // (i, j) of the (f-1)-triangle, row-major
     __shared__ int s_flag;
     __shared__ int s_broke;
     const int64_t row = blockIdx.x;
@@ -162,6 +163,11 @@ __global__ void solve_exact_kernel(const float* __restrict__ A, const float* __r
         for (int j = 0; j <= i; ++j) L[pk(i, j)] = static_cast<double>(a[i * f + j]);
         s[i] = static_cast<double>(b[i]);
     }
+    for (int i = tid; i < f - 1; i += nt)
+        for (int j = 0; j <= i; ++j) {
+            tri[2 * pk(i, j)] = static_cast<uint8_t>(i);
+            tri[2 * pk(i, j) + 1] = static_cast<uint8_t>(j);
+        }
     __syncthreads();
 
     for (int c = 0; c < f; ++c) {
@@ -185,12 +191,16 @@ __global__ void solve_exact_kernel(const float* __restrict__ A, const float* __r
         const double lcc = L[pk(c, c)];
         for (int r = c + 1 + tid; r < f; r += nt) L[pk(r, c)] = __ddiv_rn(L[pk(r, c)], lcc);
         __syncthreads();
-        // trailing update, entry (r, q) with c < q <= r: warps over rows, lanes over q
-        const int warp = tid >> 5, lane = tid & 31, nw = nt >> 5;
-        for (int r = c + 1 + warp; r < f; r += nw) {
-            const double lrc = L[pk(r, c)];
-            for (int q = c + 1 + lane; q <= r; q += 32)
-                L[pk(r, q)] = __dsub_rn(L[pk(r, q)], __dmul_rn(lrc, L[pk(q, c)]));
+        // trailing update of entries (r, q), c < q <= r, enumerated flat over the threads
+        // (row-major lower triangle: entry k of the (f-c-1)-triangle is tri[k]; the first
+        // T(T+1)/2 entries of the largest triangle are exactly the smaller ones), so short
+        // rows leave no lanes idle. Each entry still takes its updates in ascending c, one
+        // separately rounded multiply-subtract per column: the reference's order.
+        const int T = f - c - 1, nent = T * (T + 1) / 2;
+        for (int k = tid; k < nent; k += nt) {
+            const int r = c + 1 + tri[2 * k], q = c + 1 + tri[2 * k + 1];
+            const int rb = r * (r + 1) / 2;
+            L[rb + q] = __dsub_rn(L[rb + q], __dmul_rn(L[rb + c], L[q * (q + 1) / 2 + c]));
         }
         __syncthreads();
     }
@@ -307,8 +317,9 @@ void solve_exact(const float* A, const float* B, int64_t count, int f, bool /*ze
                  float* X, const SolveStatus& st, cudaStream_t s) {
     // Both policies write a zero row for a broken system; the host raises for `fail`.
     if (count <= 0) return;
-    const size_t smem = (static_cast<size_t>(f) * (f + 1) / 2 + f) * sizeof(double) + f * sizeof(float) + 16;
-    if (smem > 220 * 1024) fail_input("rank " + std::to_string(f) + " too large for device solve");
+    const size_t smem = (static_cast<size_t>(f) * (f + 1) / 2 + f) * sizeof(double) + f * sizeof(float) +
+                        static_cast<size_t>(f) * (f - 1) + 16;  // + the (f-1)-triangle's (i, j) bytes
+    if (f > 256 || smem > 220 * 1024) fail_input("rank " + std::to_string(f) + " too large for device solve");
     ALSK_CUDA(cudaFuncSetAttribute(solve_exact_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const int threads = f <= 32 ? 32 : (f <= 64 ? 64 : 128);
     for (int64_t b0 = 0; b0 < count; b0 += (1LL << 30)) {
