@@ -433,6 +433,7 @@ __device__ __forceinline__ int tr_row_search(const int64_t* __restrict__ rp, int
 
 struct TrSmem {
     uint32_t wcnt[kTrWarps][kDig];  // per-warp digit counters, then their exclusive prefix over warps
+    uint32_t match[kTrWarps][kDig]; // per-warp peer masks of the current round (zero between rounds)
     uint32_t tstart[kDig];          // tile-local start of each digit
     uint32_t gbase[kDig];           // global position of tile-local sorted index 0 of each digit's run
     uint32_t off[kDig];             // the chunk's running global offset of each digit
@@ -463,6 +464,7 @@ tr_scatter_kernel(const int64_t* __restrict__ row_ptr, const int32_t* __restrict
     const unsigned lt = (1u << lane) - 1u;
     const uint32_t* Hrow = H + static_cast<int64_t>(blockIdx.x) * kDig;
     for (int d = threadIdx.x; d < kDig; d += blockDim.x) S.off[d] = digit_base[d] + Hrow[d];
+    for (int d = lane; d < kDig; d += 32) S.match[warp][d] = 0u;
     const int64_t e0 = blockIdx.x * chunk, e1 = std::min<int64_t>(nnz, e0 + chunk);
     // this thread's elements of a tile: tb + 256 warp + 32 j + lane
     int dg[kTrSub], kk[kTrSub], rw[kTrSub];
@@ -538,23 +540,23 @@ tr_scatter_kernel(const int64_t* __restrict__ row_ptr, const int32_t* __restrict
         for (int d = lane; d < kDig; d += 32) S.wcnt[warp][d] = 0;
         __syncthreads();  // row_ptr staged, counters zeroed (and the previous tile fully written)
         // per-warp stable ranks, rounds in element order; peers = lanes with the same digit,
-        // from 8 bit ballots (MATCH.ANY measured as the kernel's main stall)
+        // matched through a per-warp mask per digit in shared memory (atomic OR of the lane
+        // bits, read back, reset by the leader): ~a dozen instructions per element, where
+        // MATCH.ANY stalled on the MIO queue and 8 bit-ballots cost ~45
+        uint32_t* mm = S.match[warp];
         int rank[kTrSub];
 #pragma unroll
         for (int j = 0; j < kTrSub; ++j) {
-            unsigned peers = __ballot_sync(0xffffffffu, dg[j] >= 0);
-            if (dg[j] < 0) peers = 1u << lane;
-#pragma unroll
-            for (int bit = 0; bit < 8; ++bit) {
-                const bool set = (dg[j] >> bit) & 1;
-                const unsigned bb = __ballot_sync(0xffffffffu, set);
-                peers &= set ? bb : ~bb;
-            }
+            if (dg[j] >= 0) atomicOr(&mm[dg[j]], 1u << lane);
+            __syncwarp();
+            const unsigned peers = dg[j] >= 0 ? mm[dg[j]] : (1u << lane);
+            __syncwarp();
             const int leader = __ffs(peers) - 1;
             uint32_t old = 0;
             if (lane == leader && dg[j] >= 0) {
                 old = S.wcnt[warp][dg[j]];
                 S.wcnt[warp][dg[j]] = old + __popc(peers);
+                mm[dg[j]] = 0u;
             }
             old = __shfl_sync(0xffffffffu, old, leader);
             rank[j] = static_cast<int>(old) + __popc(peers & lt);
