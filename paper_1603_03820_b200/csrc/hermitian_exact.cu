@@ -10,9 +10,11 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdio>
 #include <string>
 
 #include "kernels.cuh"
+#include "measure.cuh"
 
 namespace alsk {
 namespace {
@@ -136,7 +138,19 @@ __device__ __forceinline__ int pk(int i, int j) { return i * (i + 1) / 2 + j; }
 __global__ void solve_exact_kernel(const float* __restrict__ A, const float* __restrict__ Bv,
                                    int f, int64_t row_base, float* __restrict__ X,
                                    unsigned long long* __restrict__ min_row,
-                                   int32_t* __restrict__ column, double* __restrict__ pivot) {
+                                   int32_t* __restrict__ column, double* __restrict__ pivot,
+                                   unsigned long long* __restrict__ prof) {
+#ifdef ALSK_MEASURE
+    long long t_lap = clock64();  // ALSK_SE_PROF=1: cycles per phase (thread 0), measurement builds
+#define SE_LAP(slot)                                                    \
+    if (prof && threadIdx.x == 0) {                                     \
+        const long long now_ = clock64();                               \
+        atomicAdd(prof + (slot), static_cast<unsigned long long>(now_ - t_lap)); \
+        t_lap = now_;                                                   \
+    }
+#else
+#define SE_LAP(slot)
+#endif
     extern __shared__ double sm[];
     double* L = sm;                        // f(f+1)/2
     double* s = L + f * (f + 1) / 2;       // f
@@ -170,6 +184,7 @@ __global__ void solve_exact_kernel(const float* __restrict__ A, const float* __r
         }
     __syncthreads();
 
+    SE_LAP(0)
     for (int c = 0; c < f; ++c) {
         if (tid == 0) {
             const double d = L[pk(c, c)];
@@ -204,6 +219,7 @@ __global__ void solve_exact_kernel(const float* __restrict__ A, const float* __r
         }
         __syncthreads();
     }
+    SE_LAP(1)
     if (s_broke) {
         for (int i = tid; i < f; i += nt) x[i] = 0.0f;
         return;
@@ -219,6 +235,7 @@ __global__ void solve_exact_kernel(const float* __restrict__ A, const float* __r
             for (int i = j + 1 + tid; i < f; i += 32) s[i] = __dsub_rn(s[i], __dmul_rn(L[pk(i, j)], yj));
             __syncwarp();
         }
+        SE_LAP(2)
         // back substitution reads the already-rounded float x[j] (solver.hpp:254-259);
         // its order (j ascending from i+1) is inherently sequential.
         if (tid == 0) {
@@ -230,8 +247,10 @@ __global__ void solve_exact_kernel(const float* __restrict__ A, const float* __r
             }
         }
         __syncwarp();
+        SE_LAP(3)
         for (int i = tid; i < f; i += 32) x[i] = xs[i];
     }
+#undef SE_LAP
 }
 
 }  // namespace
@@ -324,11 +343,25 @@ void solve_exact(const float* A, const float* B, int64_t count, int f, bool /*ze
     const int threads = f <= 32 ? 32 : (f <= 64 ? 64 : 128);
     for (int64_t b0 = 0; b0 < count; b0 += (1LL << 30)) {
         const int64_t n = std::min<int64_t>(count - b0, 1LL << 30);
+        static const bool want_prof = measure_env("ALSK_SE_PROF") != nullptr;
+        DevBuf pb;
+        if (want_prof) {
+            pb.alloc(4 * sizeof(unsigned long long), s);
+            ALSK_CUDA(cudaMemsetAsync(pb.as<void>(), 0, 4 * sizeof(unsigned long long), s));
+        }
         solve_exact_kernel<<<static_cast<unsigned>(n), threads, smem, s>>>(
             A + static_cast<size_t>(b0) * f * f, B + static_cast<size_t>(b0) * f, f,
             b0, X + static_cast<size_t>(b0) * f, st.min_row, st.column + b0,
-            st.pivot + b0);
+            st.pivot + b0, want_prof ? pb.as<unsigned long long>() : nullptr);
         ALSK_LAUNCHED();
+        if (want_prof) {
+            unsigned long long h[4];
+            d2h(h, pb.as<unsigned long long>(), 4, s);
+            ALSK_CUDA(cudaStreamSynchronize(s));
+            std::fprintf(stderr, "[se-prof f=%d systems=%lld threads=%d] kcyc per system: load %.1f factor %.1f forward %.1f back %.1f\n",
+                         f, static_cast<long long>(n), threads, h[0] / 1e3 / n, h[1] / 1e3 / n, h[2] / 1e3 / n,
+                         h[3] / 1e3 / n);
+        }
     }
 }
 
