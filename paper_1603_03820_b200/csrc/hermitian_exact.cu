@@ -156,8 +156,6 @@ __global__ void solve_exact_kernel(const float* __restrict__ A, const float* __r
     double* s = L + f * (f + 1) / 2;       // f
     float* xs = reinterpret_cast<float*>(s + f);
     uint8_t* tri = reinterpret_cast<uint8_t*>(xs + f);  // (i, j) of the (f-1)-triangle, row-major
-    __shared__ int s_flag;
-    __shared__ int s_broke;
     const int64_t row = blockIdx.x;
     const float* a = A + row * static_cast<int64_t>(f) * f;
     const float* b = Bv + row * f;
@@ -167,7 +165,6 @@ __global__ void solve_exact_kernel(const float* __restrict__ A, const float* __r
     // all-zero test over the full f*f storage (solver.hpp:215-220)
     int nonzero = 0;
     for (int e = tid; e < f * f; e += nt) nonzero |= (a[e] != 0.0f);
-    if (tid == 0) s_broke = 0;
     if (!__syncthreads_or(nonzero)) {
         for (int i = tid; i < f; i += nt) x[i] = 0.0f;
         if (tid == 0) column[row] = 0;
@@ -185,27 +182,24 @@ __global__ void solve_exact_kernel(const float* __restrict__ A, const float* __r
     __syncthreads();
 
     SE_LAP(0)
+    bool broke = false;
     for (int c = 0; c < f; ++c) {
-        if (tid == 0) {
-            const double d = L[pk(c, c)];
-            if (!(d > 0.0)) {
-                s_flag = 1;
+        // every thread reads the pivot and takes its square root itself (the same value in
+        // every thread), so no single-thread phase and barrier precede the divisions
+        const double d = L[pk(c, c)];
+        if (!(d > 0.0)) {  // CTA-uniform
+            if (tid == 0) {
                 column[row] = c + 1;
                 pivot[row] = d;
                 atomicMin(min_row, static_cast<unsigned long long>(row_base + row));
-            } else {
-                s_flag = 0;
-                L[pk(c, c)] = sqrt(d);
             }
-        }
-        __syncthreads();
-        if (s_flag) {
-            s_broke = 1;
+            broke = true;
             break;
         }
-        const double lcc = L[pk(c, c)];
+        const double lcc = sqrt(d);
         for (int r = c + 1 + tid; r < f; r += nt) L[pk(r, c)] = __ddiv_rn(L[pk(r, c)], lcc);
-        __syncthreads();
+        __syncthreads();  // every thread has read d: the diagonal can take L[c][c] now
+        if (tid == 0) L[pk(c, c)] = lcc;
         // trailing update of entries (r, q), c < q <= r, enumerated flat over the threads
         // (row-major lower triangle: entry k of the (f-c-1)-triangle is tri[k]; the first
         // T(T+1)/2 entries of the largest triangle are exactly the smaller ones), so short
@@ -220,7 +214,7 @@ __global__ void solve_exact_kernel(const float* __restrict__ A, const float* __r
         __syncthreads();
     }
     SE_LAP(1)
-    if (s_broke) {
+    if (broke) {
         for (int i = tid; i < f; i += nt) x[i] = 0.0f;
         return;
     }
@@ -238,11 +232,20 @@ __global__ void solve_exact_kernel(const float* __restrict__ A, const float* __r
         SE_LAP(2)
         // back substitution reads the already-rounded float x[j] (solver.hpp:254-259);
         // its order (j ascending from i+1) is inherently sequential.
+        // Products of 8 consecutive j are formed ahead of their (in-order) subtractions, so
+        // only the subtraction chain is serial.
         if (tid == 0) {
             for (int i = f - 1; i >= 0; --i) {
                 double acc = s[i];
-                for (int j = i + 1; j < f; ++j)
-                    acc = __dsub_rn(acc, __dmul_rn(L[pk(j, i)], static_cast<double>(xs[j])));
+                int j = i + 1;
+                for (; j + 8 <= f; j += 8) {
+                    double p[8];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) p[u] = __dmul_rn(L[pk(j + u, i)], static_cast<double>(xs[j + u]));
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) acc = __dsub_rn(acc, p[u]);
+                }
+                for (; j < f; ++j) acc = __dsub_rn(acc, __dmul_rn(L[pk(j, i)], static_cast<double>(xs[j])));
                 xs[i] = static_cast<float>(__ddiv_rn(acc, L[pk(i, i)]));
             }
         }
