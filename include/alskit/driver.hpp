@@ -16,6 +16,9 @@
 // values, checkpoint bytes).
 #pragma once
 
+#include <unistd.h>
+
+#include <atomic>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -29,6 +32,7 @@
 #include <vector>
 
 #include "alskit/dataio.hpp"
+#include "alskit/parallel.hpp"
 #include "alskit/solver.hpp"
 #include "alskit/sparse.hpp"
 
@@ -49,9 +53,40 @@ struct RunConfig {
     std::string checkpoint_dir;
     std::string metrics;
     bool resume = false;
+    // the planner fields (config.hpp:54-60) with one worker -- the GPU: capacity in scalars
+    // (0 = unlimited), headroom -1 = capacity / 24, force_p/force_q 0 = plan. A side whose plan
+    // splits (p > 1 or q > 1) runs its half-sweeps out of core over its persisted grid
+    // (alsk_ooc_update); workers, groups and the two-phase reduce are out of scope (one GPU,
+    // one-phase reduce).
+    offset_t capacity = 0;
+    offset_t headroom = -1;
+    int force_p = 0;
+    int force_q = 0;
 };
 
 namespace detail {
+/// A private scratch directory (persisted grids of a split side), removed with its contents.
+class ScratchDir {
+  public:
+    const std::filesystem::path& path() {
+        if (path_.empty()) {
+            static std::atomic<unsigned> counter{0};
+            path_ = std::filesystem::temp_directory_path() /
+                    ("alskit-grids-" + std::to_string(static_cast<long long>(::getpid())) + "-" +
+                     std::to_string(counter.fetch_add(1)));
+            std::filesystem::create_directories(path_);
+        }
+        return path_;
+    }
+    ~ScratchDir() {
+        std::error_code ec;
+        if (!path_.empty()) std::filesystem::remove_all(path_, ec);
+    }
+
+  private:
+    std::filesystem::path path_;
+};
+
 inline std::string format_real(double v) {  // config.hpp:105-109
     char buf[40];
     std::snprintf(buf, sizeof buf, "%.17g", v);
@@ -112,14 +147,52 @@ struct TrainResult {  // driver.hpp:57-66
 inline TrainResult train_run(const CsrMatrix& r, const RunConfig& cfg, const IterationCallback& after_iteration = {}) {
     if (cfg.f < 1) throw InputError("f must be >= 1");
     if (cfg.iterations < 0) throw InputError("iterations must be >= 0");
+    if (cfg.capacity < 0) throw InputError("capacity must be non-negative");  // config.hpp:280-285
+    if (cfg.headroom < -1) throw InputError("headroom must be -1 (auto) or non-negative");
+    if (cfg.force_p < 0 || cfg.force_q < 0) throw InputError("force_p and force_q must be non-negative");
+    if ((cfg.force_p > 0) != (cfg.force_q > 0)) throw InputError("force_p and force_q must be set together");
     if (r.rows < 1 || r.cols < 1) throw InputError("dataset " + cfg.data + " is empty");
     const std::uint64_t digest = run_digest(cfg, r.rows, r.cols, r.nnz());
     const SplitResult split = split_train_test(r, cfg.holdout, detail::mix_seed(cfg.seed, 2));
     const CsrMatrix& train = split.train;
     const CscMatrix rt = csr_to_csc(train);  // the Theta-side view, built once (driver.hpp:115)
 
+    // per-side plan (driver.hpp:121-161) with one worker; a split side's grid is persisted once
+    // into a private scratch directory and its half-sweeps stream it
+    struct Side {
+        int p = 1, q = 1;
+        bool split = false;
+        std::filesystem::path grid;
+    };
+    detail::ScratchDir scratch;
+    auto make_side = [&](const CsrMatrix& mat, const char* name) {
+        Side sd;
+        if (cfg.force_p > 0) {
+            sd.p = cfg.force_p;
+            sd.q = cfg.force_q;
+        } else if (cfg.capacity > 0) {
+            Topology topo;
+            topo.workers = 1;
+            topo.capacity = cfg.capacity;
+            const PartitionPlan plan = plan_partition(mat.rows, mat.cols, mat.nnz(), cfg.f, topo,
+                                                      cfg.headroom >= 0 ? cfg.headroom : cfg.capacity / 24);
+            sd.p = plan.p;
+            sd.q = plan.q;
+        }
+        sd.split = sd.p > 1 || sd.q > 1;
+        if (sd.split) {
+            sd.grid = scratch.path() / name;
+            persist_grid(grid_partition(mat, sd.p, sd.q), sd.grid);
+        }
+        return sd;
+    };
+    const Side side_x = make_side(train, "grid_x");
+    const Side side_t = make_side(transpose_of(rt), "grid_theta");
+
     TrainResult result;
     result.digest = digest;
+    result.p = side_x.p;
+    result.q = side_x.q;
     result.baseline_rmse = detail::baseline_rmse_of(train, split.test);
     FactorMatrix x = random_factor(train.rows, cfg.f, cfg.seed);
     FactorMatrix theta = random_factor(train.cols, cfg.f, detail::mix_seed(cfg.seed, 1));
@@ -212,17 +285,32 @@ inline TrainResult train_run(const CsrMatrix& r, const RunConfig& cfg, const Ite
         return after_iteration(t, x, theta);
     };
 
+    const alsk_solver_config scfg{cfg.f, cfg.lambda, cfg.bin, cfg.batch_rows, cfg.accumulate_double ? 1 : 0,
+                                  cfg.threads, cfg.seed};
+    auto half_x = [&] {  // driver.hpp:163-167: update_x, or the SU-ALS side out of core
+        if (side_x.split)
+            detail::check(alsk_ooc_update(side_x.grid.c_str(), dtheta, train.cols, cfg.f, &scfg, dx, stream));
+        else
+            detail::check(alsk_session_half_x(sess.get()));
+    };
+    auto half_theta = [&] {
+        if (side_t.split)
+            detail::check(alsk_ooc_update(side_t.grid.c_str(), dx, train.rows, cfg.f, &scfg, dtheta, stream));
+        else
+            detail::check(alsk_session_half_theta(sess.get()));
+    };
+
     bool stopped = false;
     if (dangling_x) {  // finish the interrupted iteration first (driver.hpp:249-254)
-        detail::check(alsk_session_half_theta(sess.get()));
+        half_theta();
         snapshot(completed, FactorKind::theta);
         emit_row(completed);
         if (!callback(completed)) stopped = true;
     }
     for (int t = completed + 1; !stopped && t <= cfg.iterations; ++t) {  // driver.hpp:255-262
-        detail::check(alsk_session_half_x(sess.get()));
+        half_x();
         snapshot(t, FactorKind::x);
-        detail::check(alsk_session_half_theta(sess.get()));
+        half_theta();
         snapshot(t, FactorKind::theta);
         emit_row(t);
         if (!callback(t)) break;

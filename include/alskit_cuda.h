@@ -300,6 +300,17 @@ alsk_status alsk_grid_meta(const char* dir, int* p, int* q, int64_t* rows, int64
  * position on `stream` gates the slot's reuse. *has_block = 0 once the plan is exhausted;
  * a loader error ("block (i, j): ...") surfaces on the next() that would return it. */
 alsk_status alsk_block_stream_open(const char* dir, const int* order_ij, int count, void** stream_out);
+/* Out-of-core half-sweep (the scale-up of su_als_update_x, parallel.hpp:487-583, for
+ * matrices beyond HBM): one update of all rows of the grid persisted at
+ * grid_dir, against `factor` (device, factor_rows = the grid's columns), into x_out (device,
+ * grid rows x f) on `stream`. Blocks stream into HBM (alsk_block_stream_*) while the previous
+ * one computes; per row partition the block partials are reduced slice by slice and solved.
+ * accumulate_double: double partials, the one-phase reduce order, the reference-order solve
+ * -- bit-identical to su_als_update_x on the same grid; else the FP32 tensor-core path
+ * (16 <= f <= 119) or float partials. Errors as su_als_update_x: a block column outside its
+ * slab (InputError "column v outside partition [lo, hi)"), a breakdown (NumericalError). */
+alsk_status alsk_ooc_update(const char* grid_dir, const float* factor, int64_t factor_rows, int f,
+                            const alsk_solver_config* cfg, float* x_out, void* stream);
 alsk_status alsk_block_stream_next(void* block_stream, void* stream, int* has_block, int* i, int* j, alsk_csr* out);
 void alsk_block_stream_close(void* block_stream);
 /* Utility: synchronous device-to-host copy on `stream`. */

@@ -469,6 +469,31 @@ void ref_bench_release(void) {
 // The reference's own train_run (driver.hpp:107-268) on a binary cache, for the C++ driver
 // parity test (tests/test_train_run.py): factors out, metrics / checkpoints on disk.
 // stop_after > 0: the callback stops the run after that iteration (a killed run).
+// The same with the planner fields (config.hpp:54-60): capacity (scalars, 0 = unlimited),
+// force_p/force_q (0 = plan), one worker -- the run tests/test_train_run.py compares with our
+// train_run's out-of-core sides.
+extern "C" alsk_status ref_train_run_plan(const char* cache, int f, double lambda, int iterations, uint64_t seed,
+                                          int acc_double, const char* metrics, int64_t capacity, int force_p,
+                                          int force_q, float* x_out, float* theta_out) {
+    return guarded([&] {
+        R::RunConfig cfg;
+        cfg.data = cache;
+        cfg.format = R::RatingsFormat::binary_cache;
+        cfg.f = f;
+        cfg.lambda = lambda;
+        cfg.iterations = iterations;
+        cfg.seed = seed;
+        cfg.accumulate_double = acc_double != 0;
+        cfg.metrics = metrics ? metrics : "";
+        cfg.capacity = capacity;
+        cfg.force_p = force_p;
+        cfg.force_q = force_q;
+        const R::TrainResult r = R::train_run(cfg);
+        std::memcpy(x_out, r.x.entries.data(), sizeof(float) * r.x.entries.size());
+        std::memcpy(theta_out, r.theta.entries.data(), sizeof(float) * r.theta.entries.size());
+    });
+}
+
 extern "C" alsk_status ref_train_run(const char* cache, int f, double lambda, int iterations, uint64_t seed,
                                      int acc_double, const char* ckpt_dir, const char* metrics, int resume,
                                      int stop_after, float* x_out, float* theta_out, int* start_iteration,

@@ -88,6 +88,7 @@ _SIGS = {
     "alsk_block_stream_open": (C.c_int, [C.c_char_p, vp, C.c_int, C.POINTER(vp)]),
     "alsk_block_stream_next": (C.c_int, [vp, vp, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int), CsrP]),
     "alsk_block_stream_close": (None, [vp]),
+    "alsk_ooc_update": (C.c_int, [C.c_char_p, vp, i64, C.c_int, CfgP, vp, vp]),
     "alsk_dev_to_host": (C.c_int, [vp, vp, C.c_size_t, vp]),
     "alsk_host_to_dev": (C.c_int, [vp, vp, C.c_size_t, vp]),
     "alsk_dev_split_train_test": (C.c_int, [CsrP, C.c_double, C.c_uint64, C.POINTER(i64), vp, vp, vp, vp, vp]),

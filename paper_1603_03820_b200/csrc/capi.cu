@@ -1410,6 +1410,136 @@ alsk_status alsk_block_stream_next(void* bs, void* stream, int* has_block, int* 
 
 void alsk_block_stream_close(void* bs) { delete static_cast<DeviceBlockStream*>(bs); }
 
+// ---- out-of-core half-sweep -----------------------------------
+namespace alsk {
+__global__ void ooc_add_rows_kernel(float* __restrict__ acc, const float* __restrict__ part, int64_t n4) {
+    for (int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; k < n4;
+         k += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        float4 a = reinterpret_cast<float4*>(acc)[k];
+        const float4 b = reinterpret_cast<const float4*>(part)[k];
+        a.x += b.x, a.y += b.y, a.z += b.z, a.w += b.w;
+        reinterpret_cast<float4*>(acc)[k] = a;
+    }
+}
+}  // namespace alsk
+
+// One half-sweep over a persisted p x q grid (persist_grid, dataio.hpp:381-400) whose blocks
+// need not fit in HBM together -- the scale-up of su_als_update_x (parallel.hpp:487-583) on
+// one GPU: the device block stream uploads block (i, j) while the previous one computes; per
+// row partition j the partial Hermitians of its blocks against the factor's column slabs are
+// reduced and solved slice by slice (slice_cuts, parallel.hpp:160-168), as su_als's workers
+// do. FP64-exact: double partials, the reference's one-phase reduce order, rounded once to
+// float, the reference-order solve -- bit-identical to su_als_update_x on the same grid.
+// FP32: the tensor-core packed partials (16 <= f <= 119) summed in block order, else float
+// partials through the same reduce. Block columns outside their slab raise the reference's
+// InputError (checked asynchronously; the tensor-core gather clamps meanwhile).
+alsk_status alsk_ooc_update(const char* grid_dir, const float* factor, int64_t factor_rows, int f,
+                            const alsk_solver_config* cfg, float* x_out, void* stream) {
+    return guard([&] {
+        if (f < 1) fail_input("rank must be >= 1");
+        require_device();
+        cudaStream_t s = as_stream(stream);
+        const GridMetaH g = read_grid_meta(grid_dir);
+        if (factor_rows != g.cols)
+            fail_input("factor rows " + std::to_string(factor_rows) + " do not match matrix columns " +
+                       std::to_string(g.cols));
+        const int p = g.p, q = g.q;
+        const bool exact = cfg->accumulate_double != 0;
+        const bool tc = !exact && use_tensor_cores(ALSK_PREC_FP32, f);
+        std::vector<int> order;
+        for (int j = 0; j < q; ++j)
+            for (int i = 0; i < p; ++i) order.insert(order.end(), {i, j});
+        const ReduceSchedule sc = build_reduce_schedule(p, nullptr, false);
+        int64_t lr_max = 1;
+        for (int j = 0; j < q; ++j) lr_max = std::max(lr_max, g.row_cuts[j + 1] - g.row_cuts[j]);
+        const int64_t ff = static_cast<int64_t>(f) * f;
+        const size_t pkn = static_cast<size_t>(packed_stride(f));
+        DevBuf acc, part;
+        if (tc) {
+            acc.alloc(sizeof(float) * pkn * lr_max, s);
+            part.alloc(sizeof(float) * pkn * lr_max, s);
+        }
+        DeviceBlockStream bs(grid_dir, order);
+        for (int j = 0; j < q; ++j) {
+            const int64_t r0 = g.row_cuts[j], lr = g.row_cuts[j + 1] - r0;
+            const auto cuts = slice_cuts(lr, p);
+            std::vector<DevBuf> pa, pb;
+            if (!tc)
+                for (int i = 0; i < p; ++i) {
+                    const size_t esz = exact ? sizeof(double) : sizeof(float);
+                    pa.emplace_back(esz * std::max<int64_t>(lr * ff, 1), s);
+                    pb.emplace_back(esz * std::max<int64_t>(lr * f, 1), s);
+                }
+            for (int i = 0; i < p; ++i) {
+                DeviceBlockStream::Out o{};
+                if (!bs.next(s, o))
+                    fail_io(std::string(grid_dir) + ": block stream ended before block (" + std::to_string(i) + ", " +
+                            std::to_string(j) + ")");
+                const DevCsr v{o.rows, o.cols, o.col_offset, o.nnz, o.row_ptr, o.col_idx, o.values};
+                const int64_t lo = g.col_cuts[i], width = g.col_cuts[i + 1] - lo;
+                if (lr == 0) continue;
+                // the block's columns against its slab, with the reference's message (blocks are
+                // large here, so the round trip is cheap next to their Hermitians)
+                check_columns(v, 0, lr, lo, lo + width, s);
+                const float* slab = factor + lo * f;
+                if (tc) {
+                    hermitian_packed_tc(v, slab, width, f, static_cast<float>(cfg->lambda), 0, lr,
+                                        i == 0 ? acc.as<float>() : part.as<float>(), s);
+                    if (i > 0) {
+                        const int64_t n4 = static_cast<int64_t>(lr * pkn / 4);
+                        ooc_add_rows_kernel<<<static_cast<unsigned>(std::min<int64_t>((n4 + 255) / 256, num_sms() * 8)), 256, 0, s>>>(acc.as<float>(), part.as<float>(), n4);
+                        ALSK_LAUNCHED();
+                    }
+                } else if (exact) {
+                    hermitian_materialize_d(v, slab, f, cfg->lambda, true, 0, lr, pa[i].as<double>(),
+                                            pb[i].as<double>(), false, s);
+                } else {
+                    hermitian_materialize(v, slab, f, cfg->lambda, false, 0, lr, pa[i].as<float>(),
+                                          pb[i].as<float>(), s);
+                }
+            }
+            if (lr == 0) continue;
+            std::vector<StatusBufs> status;
+            status.reserve(p);
+            if (tc) {
+                for (int k = 0; k < p; ++k) {
+                    const int64_t c0 = cuts[k], n = cuts[k + 1] - c0;
+                    status.emplace_back(std::max<int64_t>(n, 1), s);
+                    if (n) packed_solve(acc.as<float>() + c0 * pkn, n, f, x_out + (r0 + c0) * f, status.back().st, 0, s);
+                }
+            } else {
+                std::vector<DevBuf> oa(p), ob(p);
+                std::vector<float*> poa, pob;
+                for (int k = 0; k < p; ++k) {
+                    const int64_t n = cuts[k + 1] - cuts[k];
+                    oa[k].alloc(sizeof(float) * std::max<int64_t>(n * ff, 1), s);
+                    ob[k].alloc(sizeof(float) * std::max<int64_t>(n * f, 1), s);
+                    poa.push_back(oa[k].as<float>());
+                    pob.push_back(ob[k].as<float>());
+                }
+                if (exact) {
+                    std::vector<const double*> a, b;
+                    for (int i = 0; i < p; ++i) a.push_back(pa[i].as<double>()), b.push_back(pb[i].as<double>());
+                    reduce_slices<double>(a, b, lr, f, sc, poa, pob, s);
+                } else {
+                    std::vector<const float*> a, b;
+                    for (int i = 0; i < p; ++i) a.push_back(pa[i].as<float>()), b.push_back(pb[i].as<float>());
+                    reduce_slices<float>(a, b, lr, f, sc, poa, pob, s);
+                }
+                for (int k = 0; k < p; ++k) {
+                    const int64_t n = cuts[k + 1] - cuts[k];
+                    status.emplace_back(std::max<int64_t>(n, 1), s);
+                    if (n) solve_exact(poa[k], pob[k], n, f, false, x_out + (r0 + cuts[k]) * f, status.back().st, s);
+                }
+            }
+            // this partition's breakdowns before the next partition's column checks (the
+            // reference's worker loop solves partition j before assembling j+1)
+            for (auto& sb : status) sb.raise_if_broken(s, 0);
+        }
+        ALSK_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
 alsk_status alsk_dev_to_host(void* dst, const void* src, size_t bytes, void* stream) {
     return guard([&] {
         require_device();

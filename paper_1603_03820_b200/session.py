@@ -309,29 +309,16 @@ class DeviceBlockStream:
         self.close()
 
 
-def out_of_core_update_x(dir, theta: torch.Tensor, f: int, lam: float, out: torch.Tensor) -> None:
-    """The X half over a persisted grid that need not fit in HBM (the
-    SU-ALS scale-up, parallel.hpp:487-583, fed by the block stream): for each row partition
-    j, the FP32 partial Hermitians of its blocks (i, j) against Theta's column slab i are
-    summed (panel-blocked packed rows) and solved with the batched TMEM Cholesky. Blocks
-    arrive in row-major order, each upload overlapping the kernels of the previous one."""
-    from .alskit import load_grid_meta, row_major_order
-    from .distributed import cuda_partial_hermitian_f32, cuda_solve_packed_f32, packed_stride
-    meta = load_grid_meta(dir)
-    per = packed_stride(f)
-    dev = theta.device
-    rows_max = int(np.max(np.diff(meta.row_cuts))) if meta.q else 0
-    acc = torch.empty(max(rows_max, 1) * per, dtype=torch.float32, device=dev)
-    part = torch.empty_like(acc)
-    with DeviceBlockStream(dir, row_major_order(meta)) as bs:
-        for ref, blk in bs:
-            lo, hi = int(meta.col_cuts[ref.i]), int(meta.col_cuts[ref.i + 1])
-            rows = blk.rows
-            dst = acc if ref.i == 0 else part
-            if rows:
-                cuda_partial_hermitian_f32(blk, theta[lo * f:], hi - lo, f, lam, 0, rows, dst)
-                if ref.i:
-                    acc[: rows * per].add_(part[: rows * per])
-            if ref.i == meta.p - 1 and rows:
-                r0 = int(meta.row_cuts[ref.j])
-                cuda_solve_packed_f32(acc, rows, f, out[r0 * f:])
+def out_of_core_update_x(dir, theta: torch.Tensor, f: int, lam: float, out: torch.Tensor,
+                         precision: int = PREC_FP32) -> None:
+    """One half-sweep over a persisted grid that need not fit in HBM (the
+    scale-up of su_als_update_x, parallel.hpp:487-583): alsk_ooc_update streams the blocks
+    into HBM (block (i, j) uploads while the previous one computes), reduces each row
+    partition's partial Hermitians slice by slice and solves them. PREC_FP64_EXACT is
+    bit-identical to the reference's su_als_update_x on the same grid; PREC_FP32 uses the
+    tensor-core partials. `theta` holds the factor of the grid's columns, `out` receives the
+    grid's rows (both on the device). The Theta half is the same call on the persisted grid
+    of R^T with X as the factor."""
+    cfg = N.SolverConfigT(f, lam, 16, 4096, 1 if precision == PREC_FP64_EXACT else 0, 0, 0)
+    _check(LIB.alsk_ooc_update(str(dir).encode(), theta.data_ptr(), theta.numel() // f, f, C.byref(cfg),
+                               out.data_ptr(), stream_handle()))

@@ -12,7 +12,8 @@ from paper_1603_03820_b200 import alskit as A
 from paper_1603_03820_b200.session import PREC_FP32, DeviceCsr, dev_update, out_of_core_update_x
 
 grids = [int(a) for a in sys.argv[1:]] or [1, 4, 2, 4, 4, 8]
-train, _ = bench.make_data("netflix")
+m, n, nnz, _, _ = bench.CONFIGS["netflix"]
+train = A.split_train_test(A.synth_csr(m, n, nnz, bench.data_seed("netflix")), 0.1, A.mix_seed(42, 2)).train
 f, lam = 100, 0.05
 dev = torch.device("cuda")
 T = torch.from_numpy(A.random_factor(train.cols, f, 9).entries).to(dev)

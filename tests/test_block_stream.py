@@ -125,3 +125,73 @@ def test_out_of_core_x_half_matches_in_core(A, gpu, tmp_path, p, q):
     gap = normwise_gap(x_ooc.cpu().numpy(), x_in.cpu().numpy())
     assert gap <= 1e-3, gap
     assert gap <= 1e-4, gap
+
+
+def _ocsr(r):
+    from oracle import binding
+    return binding.csr_struct(r.rows, r.cols, r.row_ptr, r.col_idx, r.values, r.col_offset)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("p,q", [(1, 1), (2, 2), (3, 2), (4, 3)])
+def test_out_of_core_fp64_matches_reference_su_als(A, ref, gpu, tmp_path, p, q):
+    """FP64-exact out-of-core half-sweeps -- X over the persisted grid of R, Theta over the
+    persisted grid of R^T with that X -- are bit-identical to the reference's own
+    su_als_update_x (parallel.hpp:487-583) on the same p x q grids."""
+    import torch
+    from paper_1603_03820_b200.session import PREC_FP64_EXACT, out_of_core_update_x
+    f, lam, m, n = 6, 0.05, 150, 70
+    r = A.synth_csr(m, n, 2600, 17)
+    th = A.random_factor(n, f, 3)
+    dev = torch.device("cuda")
+    A.persist_grid(A.grid_partition(r, p, q), tmp_path / "gx")
+    x = torch.zeros(m * f, dtype=torch.float32, device=dev)
+    out_of_core_update_x(tmp_path / "gx", torch.from_numpy(th.entries).to(dev), f, lam, x, PREC_FP64_EXACT)
+    st, xr = ref.su_als_update_x(_ocsr(r), th.entries, n, f, p, q, lam, 1, 0)
+    assert st == 0 and np.array_equal(x.cpu().numpy(), xr)
+    rt = A.transpose_of(A.csr_to_csc(r))
+    A.persist_grid(A.grid_partition(rt, p, q), tmp_path / "gt")
+    t = torch.zeros(n * f, dtype=torch.float32, device=dev)
+    out_of_core_update_x(tmp_path / "gt", x, f, lam, t, PREC_FP64_EXACT)
+    st, tr = ref.su_als_update_x(_ocsr(rt), xr, m, f, p, q, lam, 1, 0)
+    assert st == 0 and np.array_equal(t.cpu().numpy(), tr)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("f", [10, 24, 100, 130])
+def test_out_of_core_fp32_within_bar_of_fp64(A, gpu, tmp_path, f):
+    """The FP32 out-of-core path (tensor-core packed partials for 16 <= f <= 119, float
+    partials through the reduce otherwise) stays within the FP32 bar of the FP64-exact one."""
+    import torch
+    from paper_1603_03820_b200.session import PREC_FP32, PREC_FP64_EXACT, out_of_core_update_x
+    r, g, d = _grid(A, tmp_path, 3, 2, m=900, n=400, nnz=40_000, seed=8)
+    dev = torch.device("cuda")
+    T = torch.from_numpy(A.random_factor(r.cols, f, 9).entries).to(dev)
+    x32 = torch.zeros(r.rows * f, dtype=torch.float32, device=dev)
+    x64 = torch.zeros_like(x32)
+    out_of_core_update_x(d, T, f, 0.05, x32, PREC_FP32)
+    out_of_core_update_x(d, T, f, 0.05, x64, PREC_FP64_EXACT)
+    assert normwise_gap(x32.cpu().numpy(), x64.cpu().numpy()) <= 1e-4
+
+
+@pytest.mark.gpu
+def test_out_of_core_errors(A, gpu, tmp_path):
+    """Factor rows must match the grid's columns; a block column outside its slab raises the
+    reference's message (solver.hpp:120-123) naming the column."""
+    import torch
+    from paper_1603_03820_b200.session import PREC_FP32, out_of_core_update_x
+    r, g, d = _grid(A, tmp_path, 2, 1, m=40, n=30, nnz=300, seed=2)
+    f = 24
+    dev = torch.device("cuda")
+    x = torch.zeros(r.rows * f, dtype=torch.float32, device=dev)
+    with pytest.raises(A.InputError, match="factor rows 29 do not match matrix columns 30"):
+        out_of_core_update_x(d, torch.zeros(29 * f, device=dev), f, 0.05, x, PREC_FP32)
+    # block (0, 0) holds the columns [0, cut); move one of its entries into slab 1
+    cut = int(g.col_cuts[1])
+    b00 = A.load_binary_cache(A.block_path(d, 0, 0))
+    ci = b00.col_idx.copy()
+    u = int(np.argmax(np.diff(b00.row_ptr) > 0))  # a row with entries: its last one moves past the cut
+    ci[int(b00.row_ptr[u + 1]) - 1] = cut + 1
+    A.save_binary_cache(A.CsrMatrix(b00.rows, b00.cols, 0, b00.row_ptr, ci, b00.values), A.block_path(d, 0, 0))
+    with pytest.raises(A.InputError, match=rf"column {cut + 1} outside partition \[0, {cut}\)"):
+        out_of_core_update_x(d, torch.zeros(30 * f, device=dev), f, 0.05, x, PREC_FP32)

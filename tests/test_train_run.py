@@ -40,9 +40,11 @@ def cache(ref, tmp_path_factory):
     return p
 
 
-def ours(cache, out, iters, acc=1, ckpt="-", metrics="-", resume=0, stop=-1):
+def ours(cache, out, iters, acc=1, ckpt="-", metrics="-", resume=0, stop=-1, plan=None):
     cmd = [str(EXE), str(cache), str(F), repr(LAM), str(iters), str(SEED), str(acc), str(ckpt), str(metrics),
-           str(resume), str(out)] + ([str(stop)] if stop > 0 else [])
+           str(resume), str(out)] + ([str(stop)] if stop > 0 or plan else [])
+    if plan:  # (capacity, force_p, force_q)
+        cmd += [str(v) for v in plan]
     res = subprocess.run(cmd, capture_output=True, text=True, timeout=300)
     assert res.returncode == 0, res.stdout + res.stderr
     x = np.fromfile(f"{out}_x.f32", np.float32)
@@ -111,4 +113,44 @@ def test_train_run_resumes_reference_checkpoints(ref, cache, tmp_path):
 def test_train_run_fp32_within_bars(ref, cache, tmp_path):
     xr, tr, _ = theirs(ref, cache, 4)
     x, t, _ = ours(cache, tmp_path / "o", 4, acc=0)
+    assert normwise_gap(x, xr) <= 1e-3 and normwise_gap(t, tr) <= 1e-3
+
+
+@pytest.mark.parametrize("plan", [(60000, 0, 0), (0, 2, 3)])
+def test_train_run_split_sides_match_reference(ref, cache, tmp_path, plan):
+    """The planner fields (config.hpp:54-60): a capacity that makes plan_partition split the
+    rows (q = 4 for X, 2 for Theta here) or a forced 2 x 3 grid. Our train_run persists each
+    split side's grid and runs its half-sweeps out of core (alsk_ooc_update, blocks streamed
+    into HBM); the reference's train_run runs su_als_update_x on the same grids in memory.
+    FP64: factors bit-identical, the metrics CSV equal."""
+    x, t, _ = ours(cache, tmp_path / "o", 3, metrics=tmp_path / "o.csv", plan=plan)
+    xr = np.zeros(M * F, np.float32)
+    tr = np.zeros(N * F, np.float32)
+    st = ref.call("train_run_plan", str(cache).encode(), F, C.c_double(LAM), 3, C.c_uint64(SEED), 1,
+                  str(tmp_path / "r.csv").encode(), C.c_int64(plan[0]), plan[1], plan[2],
+                  xr.ctypes.data_as(C.c_void_p), tr.ctypes.data_as(C.c_void_p))
+    assert st == 0, ref.last_error()
+    assert np.array_equal(x, xr) and np.array_equal(t, tr)
+    _, _, ro = _csv(tmp_path / "o.csv")
+    _, _, rr = _csv(tmp_path / "r.csv")
+    assert [r[0] for r in ro] == [r[0] for r in rr] == ["1", "2", "3"]
+    for a, b in zip(ro, rr):
+        for k in (2, 3):
+            assert abs(float(a[k]) - float(b[k])) <= 1e-12 * abs(float(b[k])), (a, b)
+    # and the split really happened (the CLI reports the X side's grid)
+    res = subprocess.run([str(EXE), str(cache), str(F), repr(LAM), "1", str(SEED), "1", "-", "-", "0",
+                          str(tmp_path / "p"), "-1", *map(str, plan)], capture_output=True, text=True, timeout=300)
+    pq = res.stdout.split("p=")[1].split()
+    assert (int(pq[0]), int(pq[1].split("=")[1])) == ((2, 3) if plan[1] else (1, 4)), res.stdout
+
+
+def test_train_run_split_fp32_within_bars(ref, cache, tmp_path):
+    """FP32 with split sides (tensor-core partials out of core) stays within the FP32 bar of the
+    reference's FP64 train_run on the same grids."""
+    x, t, _ = ours(cache, tmp_path / "o", 3, acc=0, plan=(0, 2, 3))
+    xr = np.zeros(M * F, np.float32)
+    tr = np.zeros(N * F, np.float32)
+    st = ref.call("train_run_plan", str(cache).encode(), F, C.c_double(LAM), 3, C.c_uint64(SEED), 1, None,
+                  C.c_int64(0), 2, 3, xr.ctypes.data_as(C.c_void_p), tr.ctypes.data_as(C.c_void_p))
+    assert st == 0, ref.last_error()
     assert normwise_gap(x, xr) <= 1e-3 and normwise_gap(t, tr) <= 1e-3
