@@ -529,33 +529,53 @@ small_update_kernel(const int64_t* __restrict__ row_ptr, const int32_t* __restri
 #pragma unroll
     for (int q = 0; q < F; ++q) b[q] = 0.f;
     const int64_t k0 = row_ptr[u], k1 = row_ptr[u + 1];
-    for (int64_t k = k0 + lane; k < k1; k += (WARP ? 32 : 1)) {
-        const int v = col_idx[k] - static_cast<int>(col_lo);
-        const float r = values[k];
+    // SU ratings per lane per round: every index, value and row load of the round is issued
+    // before the first product, so a thread has SU gathers in flight instead of one dependent
+    // col_idx -> row chain. Slots past the row end load nothing and add exact zeros, so the
+    // sums keep the one-rating-at-a-time order.
+    constexpr int SU = F <= 12 ? 4 : 2;
+    constexpr int64_t step = WARP ? 32 : 1;
+    for (int64_t k = k0 + lane; k < k1; k += SU * step) {
+        int vv[SU];
+        float rr[SU];
+#pragma unroll
+        for (int j = 0; j < SU; ++j) {
+            const bool ok = k + j * step < k1;
+            vv[j] = ok ? __ldg(col_idx + k + j * step) - static_cast<int>(col_lo) : 0;
+            rr[j] = ok ? __ldg(values + k + j * step) : 0.f;
+        }
         // the caller's rows in place (no padded copy): 16-, 8- or 4-byte loads by F's alignment
-        const float* src = theta + static_cast<int64_t>(v) * ldt;
-        float th[4 * NQ];
-        if constexpr (F % 4 == 0) {
+        float th[SU][4 * NQ];
 #pragma unroll
-            for (int q = 0; q < NQ; ++q) {
-                const float4 w = __ldg(reinterpret_cast<const float4*>(src) + q);
-                th[4 * q] = w.x, th[4 * q + 1] = w.y, th[4 * q + 2] = w.z, th[4 * q + 3] = w.w;
+        for (int j = 0; j < SU; ++j) {
+            const bool ok = k + j * step < k1;
+            const float* src = theta + static_cast<int64_t>(ok ? vv[j] : 0) * ldt;
+            if constexpr (F % 4 == 0) {
+#pragma unroll
+                for (int q = 0; q < NQ; ++q) {
+                    const float4 w = ok ? __ldg(reinterpret_cast<const float4*>(src) + q) : make_float4(0.f, 0.f, 0.f, 0.f);
+                    th[j][4 * q] = w.x, th[j][4 * q + 1] = w.y, th[j][4 * q + 2] = w.z, th[j][4 * q + 3] = w.w;
+                }
+            } else if constexpr (F % 2 == 0) {
+#pragma unroll
+                for (int q = 0; q < F / 2; ++q) {
+                    const float2 w = ok ? __ldg(reinterpret_cast<const float2*>(src) + q) : make_float2(0.f, 0.f);
+                    th[j][2 * q] = w.x, th[j][2 * q + 1] = w.y;
+                }
+            } else {
+#pragma unroll
+                for (int q = 0; q < F; ++q) th[j][q] = ok ? __ldg(src + q) : 0.f;
             }
-        } else if constexpr (F % 2 == 0) {
-#pragma unroll
-            for (int q = 0; q < F / 2; ++q) {
-                const float2 w = __ldg(reinterpret_cast<const float2*>(src) + q);
-                th[2 * q] = w.x, th[2 * q + 1] = w.y;
-            }
-        } else {
-#pragma unroll
-            for (int q = 0; q < F; ++q) th[q] = __ldg(src + q);
         }
 #pragma unroll
-        for (int i = 0; i < F; ++i) {
-            b[i] = fmaf(r, th[i], b[i]);
+        for (int j = 0; j < SU; ++j) {
+            if (k + j * step >= k1) break;  // past the row end
 #pragma unroll
-            for (int j = 0; j <= i; ++j) a[i * (i + 1) / 2 + j] = fmaf(th[i], th[j], a[i * (i + 1) / 2 + j]);
+            for (int i = 0; i < F; ++i) {
+                b[i] = fmaf(rr[j], th[j][i], b[i]);
+#pragma unroll
+                for (int c = 0; c <= i; ++c) a[i * (i + 1) / 2 + c] = fmaf(th[j][i], th[j][c], a[i * (i + 1) / 2 + c]);
+            }
         }
     }
     if constexpr (WARP) {  // every lane ends with the same sums (fixed butterfly order)
