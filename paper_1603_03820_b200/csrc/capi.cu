@@ -1326,14 +1326,14 @@ alsk_status alsk_checkpoint_latest(const char* dir, int which, char* out, size_t
 
 alsk_status alsk_ckpt_writer_create(const char* dir, void** writer) {
     return guard([&] {
-        require_device();
-        *writer = new DeviceWriter(dir);
+        *writer = new DeviceWriter(dir);  // CUDA state is created on the first device submit
     });
 }
 
 alsk_status alsk_ckpt_writer_submit_device(void* writer, int iteration, int which, int64_t rows, int f,
                                            uint64_t digest, const float* d_factor, void* stream) {
     return guard([&] {
+        require_device();
         static_cast<DeviceWriter*>(writer)->submit_device(iteration, which, rows, f, digest, d_factor,
                                                           static_cast<cudaStream_t>(stream));
     });

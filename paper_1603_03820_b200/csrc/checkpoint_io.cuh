@@ -18,6 +18,8 @@
 // write, as the reference's does); a write failure is sticky and returned by the next
 // submit() or flush().
 #pragma once
+#include <algorithm>
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 #include <condition_variable>
@@ -135,13 +137,10 @@ std::string latest_checkpoint(const std::string& dir, int which) {
 
 class DeviceWriter {
   public:
-    explicit DeviceWriter(std::string dir) : dir_(std::move(dir)) {
-        ALSK_CUDA(cudaGetDevice(&device_));
-        ALSK_CUDA(cudaStreamCreateWithFlags(&copy_, cudaStreamNonBlocking));
-        ALSK_CUDA(cudaEventCreateWithFlags(&after_caller_, cudaEventDisableTiming));
-        ALSK_CUDA(cudaEventCreateWithFlags(&copied_, cudaEventDisableTiming));
-        worker_ = std::thread([this] { run(); });
-    }
+    // host-only use (submit_host) touches no CUDA state, like the reference's pure-host
+    // writer (dataio.hpp:565-651); the stream, events and pinned staging appear on the
+    // first submit_device
+    explicit DeviceWriter(std::string dir) : dir_(std::move(dir)) { worker_ = std::thread([this] { run(); }); }
 
     ~DeviceWriter() {
         {
@@ -150,18 +149,20 @@ class DeviceWriter {
         }
         cv_.notify_all();
         worker_.join();  // drains a pending write
-        if (pinned_) cudaFreeHost(pinned_);
+        release_buffer();
         if (dscratch_) cudaFree(dscratch_);
-        cudaEventDestroy(after_caller_);
-        cudaEventDestroy(copied_);
-        cudaStreamDestroy(copy_);
+        if (copy_) {
+            cudaEventDestroy(after_caller_);
+            cudaEventDestroy(copied_);
+            cudaStreamDestroy(copy_);
+        }
     }
 
     // device factor (rows x f, row-major) ordered after `stream`; returns once the copy is
     // queued (and any previous write has finished)
     void submit_device(int iteration, int which, int64_t rows, int f, uint64_t digest, const float* d,
                        cudaStream_t stream) {
-        submit(iteration, which, rows, f, digest, [&](float* dst, size_t bytes) {
+        submit(iteration, which, rows, f, digest, true, [&](float* dst, size_t bytes) {
             // value semantics at HBM speed: a device-to-device copy on the caller's stream
             // (the caller may overwrite the factor right after), then the slow D2H from
             // that copy on the private stream, overlapping the caller's next kernels
@@ -180,7 +181,7 @@ class DeviceWriter {
     }
 
     void submit_host(int iteration, int which, int64_t rows, int f, uint64_t digest, const float* h) {
-        submit(iteration, which, rows, f, digest, [&](float* dst, size_t bytes) {
+        submit(iteration, which, rows, f, digest, false, [&](float* dst, size_t bytes) {
             if (bytes) std::memcpy(dst, h, bytes);
         });
     }
@@ -197,33 +198,45 @@ class DeviceWriter {
         int64_t rows;
         int f;
         uint64_t digest;
+        bool device;
     };
 
     template <class Fill>
-    void submit(int iteration, int which, int64_t rows, int f, uint64_t digest, Fill&& fill) {
+    void submit(int iteration, int which, int64_t rows, int f, uint64_t digest, bool device, Fill&& fill) {
         if (which != 0 && which != 1) fail_input("factor kind must be 0 (x) or 1 (theta)");
         if (rows < 0 || f < 1) fail_input("invalid factor shape");
         std::unique_lock<std::mutex> lock(mu_);
         cv_.wait(lock, [&] { return (!pending_ && !writing_) || error_; });
         rethrow_locked();
+        if (device && !copy_) {
+            ALSK_CUDA(cudaGetDevice(&device_));
+            ALSK_CUDA(cudaStreamCreateWithFlags(&copy_, cudaStreamNonBlocking));
+            ALSK_CUDA(cudaEventCreateWithFlags(&after_caller_, cudaEventDisableTiming));
+            ALSK_CUDA(cudaEventCreateWithFlags(&copied_, cudaEventDisableTiming));
+        }
         const size_t bytes = sizeof(float) * static_cast<size_t>(rows) * static_cast<size_t>(f);
-        if (bytes > cap_) {  // nothing is in flight: the buffer is free to replace
-            if (pinned_) ALSK_CUDA(cudaFreeHost(pinned_));
-            pinned_ = nullptr;
-            cap_ = 0;
-            ALSK_CUDA(cudaMallocHost(reinterpret_cast<void**>(&pinned_), bytes));
+        // nothing is in flight: the buffer is free to replace (pinned once a device copy needs it)
+        if (bytes > cap_ || (device && !is_pinned_)) {
+            release_buffer();
+            if (device) {
+                ALSK_CUDA(cudaMallocHost(reinterpret_cast<void**>(&pinned_), std::max<size_t>(bytes, 1)));
+            } else {
+                pinned_ = static_cast<float*>(std::malloc(std::max<size_t>(bytes, 1)));
+                if (!pinned_) throw std::bad_alloc();
+            }
+            is_pinned_ = device;
             cap_ = bytes;
         }
         fill(pinned_, bytes);
-        ALSK_CUDA(cudaEventRecord(copied_, copy_));
-        job_ = Job{iteration, which, rows, f, digest};
+        if (device) ALSK_CUDA(cudaEventRecord(copied_, copy_));
+        job_ = Job{iteration, which, rows, f, digest, device};
         pending_ = true;
         lock.unlock();
         cv_.notify_all();
     }
 
     void run() {
-        cudaSetDevice(device_);
+        bool bound = false;
         for (;;) {
             std::unique_lock<std::mutex> lock(mu_);
             cv_.wait(lock, [&] { return pending_ || stop_; });
@@ -235,7 +248,11 @@ class DeviceWriter {
             alsk_status st = ALSK_OK;
             std::string msg;
             try {
-                ALSK_CUDA(cudaEventSynchronize(copied_));
+                if (job.device) {
+                    if (!bound) ALSK_CUDA(cudaSetDevice(device_));
+                    bound = true;
+                    ALSK_CUDA(cudaEventSynchronize(copied_));
+                }
                 write_checkpoint_file(dir_, job.iteration, job.which, job.rows, job.f, job.digest, pinned_);
             } catch (const Failure& e) {
                 st = e.status;
@@ -255,6 +272,15 @@ class DeviceWriter {
         }
     }
 
+    void release_buffer() {
+        if (pinned_) {
+            if (is_pinned_) cudaFreeHost(pinned_);
+            else std::free(pinned_);
+        }
+        pinned_ = nullptr;
+        cap_ = 0;
+    }
+
     void rethrow_locked() {
         if (error_) throw Failure(error_, error_msg_);
     }
@@ -263,7 +289,8 @@ class DeviceWriter {
     int device_ = 0;
     cudaStream_t copy_ = nullptr;
     cudaEvent_t after_caller_ = nullptr, copied_ = nullptr;
-    float* pinned_ = nullptr;
+    float* pinned_ = nullptr;  // staging: page-locked after the first device submit
+    bool is_pinned_ = false;
     size_t cap_ = 0;
     float* dscratch_ = nullptr;
     size_t dcap_ = 0;

@@ -128,6 +128,37 @@ def _session(A, seed=3, fp64=True):
     return r, cfg, lambda: AlsSession(r, None, None, cfg, x0, t0)
 
 
+def test_host_writer_needs_no_device(A, tmp_path):
+    """The C-ABI writer's host submit runs without a GPU, like the reference's pure-host
+    CheckpointWriter (dataio.hpp:717-786): files identical to write_checkpoint's, errors
+    sticky."""
+    import ctypes as C
+    from paper_1603_03820_b200 import _native as N
+    fm = factor(A, 33, 5, 4)
+    h = C.c_void_p()
+    A._check(N.LIB.alsk_ckpt_writer_create(str(tmp_path / "w").encode(), C.byref(h)))
+    try:
+        for it, wh in ((1, 0), (1, 1), (2, 0)):
+            A._check(N.LIB.alsk_ckpt_writer_submit_host(h, it, wh, 33, 5, 9, fm.entries.ctypes.data))
+        A._check(N.LIB.alsk_ckpt_writer_flush(h))
+    finally:
+        N.LIB.alsk_ckpt_writer_destroy(h)
+    want = A.write_checkpoint(A.Checkpoint(2, A.FactorKind.x, fm, 9), tmp_path / "direct")
+    assert (tmp_path / "w" / "ckpt_000002_x.bin").read_bytes() == open(want, "rb").read()
+    assert sorted(x.name for x in (tmp_path / "w").iterdir()) == [
+        "ckpt_000001_theta.bin", "ckpt_000001_x.bin", "ckpt_000002_x.bin"]
+    blocker = tmp_path / "file"
+    blocker.write_bytes(b"")
+    A._check(N.LIB.alsk_ckpt_writer_create(str(blocker / "sub").encode(), C.byref(h)))
+    try:
+        A._check(N.LIB.alsk_ckpt_writer_submit_host(h, 1, 0, 33, 5, 9, fm.entries.ctypes.data))
+        for _ in range(2):
+            with pytest.raises(A.IoError, match="cannot create directory"):
+                A._check(N.LIB.alsk_ckpt_writer_flush(h))
+    finally:
+        N.LIB.alsk_ckpt_writer_destroy(h)
+
+
 @pytest.mark.gpu
 def test_device_writer_snapshots_by_value(A, gpu, tmp_path):
     import torch
