@@ -130,16 +130,36 @@ __global__ void check_columns_kernel(const int64_t* __restrict__ row_ptr,
     }
 }
 
-// Packed lower-triangular index.
-__device__ __forceinline__ int pk(int i, int j) { return i * (i + 1) / 2 + j; }
-
 // One CTA per system. Shared: packed lower L (double), rhs/forward vector s (double),
 // x (float).
+// Back substitution does not run here: it is one serial chain of f(f-1)/2 subtractions per
+// system (the reference's order), which would hold the whole CTA. The kernel hands each
+// system to backsub_exact_kernel instead, through `work` (subst_stride(f) doubles per
+// system): y (f doubles), then for i = f-1 down to 0 the diagonal L[i][i] followed by
+// L[j][i], j = i+1..f-1 -- the order the substitution consumes them. A system that needs no
+// substitution (all-zero or broken; x already written) gets 0 as its first diagonal.
+// Element e of system t sits at subst_at(t, e): interleaved by 32 systems, so the
+// substitution warp's loads of one element are a single 256-byte access.
+__host__ __device__ inline int64_t subst_stride(int f) { return static_cast<int64_t>(f) * (f + 1) / 2 + f; }
+__device__ __forceinline__ int64_t subst_at(int64_t t, int64_t e, int64_t per) {
+    return (t >> 5) * (per * 32) + e * 32 + (t & 31);
+}
+
+// One CTA per system, left-looking Cholesky in the reference's order (solver.hpp:222-244):
+// for column c every row r >= c forms s = a_rc - sum_{t<c} l_rt l_ct, t ascending, each
+// product and difference rounded separately -- one thread per row with the running sum in a
+// register (no trailing-matrix stores); the diagonal row checks s > 0 and every thread takes
+// the square root, the other rows divide. L is held column-major packed (column t = rows
+// t..f-1, contiguous), so a warp's l_rt loads are consecutive doubles and l_ct is a
+// broadcast. The forward substitution (solver.hpp:249-253) rides one column behind on the
+// last thread: y_{c-1} needs row c-1 of L (final once column c-1 is) and y_0..y_{c-2}.
+constexpr int SE_U = 8;  // dot products formed ahead of their in-order subtractions
+
 __global__ void solve_exact_kernel(const float* __restrict__ A, const float* __restrict__ Bv,
                                    int f, int64_t row_base, float* __restrict__ X,
                                    unsigned long long* __restrict__ min_row,
                                    int32_t* __restrict__ column, double* __restrict__ pivot,
-                                   unsigned long long* __restrict__ prof) {
+                                   double* __restrict__ work, unsigned long long* __restrict__ prof) {
 #ifdef ALSK_MEASURE
     long long t_lap = clock64();  // ALSK_SE_PROF=1: cycles per phase (thread 0), measurement builds
 #define SE_LAP(slot)                                                    \
@@ -152,41 +172,73 @@ __global__ void solve_exact_kernel(const float* __restrict__ A, const float* __r
 #define SE_LAP(slot)
 #endif
     extern __shared__ double sm[];
-    double* L = sm;                        // f(f+1)/2
-    double* s = L + f * (f + 1) / 2;       // f
-    float* xs = reinterpret_cast<float*>(s + f);
-    uint8_t* tri = reinterpret_cast<uint8_t*>(xs + f);  // (i, j) of the (f-1)-triangle, row-major
+    double* L = sm;                    // f(f+1)/2, column-major packed: l_rt at colstart(t) + r
+    double* y = L + f * (f + 1) / 2;   // f: b, overwritten by the forward solution
+    double* piv = y + f;               // the current column's pivot
     const int64_t row = blockIdx.x;
     const float* a = A + row * static_cast<int64_t>(f) * f;
     const float* b = Bv + row * f;
     float* x = X + row * f;
+    const int64_t per = subst_stride(f);
     const int tid = threadIdx.x, nt = blockDim.x;
+    // column t starts at colstart(t) - t + t = t(f-1) - t(t-1)/2 (+ r for row r)
+    auto colstart = [f](int t) { return t * (f - 1) - t * (t - 1) / 2; };
 
-    // all-zero test over the full f*f storage (solver.hpp:215-220)
+    // all-zero test over the full f*f storage (solver.hpp:215-220), then the lower triangle
     int nonzero = 0;
     for (int e = tid; e < f * f; e += nt) nonzero |= (a[e] != 0.0f);
+    {
+        const int lane = tid & 31, nw = nt >> 5;
+        for (int i = tid >> 5; i < f; i += nw)  // a warp per row (L2-warm re-read)
+            for (int j = lane; j <= i; j += 32) L[colstart(j) + i] = static_cast<double>(a[static_cast<int64_t>(i) * f + j]);
+    }
+    for (int i = tid; i < f; i += nt) y[i] = static_cast<double>(b[i]);
     if (!__syncthreads_or(nonzero)) {
         for (int i = tid; i < f; i += nt) x[i] = 0.0f;
-        if (tid == 0) column[row] = 0;
+        if (tid == 0) {
+            column[row] = 0;
+            work[subst_at(row, f, per)] = 0.0;
+        }
         return;
     }
-    for (int i = tid; i < f; i += nt) {
-        for (int j = 0; j <= i; ++j) L[pk(i, j)] = static_cast<double>(a[i * f + j]);
-        s[i] = static_cast<double>(b[i]);
-    }
-    for (int i = tid; i < f - 1; i += nt)
-        for (int j = 0; j <= i; ++j) {
-            tri[2 * pk(i, j)] = static_cast<uint8_t>(i);
-            tri[2 * pk(i, j) + 1] = static_cast<uint8_t>(j);
-        }
-    __syncthreads();
 
     SE_LAP(0)
+    const int ythr = nt - 1;
+    auto forward = [&](int i) {  // y_i = (b_i - sum_{j<i} l_ij y_j) / l_ii, j ascending
+        double acc = y[i];
+        int off = 0;
+        for (int j = 0; j < i; ++j) {
+            acc = __dsub_rn(acc, __dmul_rn(L[off + i], y[j]));
+            off += f - 1 - j;
+        }
+        y[i] = __ddiv_rn(acc, L[off + i]);
+    };
     bool broke = false;
     for (int c = 0; c < f; ++c) {
-        // every thread reads the pivot and takes its square root itself (the same value in
-        // every thread), so no single-thread phase and barrier precede the divisions
-        const double d = L[pk(c, c)];
+        for (int r = c + tid; r < f; r += nt) {
+            double acc = L[colstart(c) + r];
+            int off = 0;
+            int t = 0;
+            for (; t + SE_U <= c; t += SE_U) {  // products formed ahead; only the subtractions chain
+                double p[SE_U];
+#pragma unroll
+                for (int q = 0; q < SE_U; ++q) {
+                    p[q] = __dmul_rn(L[off + r], L[off + c]);
+                    off += f - 1 - (t + q);
+                }
+#pragma unroll
+                for (int q = 0; q < SE_U; ++q) acc = __dsub_rn(acc, p[q]);
+            }
+            for (; t < c; ++t) {
+                acc = __dsub_rn(acc, __dmul_rn(L[off + r], L[off + c]));
+                off += f - 1 - t;
+            }
+            if (r == c) *piv = acc;
+            else L[colstart(c) + r] = acc;
+        }
+        if (tid == ythr && c > 0) forward(c - 1);
+        __syncthreads();
+        const double d = *piv;
         if (!(d > 0.0)) {  // CTA-uniform
             if (tid == 0) {
                 column[row] = c + 1;
@@ -197,63 +249,70 @@ __global__ void solve_exact_kernel(const float* __restrict__ A, const float* __r
             break;
         }
         const double lcc = sqrt(d);
-        for (int r = c + 1 + tid; r < f; r += nt) L[pk(r, c)] = __ddiv_rn(L[pk(r, c)], lcc);
-        __syncthreads();  // every thread has read d: the diagonal can take L[c][c] now
-        if (tid == 0) L[pk(c, c)] = lcc;
-        // trailing update of entries (r, q), c < q <= r, enumerated flat over the threads
-        // (row-major lower triangle: entry k of the (f-c-1)-triangle is tri[k]; the first
-        // T(T+1)/2 entries of the largest triangle are exactly the smaller ones), so short
-        // rows leave no lanes idle. Each entry still takes its updates in ascending c, one
-        // separately rounded multiply-subtract per column: the reference's order.
-        const int T = f - c - 1, nent = T * (T + 1) / 2;
-        for (int k = tid; k < nent; k += nt) {
-            const int r = c + 1 + tri[2 * k], q = c + 1 + tri[2 * k + 1];
-            const int rb = r * (r + 1) / 2;
-            L[rb + q] = __dsub_rn(L[rb + q], __dmul_rn(L[rb + c], L[q * (q + 1) / 2 + c]));
-        }
+        for (int r = c + 1 + tid; r < f; r += nt) L[colstart(c) + r] = __ddiv_rn(L[colstart(c) + r], lcc);
+        if (tid == 0) L[colstart(c) + c] = lcc;
         __syncthreads();
     }
     SE_LAP(1)
     if (broke) {
         for (int i = tid; i < f; i += nt) x[i] = 0.0f;
+        if (tid == 0) work[subst_at(row, f, per)] = 0.0;
         return;
     }
+    if (tid == ythr) forward(f - 1);
     if (tid == 0) column[row] = 0;
-    // forward substitution, column oriented: s_i -= L[i][j]*y_j for j ascending
-    // (same per-entry order as the reference's row-oriented loop, solver.hpp:249-253).
-    if (tid < 32) {
-        for (int j = 0; j < f; ++j) {
-            const double yj = __ddiv_rn(s[j], L[pk(j, j)]);
-            __syncwarp();
-            if (tid == 0) s[j] = yj;
-            for (int i = j + 1 + tid; i < f; i += 32) s[i] = __dsub_rn(s[i], __dmul_rn(L[pk(i, j)], yj));
-            __syncwarp();
-        }
-        SE_LAP(2)
-        // back substitution reads the already-rounded float x[j] (solver.hpp:254-259);
-        // its order (j ascending from i+1) is inherently sequential.
-        // Products of 8 consecutive j are formed ahead of their (in-order) subtractions, so
-        // only the subtraction chain is serial.
-        if (tid == 0) {
-            for (int i = f - 1; i >= 0; --i) {
-                double acc = s[i];
-                int j = i + 1;
-                for (; j + 8 <= f; j += 8) {
-                    double p[8];
-#pragma unroll
-                    for (int u = 0; u < 8; ++u) p[u] = __dmul_rn(L[pk(j + u, i)], static_cast<double>(xs[j + u]));
-#pragma unroll
-                    for (int u = 0; u < 8; ++u) acc = __dsub_rn(acc, p[u]);
-                }
-                for (; j < f; ++j) acc = __dsub_rn(acc, __dmul_rn(L[pk(j, i)], static_cast<double>(xs[j])));
-                xs[i] = static_cast<float>(__ddiv_rn(acc, L[pk(i, i)]));
-            }
-        }
-        __syncwarp();
-        SE_LAP(3)
-        for (int i = tid; i < f; i += 32) x[i] = xs[i];
+    __syncthreads();
+    SE_LAP(2)
+    // hand off to backsub_exact_kernel: y, then per row i (descending) the diagonal and
+    // column i below it -- one contiguous run of the column-major L
+    double* wk = work + subst_at(row, 0, per);
+    for (int i = tid; i < f; i += nt) wk[32 * i] = y[i];
+    int64_t e = f;
+    for (int i = f - 1; i >= 0; --i) {
+        const int n = f - i;
+        const double* col = L + colstart(i) + i;
+        for (int jj = tid; jj < n; jj += nt) wk[32 * (e + jj)] = col[jj];
+        e += n;
     }
+    SE_LAP(3)
 #undef SE_LAP
+}
+
+// Back substitution, one thread per system (solver.hpp:254-259): for i = f-1 down to 0,
+// x_i = float((y_i - sum_{j>i} L[j][i] * double(x_j)) / L[i][i]), the sum subtracted in
+// ascending j, each product and difference rounded separately -- the reference's order,
+// inherently one chain per system, so systems run side by side (thousands per SM) instead
+// of on one thread of a CTA. x lives in shared memory, [j][thread] (conflict-free).
+__global__ void __launch_bounds__(128) backsub_exact_kernel(const double* __restrict__ work, int f, int64_t count,
+                                                            float* __restrict__ X) {
+    extern __shared__ float xsh[];
+    const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (t >= count) return;
+    const int64_t per = subst_stride(f);
+    const double* y = work + subst_at(t, 0, per);  // element e at y[32 * e]
+    const double* u = y + 32 * f;
+    if (!(u[0] > 0.0)) return;  // all-zero or broken system: x already written
+    float* xs = xsh + threadIdx.x;
+    const int bd = blockDim.x;
+    for (int i = f - 1; i >= 0; --i) {
+        const double d = u[0];
+        double acc = y[32 * i];
+        const double* c = u + 32;
+        const int n = f - 1 - i;
+        int k = 0;
+        for (; k + 8 <= n; k += 8) {  // products formed ahead; only the subtractions chain
+            double p[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) p[q] = __dmul_rn(c[32 * (k + q)], static_cast<double>(xs[(i + 1 + k + q) * bd]));
+#pragma unroll
+            for (int q = 0; q < 8; ++q) acc = __dsub_rn(acc, p[q]);
+        }
+        for (; k < n; ++k) acc = __dsub_rn(acc, __dmul_rn(c[32 * k], static_cast<double>(xs[(i + 1 + k) * bd])));
+        xs[i * bd] = static_cast<float>(__ddiv_rn(acc, d));
+        u += 32 * (n + 1);
+    }
+    float* x = X + t * f;
+    for (int i = 0; i < f; ++i) x[i] = xs[i * bd];
 }
 
 }  // namespace
@@ -339,13 +398,20 @@ void solve_exact(const float* A, const float* B, int64_t count, int f, bool /*ze
                  float* X, const SolveStatus& st, cudaStream_t s) {
     // Both policies write a zero row for a broken system; the host raises for `fail`.
     if (count <= 0) return;
-    const size_t smem = (static_cast<size_t>(f) * (f + 1) / 2 + f) * sizeof(double) + f * sizeof(float) +
-                        static_cast<size_t>(f) * (f - 1) + 16;  // + the (f-1)-triangle's (i, j) bytes
+    const size_t smem = (static_cast<size_t>(f) * (f + 1) / 2 + f + 1) * sizeof(double);
     if (f > 256 || smem > 220 * 1024) fail_input("rank " + std::to_string(f) + " too large for device solve");
     ALSK_CUDA(cudaFuncSetAttribute(solve_exact_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const int threads = f <= 32 ? 32 : (f <= 64 ? 64 : 128);
-    for (int64_t b0 = 0; b0 < count; b0 += (1LL << 30)) {
-        const int64_t n = std::min<int64_t>(count - b0, 1LL << 30);
+    // the hand-off scratch bounds a launch: ~4 GB of (y, L) streams at a time, whole groups
+    // of 32 systems
+    const int64_t per = subst_stride(f);
+    const int64_t chunk = std::max<int64_t>(32, std::min<int64_t>(1LL << 30, (int64_t{4} << 30) / (per * 8)) & ~int64_t{31});
+    DevBuf work(sizeof(double) * per * ((std::min(count, chunk) + 31) & ~int64_t{31}), s);
+    constexpr int BT = 128;
+    const size_t bsmem = static_cast<size_t>(BT) * f * sizeof(float);
+    ALSK_CUDA(cudaFuncSetAttribute(backsub_exact_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsmem));
+    for (int64_t b0 = 0; b0 < count; b0 += chunk) {
+        const int64_t n = std::min<int64_t>(count - b0, chunk);
         static const bool want_prof = measure_env("ALSK_SE_PROF") != nullptr;
         DevBuf pb;
         if (want_prof) {
@@ -355,13 +421,16 @@ void solve_exact(const float* A, const float* B, int64_t count, int f, bool /*ze
         solve_exact_kernel<<<static_cast<unsigned>(n), threads, smem, s>>>(
             A + static_cast<size_t>(b0) * f * f, B + static_cast<size_t>(b0) * f, f,
             b0, X + static_cast<size_t>(b0) * f, st.min_row, st.column + b0,
-            st.pivot + b0, want_prof ? pb.as<unsigned long long>() : nullptr);
+            st.pivot + b0, work.as<double>(), want_prof ? pb.as<unsigned long long>() : nullptr);
+        ALSK_LAUNCHED();
+        backsub_exact_kernel<<<static_cast<unsigned>((n + BT - 1) / BT), BT, bsmem, s>>>(
+            work.as<double>(), f, n, X + static_cast<size_t>(b0) * f);
         ALSK_LAUNCHED();
         if (want_prof) {
             unsigned long long h[4];
             d2h(h, pb.as<unsigned long long>(), 4, s);
             ALSK_CUDA(cudaStreamSynchronize(s));
-            std::fprintf(stderr, "[se-prof f=%d systems=%lld threads=%d] kcyc per system: load %.1f factor %.1f forward %.1f back %.1f\n",
+            std::fprintf(stderr, "[se-prof f=%d systems=%lld threads=%d] kcyc per system: load %.1f factor+forward %.1f last row %.1f hand-off %.1f\n",
                          f, static_cast<long long>(n), threads, h[0] / 1e3 / n, h[1] / 1e3 / n, h[2] / 1e3 / n,
                          h[3] / 1e3 / n);
         }

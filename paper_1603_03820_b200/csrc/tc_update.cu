@@ -330,7 +330,22 @@ tc_update_kernel(const float* __restrict__ theta, int ldt, const int64_t* __rest
                     raw_vals[s * KC + lane] = rv;
                     if (lane == 0) raw_info[s] = ci;
                 }
-                if (ci.cnt > 0) {
+                if (ci.cnt > 0 && (dry & 128u)) {
+                    // lane = 16-byte piece: one coalesced row per instruction, loader ldr
+                    // takes rows ldr, ldr + NLOAD, ...; padding rows of the last k-group zeroed
+                    const int kend = (ci.cnt + 7) & ~7;
+                    for (int i = ldr; i < kend; i += NLOAD) {
+                        const int vi = __shfl_sync(0xffffffffu, v, i);
+                        uint8_t* rowp = stage + i * rs4;
+                        if (i < ci.cnt) {
+                            const float* src = theta + static_cast<int64_t>(vi) * ldt;
+                            for (int c = lane; c < n16; c += 32) cp_async16_ca(smem_u32(rowp + c * 16), src + 4 * c);
+                        } else {
+                            for (int c = lane; c < n16; c += 32)
+                                *reinterpret_cast<float4*>(rowp + c * 16) = make_float4(0.f, 0.f, 0.f, 0.f);
+                        }
+                    }
+                } else if (ci.cnt > 0) {
                     // lane = rating slot: each lane streams its own factor row, 16 bytes per
                     // instruction; padding slots of the last k-group get zeros
                     const int kend = (ci.cnt + 7) & ~7;
