@@ -56,16 +56,30 @@ __global__ void herm_mat_kernel(const int64_t* __restrict__ row_ptr,
     for (int64_t k = k0; k < k1; k += kChunk) {
         const int cnt = static_cast<int>(((k1 - k) < kChunk ? (k1 - k) : (int64_t)kChunk));
         __syncthreads();
-        for (int e = threadIdx.x; e < cnt * fp; e += blockDim.x) {
-            const int kk = e / fp, c = e - kk * fp;
-            float v = 0.f;
-            if (c < f) {
+        // a warp per staged rating, lanes over the features: no index division, and each
+        // lane's loads of a round are issued before its stores (double-buffering the tile
+        // with cp.async measured slower: 9.85 vs 9.70 ms per Netflix launch)
+        {
+            const int lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+            for (int kk = threadIdx.x >> 5; kk < cnt; kk += nw) {
                 const int64_t row = static_cast<int64_t>(col_idx[k + kk]) - col_lo;
-                v = theta[row * f + c];
-            } else if (c == f) {
-                v = values[k + kk];
+                const float rv = values[k + kk];
+                const float* src = theta + row * f;
+                float* dst = tile + kk * fp;
+                for (int c0 = 0; c0 < fp; c0 += 128) {
+                    float v[4];
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const int c = c0 + lane + 32 * q;
+                        v[q] = c < f ? src[c] : (c == f ? rv : 0.f);
+                    }
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const int c = c0 + lane + 32 * q;
+                        if (c < fp) dst[c] = v[q];
+                    }
+                }
             }
-            tile[kk * fp + c] = v;
         }
         __syncthreads();
         if (active) {
