@@ -40,6 +40,8 @@
 // registers with LDG is ~25 cycles per row in isolation, but inside this kernel (gather
 // fused into the split warps, 3 chunks in flight) it measured 2.3x slower than the cp.async
 // ring, as did st.async staging (75 cycles per row in isolation).
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -66,26 +68,24 @@ constexpr int NSPLIT = 12;                // split warps (8 and 16 measured ~1% 
 constexpr int NG = 1;                     // epilogue groups (two measured 1% slower once the epilogue
                                           // lost its transpose; with it, one was 12% slower)
 constexpr int W_SPLIT = 4 * NG, W_MMA = W_SPLIT + NSPLIT, W_LOAD = W_MMA + 1;
-constexpr int NLOAD = 4;                  // loader warps
+constexpr int NLOAD = 1;                  // loader warp (TMA gather issue)
 constexpr int NWARPS = W_LOAD + NLOAD;
 constexpr int NTHREADS = 32 * NWARPS;     // 4*NG epilogue + NSPLIT split + MMA + NLOAD loader warps
 constexpr int TMEM_COLS = 512;           // two buffers x 256 columns (D0 @ +0, D1 @ +NF)
 
 // ---- shared-memory plan (host and device agree) ----
-// Staged factor rows keep the caller's row length rounded to 4 (mod 8) floats: with an odd
-// number of 16-byte chunks per row, a quarter-warp reading one chunk of 8 consecutive rows
-// touches 8 distinct bank groups.
-__host__ __device__ inline int staging_stride(int ldt) { return (ldt % 8 == 4) ? ldt : ldt + 4; }
+// A stage holds KC gathered factor rows as KC/4 TMA gather4 groups: 4 rows of ldt floats
+// back to back, each group padded to a 128-byte boundary (the TMA destination alignment).
+__host__ __device__ inline int group_stride(int ldt) { return (16 * ldt + 127) & ~127; }
 
 struct TcPlan {
-    int f, sld, stages, nb, hls, rs, raw_bytes;
+    int f, stages, nb, hls, gs, raw_bytes;
     int s_floats, grp_floats;
     size_t hl_off, ring_bytes, grp_bytes, bar_off, info_off, total;
     __host__ __device__ TcPlan(int f_, int nb_, int stages_, int ldt, int hls_)
         : f(f_), stages(stages_), nb(nb_), hls(hls_) {
-        rs = staging_stride(ldt);
-        raw_bytes = (KC * rs * 4 + 127) & ~127;
-        sld = 0;
+        gs = group_stride(ldt);
+        raw_bytes = (KC / 4) * gs;
         s_floats = static_cast<int>(packed_stride(f));  // segment sums, panel-blocked (kernels.cuh)
         grp_floats = s_floats;
         hl_off = (static_cast<size_t>(stages) * raw_bytes + 1023) & ~static_cast<size_t>(1023);  // UMMA atoms: 1 KB
@@ -96,6 +96,17 @@ struct TcPlan {
         total = info_off + static_cast<size_t>(stages) * (KC * 4 + 16) + hls * 16 + 1024;  // + align slack
     }
 };
+
+// 4 factor rows (r0..r3, full width) into shared memory by one TMA gather, completion as
+// transaction bytes on `bar`; rows at or past the map's row count arrive as zeros
+__device__ __forceinline__ void tma_gather4(uint32_t dst, const CUtensorMap* map, int r0, int r1, int r2, int r3,
+                                            uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(0), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(smem_u32(bar))
+        : "memory");
+}
 
 // spin (ns == 0) or nanosleep back-off
 __device__ __forceinline__ void tc_wait(uint64_t* bar, uint32_t parity, uint32_t ns) {
@@ -206,7 +217,7 @@ enum { MODE_FULL = 1, MODE_PACKED = 2 };
 
 template <int NB, int MODE>
 __global__ void __launch_bounds__(NTHREADS, 1)
-tc_update_kernel(const float* __restrict__ theta, int ldt, const int64_t* __restrict__ row_ptr,
+tc_update_kernel(const __grid_constant__ CUtensorMap theta_map, int ldt, const int64_t* __restrict__ row_ptr,
                  const int32_t* __restrict__ col_idx, const float* __restrict__ values, int64_t col_lo, int theta_last, int f,
                  float lambda, int64_t rb, int64_t nrows, int stages, float* __restrict__ out_a,
                  float* __restrict__ out_b, long long* __restrict__ prof, int hls, uint32_t epi_sleep,
@@ -247,7 +258,7 @@ tc_update_kernel(const float* __restrict__ theta, int ldt, const int64_t* __rest
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
         for (int s = 0; s < stages; ++s) {
-            mbar_init(&raw_full[s], 32 * NLOAD + 1);  // NLOAD x 32 cp.async arrivals + the publishing lane
+            mbar_init(&raw_full[s], 1);  // the loader's arrival (+ the gathers' transaction bytes)
             mbar_init(&raw_empty[s], NSPLIT);
         }
         for (int s = 0; s < HL_STAGES; ++s) {
@@ -269,17 +280,17 @@ tc_update_kernel(const float* __restrict__ theta, int ldt, const int64_t* __rest
     if (prof) tp0 = clock64();
 
     if (warp >= W_LOAD) {
-        // ---------------- loaders (the only readers of the CSR arrays) ----------------
-        // NLOAD warps walk the same chunk sequence; loader ld copies the 16-byte pieces
-        // ld, ld+NLOAD, ... of every gathered row, loader 0 also publishes ratings and metadata.
-        // A 4-deep register queue holds the column indices and ratings of upcoming chunks, so
-        // their global loads are in flight long before the chunk is staged. Each factor row
-        // is copied by cp.async (LDGSTS, 16 bytes per lane, one coalesced row per
-        // instruction) and completion is counted on the stage's mbarrier per lane.
+        // ---------------- loader (the only reader of the CSR arrays) ----------------
+        // Walks the chunk sequence, lane = rating slot. A 4-deep register queue holds the
+        // column indices and ratings of upcoming chunks, so their global loads are in flight
+        // long before the chunk is staged. The factor rows are fetched by TMA: lanes 0..7
+        // issue one tile::gather4 each (rows 4g..4g+3 of the chunk), completion counted as
+        // transaction bytes on the stage's mbarrier; the padding slots of the last k-group
+        // gather row `theta_rows` (past the map) and arrive as zeros. No per-lane copies:
+        // the LSU/L1 stays free for the split warps.
         constexpr int D = 4;
-        const int ldr = warp - W_LOAD;
-        const int n16 = ldt >> 2;  // 16-byte pieces per factor row
-        const int rs4 = P.rs * 4;
+        const int oob_row = theta_last + 1;
+        const uint32_t row_bytes = static_cast<uint32_t>(ldt) * 4u;
         ChunkWalker w(row_ptr, rb, nrows);
         ChunkInfo qi[D];
         int qc[D];
@@ -299,15 +310,16 @@ tc_update_kernel(const float* __restrict__ theta, int ldt, const int64_t* __rest
         // register holding an in-flight load is next read D chunks later, so the loads never
         // stall the loop.
         bool done = false;
-        for (uint32_t ctr0 = 0; !done; ctr0 += D) {
+        int ring_s = 0;  // stage and phase of the ring position (no runtime division per chunk)
+        uint32_t ring_ph = 0;
+        for (;;) {
 #pragma unroll
             for (int d = 0; d < D; ++d) {
                 if (done) break;
-                const uint32_t ctr = ctr0 + d;
                 const ChunkInfo ci = qi[d];
                 // never gather outside Theta: an out-of-partition column is reported by the
                 // caller's column check (solver.hpp:120-123), possibly after this launch
-                const int v = min(max(qc[d] - static_cast<int>(col_lo), 0), theta_last);
+                const int v = lane < ci.cnt ? min(max(qc[d] - static_cast<int>(col_lo), 0), theta_last) : oob_row;
                 const float rv = qv[d];
                 qi[d] = w.info();
                 qc[d] = 0;
@@ -318,56 +330,30 @@ tc_update_kernel(const float* __restrict__ theta, int ldt, const int64_t* __rest
                 }
                 if (w.valid()) w.advance();
 
-                const int s = ctr % stages;
-                const uint32_t ph = (ctr / stages) & 1u;
+                const int s = ring_s;
+                const uint32_t ph = ring_ph;
                 {
                     TP(t0);
                     mbar_wait_sleep(&raw_empty[s], ph ^ 1u, load_sleep);
                     TA(t0, 0);
                 }
-                uint8_t* stage = ring + s * RAW;
-                if (ldr == 0) {
-                    raw_vals[s * KC + lane] = rv;
-                    if (lane == 0) raw_info[s] = ci;
-                }
-                if (ci.cnt > 0 && (dry & 128u)) {
-                    // lane = 16-byte piece: one coalesced row per instruction, loader ldr
-                    // takes rows ldr, ldr + NLOAD, ...; padding rows of the last k-group zeroed
-                    const int kend = (ci.cnt + 7) & ~7;
-                    for (int i = ldr; i < kend; i += NLOAD) {
-                        const int vi = __shfl_sync(0xffffffffu, v, i);
-                        uint8_t* rowp = stage + i * rs4;
-                        if (i < ci.cnt) {
-                            const float* src = theta + static_cast<int64_t>(vi) * ldt;
-                            for (int c = lane; c < n16; c += 32) cp_async16_ca(smem_u32(rowp + c * 16), src + 4 * c);
-                        } else {
-                            for (int c = lane; c < n16; c += 32)
-                                *reinterpret_cast<float4*>(rowp + c * 16) = make_float4(0.f, 0.f, 0.f, 0.f);
-                        }
-                    }
-                } else if (ci.cnt > 0) {
-                    // lane = rating slot: each lane streams its own factor row, 16 bytes per
-                    // instruction; padding slots of the last k-group get zeros
-                    const int kend = (ci.cnt + 7) & ~7;
-                    uint8_t* my = stage + lane * rs4;
-                    if (lane < ci.cnt) {
-                        const float* src = theta + static_cast<int64_t>(v) * ldt;
-                        const uint32_t dst = smem_u32(my);
-                        if (dry & 64u) {
-                            for (int c = ldr; c < n16; c += NLOAD) cp_async16(dst + c * 16, src + 4 * c);
-                        } else {
-                            for (int c = ldr; c < n16; c += NLOAD) cp_async16_ca(dst + c * 16, src + 4 * c);
-                        }
-                    } else if (lane < kend) {
-                        for (int c = ldr; c < n16; c += NLOAD)
-                            *reinterpret_cast<float4*>(my + c * 16) = make_float4(0.f, 0.f, 0.f, 0.f);
-                    }
-                }
-                cp_async_arrive_noinc(&raw_full[s]);
+                raw_vals[s * KC + lane] = rv;
+                if (lane == 0) raw_info[s] = ci;
+                const int ngrp = ci.cnt > 0 ? ((ci.cnt + 7) & ~7) >> 2 : 0;
+                const int g = lane & 7;
+                const int r0 = __shfl_sync(0xffffffffu, v, 4 * g), r1 = __shfl_sync(0xffffffffu, v, 4 * g + 1);
+                const int r2 = __shfl_sync(0xffffffffu, v, 4 * g + 2), r3 = __shfl_sync(0xffffffffu, v, 4 * g + 3);
                 __syncwarp();
-                if (ldr == 0 && lane == 0) mbar_arrive(&raw_full[s]);
+                if (lane == 0) {
+                    if (ngrp > 0) mbar_expect_tx(&raw_full[s], static_cast<uint32_t>(ngrp) * 4u * row_bytes);
+                    else mbar_arrive(&raw_full[s]);
+                }
+                __syncwarp();
+                if (lane < ngrp) tma_gather4(smem_u32(ring + s * RAW + lane * P.gs), &theta_map, r0, r1, r2, r3, &raw_full[s]);
                 if (ci.cnt < 0) done = true;
+                if (++ring_s == stages) ring_s = 0, ring_ph ^= 1u;
             }
+            if (done) break;
         }
     } else if (warp >= W_SPLIT && warp < W_MMA) {
         // ---------------- split warps ----------------
@@ -375,7 +361,7 @@ tc_update_kernel(const float* __restrict__ theta, int ldt, const int64_t* __rest
         // Every offset below is a per-thread constant plus a multiple of t.
         const int pw = warp - W_SPLIT;
         const int k = lane;
-        const uint32_t raw_k = static_cast<uint32_t>(k * P.rs * 4 + pw * 16);
+        const uint32_t raw_k = static_cast<uint32_t>((k >> 2) * P.gs + (k & 3) * ldt * 4 + pw * 16);
         uint32_t kq[4];
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
@@ -392,15 +378,18 @@ tc_update_kernel(const float* __restrict__ theta, int ldt, const int64_t* __rest
         constexpr int NC16 = 2 * NB;              // 16-byte feature chunks below 8*NB
         constexpr int TPW = (NC16 + NSPLIT - 1) / NSPLIT;  // chunks per split warp (upper bound)
         const int nc16 = NC16 < (NF >> 2) ? NC16 : (NF >> 2);  // never spill H rows into the L half
-        for (uint32_t ctr = 0;; ++ctr) {
-            const int s = ctr % stages;
-            const int hs = ctr % HL_STAGES;
+        int ring_s = 0, ring_hs = 0;
+        uint32_t ring_ph = 0, ring_hph = 0;
+        for (;; ring_s = ring_s + 1 == stages ? (ring_ph ^= 1u, 0) : ring_s + 1,
+                ring_hs = ring_hs + 1 == HL_STAGES ? (ring_hph ^= 1u, 0) : ring_hs + 1) {
+            const int s = ring_s;
+            const int hs = ring_hs;
             TP(t0);
-            tc_wait(&raw_full[s], (ctr / stages) & 1u, split_sleep);
+            tc_wait(&raw_full[s], ring_ph, split_sleep);
             TA(t0, 0);
             const ChunkInfo ci = raw_info[s];
             TP(t1);
-            tc_wait(&hl_empty[hs], ((ctr / HL_STAGES) & 1u) ^ 1u, split_sleep);
+            tc_wait(&hl_empty[hs], ring_hph ^ 1u, split_sleep);
             TA(t1, 1);
             TP(t2);
             if (ci.cnt >= 0 && !(dry & 1u)) {
@@ -448,12 +437,14 @@ tc_update_kernel(const float* __restrict__ theta, int ldt, const int64_t* __rest
         // ---------------- MMA issuer ----------------
         const uint32_t idesc = idesc_tf32(128, 2 * NF), idesc1 = idesc_tf32(128, NF);
         uint32_t job = 0;
-        for (uint32_t ctr = 0;; ++ctr) {
-            const int hs = ctr % HL_STAGES;
+        int ring_hs = 0;
+        uint32_t ring_hph = 0;
+        for (;; ring_hs = ring_hs + 1 == HL_STAGES ? (ring_hph ^= 1u, 0) : ring_hs + 1) {
+            const int hs = ring_hs;
             // every lane waits (a lane-0-only wait followed by a warp shuffle measured ~700
             // cycles of reconvergence per chunk)
             TP(t0);
-            tc_wait(&hl_full[hs], (ctr / HL_STAGES) & 1u, mma_sleep);
+            tc_wait(&hl_full[hs], ring_hph, mma_sleep);
             TA(t0, 0);
             const ChunkInfo ci = hl_info[hs];
             if (ci.cnt < 0) break;
@@ -610,6 +601,44 @@ tc_update_kernel(const float* __restrict__ theta, int ldt, const int64_t* __rest
 }
 
 // ---- host side ----
+// TMA map of the factor rows for the loader's gathers: rows x ldt floats, one row per box
+// row, out-of-range rows read as zeros. A factor without rows maps a zeroed dummy row (only
+// empty rows can then be valid; anything else fails the caller's column check).
+CUtensorMap factor_rows_map(const float* theta, int64_t theta_rows, int ldt) {
+    static const PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        ALSK_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+        if (!fn || q != cudaDriverEntryPointSuccess) throw Failure(ALSK_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+        return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }();
+    const void* base = theta;
+    int64_t rows = theta_rows;
+    if (!theta || theta_rows < 1) {
+        static std::mutex mu;
+        static std::vector<void*> dummies;  // per device, process lifetime (512 zero bytes)
+        int dev = 0;
+        ALSK_CUDA(cudaGetDevice(&dev));
+        std::lock_guard<std::mutex> lock(mu);
+        if (dummies.size() <= static_cast<size_t>(dev)) dummies.resize(dev + 1, nullptr);
+        if (!dummies[dev]) {
+            ALSK_CUDA(cudaMalloc(&dummies[dev], 512));
+            ALSK_CUDA(cudaMemset(dummies[dev], 0, 512));
+        }
+        base = dummies[dev];
+        rows = 1;
+    }
+    CUtensorMap m;
+    const cuuint64_t dims[2] = {static_cast<cuuint64_t>(ldt), static_cast<cuuint64_t>(rows)};
+    const cuuint64_t strides[1] = {static_cast<cuuint64_t>(ldt) * 4};
+    const cuuint32_t box[2] = {static_cast<cuuint32_t>(ldt), 1}, es[2] = {1, 1};
+    const CUresult rc = encode(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), dims, strides, box, es,
+                               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (rc != CUDA_SUCCESS) throw Failure(ALSK_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string(static_cast<int>(rc)) + ")");
+    return m;
+}
+
 template <int NB, int MODE>
 void launch_tc(const DevCsr& r, const float* theta, int64_t theta_rows, int f, int ldt, float lambda, int64_t rb,
                int64_t re, float* x, float* a, float* b, const SolveStatus* st, cudaStream_t s) {
@@ -620,7 +649,7 @@ void launch_tc(const DevCsr& r, const float* theta, int64_t theta_rows, int f, i
     }();
     static const int max_stages = [] {
         const char* e = measure_env("ALSK_TC_STAGES");
-        return e ? std::max(2, std::min(8, std::atoi(e))) : 6;  // 4-6 within noise (6 best with cp.async.ca), 3, 2, 7 slower
+        return e ? std::max(2, std::min(8, std::atoi(e))) : 8;  // 8 vs 6: -0.3 ms per half with the TMA loader
     }();
     int hls = max_hls, stages = max_stages;
     for (;;) {
@@ -656,7 +685,8 @@ void launch_tc(const DevCsr& r, const float* theta, int64_t theta_rows, int f, i
         prof.alloc(sizeof(long long) * grid * NWARPS * 6, s);
         ALSK_CUDA(cudaMemsetAsync(prof.as<void>(), 0, sizeof(long long) * grid * NWARPS * 6, s));
     }
-    k<<<grid, NTHREADS, P.total, s>>>(theta, ldt, r.row_ptr, r.col_idx, r.values, r.col_offset,
+    const CUtensorMap map = factor_rows_map(theta, theta_rows, ldt);
+    k<<<grid, NTHREADS, P.total, s>>>(map, ldt, r.row_ptr, r.col_idx, r.values, r.col_offset,
                                        static_cast<int>(std::max<int64_t>(theta_rows, 1) - 1), f, lambda, rb, nrows, stages,
                                        a, b, want_prof ? prof.as<long long>() : nullptr, hls, sleeps[0], sleeps[1],
                                        sleeps[2], sleeps[3], dry);
