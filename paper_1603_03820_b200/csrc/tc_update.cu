@@ -69,6 +69,9 @@ constexpr int NG = 1;                     // epilogue groups (two measured 1% sl
                                           // lost its transpose; with it, one was 12% slower)
 constexpr int W_SPLIT = 4 * NG, W_MMA = W_SPLIT + NSPLIT, W_LOAD = W_MMA + 1;
 constexpr int NLOAD = 1;                  // loader warp (TMA gather issue)
+#ifndef TC_QUEUE
+#define TC_QUEUE 8                        // chunks of CSR indices/ratings in flight in the loader
+#endif
 constexpr int NWARPS = W_LOAD + NLOAD;
 constexpr int NTHREADS = 32 * NWARPS;     // 4*NG epilogue + NSPLIT split + MMA + NLOAD loader warps
 constexpr int TMEM_COLS = 512;           // two buffers x 256 columns (D0 @ +0, D1 @ +NF)
@@ -288,7 +291,7 @@ tc_update_kernel(const __grid_constant__ CUtensorMap theta_map, int ldt, const i
         // transaction bytes on the stage's mbarrier; the padding slots of the last k-group
         // gather row `theta_rows` (past the map) and arrive as zeros. No per-lane copies:
         // the LSU/L1 stays free for the split warps.
-        constexpr int D = 4;
+        constexpr int D = TC_QUEUE;
         const int oob_row = theta_last + 1;
         const uint32_t row_bytes = static_cast<uint32_t>(ldt) * 4u;
         ChunkWalker w(row_ptr, rb, nrows);
