@@ -19,7 +19,7 @@
 // added into a per-group shared-memory row (panel-blocked lower triangle) with
 // round-to-nearest FP32 adds.
 //
-// Warp roles (672 threads, 1 CTA per SM, rows j = blockIdx.x + t*gridDim.x):
+// Warp roles (576 threads, 1 CTA per SM, rows j = blockIdx.x + t*gridDim.x):
 //   warps 0-3  : the epilogue group (NG = 1; the code supports NG groups taking rows
 //                t % NG). Lane i reads row i's lower cells from TMEM (segment sums in shared
 //                memory) and writes A_u + lambda n_u and B_u to HBM, 32 bytes per lane and
@@ -28,18 +28,22 @@
 //                write them transposed into the K-major operand tile (lane = rating), with
 //                zero padding of partial k-groups.
 //   warp 16    : MMA issuer (one thread), owns the TMEM allocation (2 buffers x 256 columns).
-//   warps 17-20: loaders: the only readers of the CSR arrays (4-chunk register prefetch queue);
-//                lane = rating slot, each lane copies 16-byte pieces of its gathered factor
-//                row with cp.async into a rating-major staging ring, completion counted per
-//                lane on the stage mbarrier (cp.async.mbarrier.arrive.noinc).
-// Pipelines: staging ring (raw_full / raw_empty, 6 deep), operand ring (hl_full / hl_empty,
+//   warp 17    : loader, the only reader of the CSR arrays (8-chunk register prefetch queue of
+//                column indices and ratings); the factor rows arrive by TMA tile::gather4, four
+//                rows per instruction, into a staging ring of 4-row groups, completion counted
+//                as transaction bytes on the stage mbarrier. Padding rows of a partial k-group
+//                gather a row past the tensor map and arrive as zeros.
+// Pipelines: staging ring (raw_full / raw_empty, 8 deep), operand ring (hl_full / hl_empty,
 // 2 deep, released by tcgen05.commit; deeper rings measured slower) and the TMEM double
-// buffer (tfull / tempty), one TMEM job per row segment.
-// The gather is the bound: ~46 cycles per 400-byte row per SM through cp.async into shared
-// memory, L2- or HBM-resident alike (scripts/probes/gather_probe.cu). Gathering into
-// registers with LDG is ~25 cycles per row in isolation, but inside this kernel (gather
-// fused into the split warps, 3 chunks in flight) it measured 2.3x slower than the cp.async
-// ring, as did st.async staging (75 cycles per row in isolation).
+// buffer (tfull / tempty), one TMEM job per row segment. Ring positions are kept as counters
+// (a runtime `% stages` per chunk in every role cost ~10% of the issue slots).
+// The gather is not the bound any more: with per-lane cp.async (lane = rating, 16 bytes per
+// instruction, 32 rows touched by each) the L1 handled one 16-byte request per clock and the
+// loaders were busy ~90% of the kernel; TMA gather4 moves a 400-byte row in ~6 cycles per SM
+// in isolation (scripts/probes/l2bw_probe.cu mode 7). What remains is the tensor pipe (the
+// MMA issuer is busy ~46% of the kernel: 2.75 MFLOP of tcgen05 work per 32-rating chunk at
+// f = 100, 8x the algorithmic flops because of M = 128 padding and the three split
+// products) and the split warps' shared-memory traffic (~49%), overlapping imperfectly.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
