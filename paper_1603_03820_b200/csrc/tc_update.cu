@@ -68,11 +68,17 @@ constexpr int KC = 32;                   // ratings per stage (four k-groups of 
 constexpr int HL_BYTES = 256 * KC * 4;      // 32 KB: H rows [0,NF) then L rows [NF,2NF), K-major
 constexpr int HL_STAGES_MAX = 2;           // operand-ring depth (measured: 2 58.5, 3 59.8, 4 60.2 ms/iter)
 constexpr int SEG_CHUNKS = 16;              // TMEM accumulation segment: 16 x 32 ratings
-constexpr int NSPLIT = 12;                // split warps (8 and 16 measured ~1% slower)
+#ifndef TC_NSPLIT
+#define TC_NSPLIT 12
+#endif
+constexpr int NSPLIT = TC_NSPLIT;                // split warps (8 and 16 measured ~1% slower)
 constexpr int NG = 1;                     // epilogue groups (two measured 1% slower once the epilogue
                                           // lost its transpose; with it, one was 12% slower)
 constexpr int W_SPLIT = 4 * NG, W_MMA = W_SPLIT + NSPLIT, W_LOAD = W_MMA + 1;
-constexpr int NLOAD = 1;                  // loader warp (TMA gather issue)
+#ifndef TC_NLOAD
+#define TC_NLOAD 1
+#endif
+constexpr int NLOAD = TC_NLOAD;           // loader warps (each issues its share of a chunk's TMA gathers)
 #ifndef TC_QUEUE
 #define TC_QUEUE 8                        // chunks of CSR indices/ratings in flight in the loader
 #endif
@@ -265,7 +271,7 @@ tc_update_kernel(const __grid_constant__ CUtensorMap theta_map, int ldt, const i
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
         for (int s = 0; s < stages; ++s) {
-            mbar_init(&raw_full[s], 1);  // the loader's arrival (+ the gathers' transaction bytes)
+            mbar_init(&raw_full[s], NLOAD);  // one arrival per loader warp (+ the gathers' transaction bytes)
             mbar_init(&raw_empty[s], NSPLIT);
         }
         for (int s = 0; s < HL_STAGES; ++s) {
@@ -296,6 +302,7 @@ tc_update_kernel(const __grid_constant__ CUtensorMap theta_map, int ldt, const i
         // gather row `theta_rows` (past the map) and arrive as zeros. No per-lane copies:
         // the LSU/L1 stays free for the split warps.
         constexpr int D = TC_QUEUE;
+        const int ldr = warp - W_LOAD;
         const int oob_row = theta_last + 1;
         const uint32_t row_bytes = static_cast<uint32_t>(ldt) * 4u;
         ChunkWalker w(row_ptr, rb, nrows);
@@ -344,19 +351,23 @@ tc_update_kernel(const __grid_constant__ CUtensorMap theta_map, int ldt, const i
                     mbar_wait_sleep(&raw_empty[s], ph ^ 1u, load_sleep);
                     TA(t0, 0);
                 }
-                raw_vals[s * KC + lane] = rv;
-                if (lane == 0) raw_info[s] = ci;
+                if (ldr == 0) {
+                    raw_vals[s * KC + lane] = rv;
+                    if (lane == 0) raw_info[s] = ci;
+                }
+                // loader ldr issues groups g = ldr, ldr + NLOAD, ... (lane q: g = ldr + NLOAD q)
                 const int ngrp = ci.cnt > 0 ? ((ci.cnt + 7) & ~7) >> 2 : 0;
-                const int g = lane & 7;
+                const int mine = ngrp > ldr ? (ngrp - ldr + NLOAD - 1) / NLOAD : 0;
+                const int g = (ldr + NLOAD * lane) & 7;
                 const int r0 = __shfl_sync(0xffffffffu, v, 4 * g), r1 = __shfl_sync(0xffffffffu, v, 4 * g + 1);
                 const int r2 = __shfl_sync(0xffffffffu, v, 4 * g + 2), r3 = __shfl_sync(0xffffffffu, v, 4 * g + 3);
                 __syncwarp();
                 if (lane == 0) {
-                    if (ngrp > 0) mbar_expect_tx(&raw_full[s], static_cast<uint32_t>(ngrp) * 4u * row_bytes);
+                    if (mine > 0) mbar_expect_tx(&raw_full[s], static_cast<uint32_t>(mine) * 4u * row_bytes);
                     else mbar_arrive(&raw_full[s]);
                 }
                 __syncwarp();
-                if (lane < ngrp) tma_gather4(smem_u32(ring + s * RAW + lane * P.gs), &theta_map, r0, r1, r2, r3, &raw_full[s]);
+                if (lane < mine) tma_gather4(smem_u32(ring + s * RAW + g * P.gs), &theta_map, r0, r1, r2, r3, &raw_full[s]);
                 if (ci.cnt < 0) done = true;
                 if (++ring_s == stages) ring_s = 0, ring_ph ^= 1u;
             }
