@@ -106,10 +106,6 @@ __host__ __device__ inline int64_t pb_index(int f, int i, int j) {
 //  packed_solve_tiles - CUDA-core 8x8 register-tile Cholesky (chol_solve.cu).
 bool packed_solve(const float* packed, int64_t count, int f, float* x, const SolveStatus& st, int64_t status_off,
                   cudaStream_t s);
-//  packed_solve16     - the TMEM Cholesky with 16-column steps (tc_solve16.cu); false if f is
-//                       outside 16..127.
-bool packed_solve16(const float* packed, int64_t count, int f, float* x, const SolveStatus& st,
-                    int64_t status_off, cudaStream_t s);
 bool packed_solve_tiles(const float* packed, int64_t count, int f, float* x, const SolveStatus& st,
                         int64_t status_off, cudaStream_t s);
 //  warp_solve         - one system per warp in shared memory, mma.sync Schur updates

@@ -552,11 +552,6 @@ bool packed_solve(const float* packed, int64_t count, int f, float* x, const Sol
     if (!tmem && warp_solve(packed, count, f, x, st, status_off, s)) return true;
     if (f < 8 || f > 127) return packed_solve_tiles(packed, count, f, x, st, status_off, s);
     if (count <= 0) return true;
-    static const int bw = [] {  // column-step width of the TMEM Cholesky (A/B switch)
-        const char* e = measure_env("ALSK_TS_BW");
-        return e ? std::atoi(e) : 8;
-    }();
-    if (bw == 16 && packed_solve16(packed, count, f, x, st, status_off, s)) return true;
     launch_solve(packed, count, f, x, st, status_off, s);
     return true;
 }
