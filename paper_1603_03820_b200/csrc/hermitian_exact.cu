@@ -19,7 +19,7 @@
 namespace alsk {
 namespace {
 
-constexpr int kChunk = 32;  // nonzeros staged per shared-memory tile
+constexpr int kChunk = 64;  // nonzeros staged per shared-memory tile
 
 // Lower-triangular tile enumeration: t -> (bi, bj), bj <= bi, row-major.
 __device__ __forceinline__ void tile_coords(int t, int& bi, int& bj) {
@@ -83,6 +83,7 @@ __global__ void herm_mat_kernel(const int64_t* __restrict__ row_ptr,
         }
         __syncthreads();
         if (active) {
+#pragma unroll 4
             for (int kk = 0; kk < cnt; ++kk) {
                 const float* trow = tile + kk * fp;
                 Acc a[TB], b[TB];
