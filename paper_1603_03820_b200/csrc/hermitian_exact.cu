@@ -150,8 +150,9 @@ __global__ void check_columns_kernel(const int64_t* __restrict__ row_ptr,
 // Back substitution does not run here: it is one serial chain of f(f-1)/2 subtractions per
 // system (the reference's order), which would hold the whole CTA. The kernel hands each
 // system to backsub_exact_kernel instead, through `work` (subst_stride(f) doubles per
-// system): y (f doubles), then for i = f-1 down to 0 the diagonal L[i][i] followed by
-// L[j][i], j = i+1..f-1 -- the order the substitution consumes them. A system that needs no
+// system): b (f doubles), then for i = f-1 down to 0 the diagonal L[i][i] followed by
+// L[j][i], j = i+1..f-1 -- column i of L, read in ascending column order by the forward
+// substitution and in the stored order by the back substitution. A system that needs no
 // substitution (all-zero or broken; x already written) gets 0 as its first diagonal.
 // Element e of system t sits at subst_at(t, e): interleaved by 32 systems, so the
 // substitution warp's loads of one element are a single 256-byte access.
@@ -166,8 +167,8 @@ __device__ __forceinline__ int64_t subst_at(int64_t t, int64_t e, int64_t per) {
 // register (no trailing-matrix stores); the diagonal row checks s > 0 and every thread takes
 // the square root, the other rows divide. L is held column-major packed (column t = rows
 // t..f-1, contiguous), so a warp's l_rt loads are consecutive doubles and l_ct is a
-// broadcast. The forward substitution (solver.hpp:249-253) rides one column behind on the
-// last thread: y_{c-1} needs row c-1 of L (final once column c-1 is) and y_0..y_{c-2}.
+// broadcast. Both substitutions run in backsub_exact_kernel (a single lane's chain here cost
+// 11% of this kernel's time in shared-memory wavefronts and issue slots).
 constexpr int SE_U = 8;  // dot products formed ahead of their in-order subtractions
 
 __global__ void solve_exact_kernel(const float* __restrict__ A, const float* __restrict__ Bv,
@@ -188,7 +189,7 @@ __global__ void solve_exact_kernel(const float* __restrict__ A, const float* __r
 #endif
     extern __shared__ double sm[];
     double* L = sm;                    // f(f+1)/2, column-major packed: l_rt at colstart(t) + r
-    double* y = L + f * (f + 1) / 2;   // f: b, overwritten by the forward solution
+    double* y = L + f * (f + 1) / 2;   // f: b (as double)
     double* piv = y + f;               // the current column's pivot
     const int64_t row = blockIdx.x;
     const float* a = A + row * static_cast<int64_t>(f) * f;
@@ -218,16 +219,6 @@ __global__ void solve_exact_kernel(const float* __restrict__ A, const float* __r
     }
 
     SE_LAP(0)
-    const int ythr = nt - 1;
-    auto forward = [&](int i) {  // y_i = (b_i - sum_{j<i} l_ij y_j) / l_ii, j ascending
-        double acc = y[i];
-        int off = 0;
-        for (int j = 0; j < i; ++j) {
-            acc = __dsub_rn(acc, __dmul_rn(L[off + i], y[j]));
-            off += f - 1 - j;
-        }
-        y[i] = __ddiv_rn(acc, L[off + i]);
-    };
     bool broke = false;
     for (int c = 0; c < f; ++c) {
         for (int r = c + tid; r < f; r += nt) {
@@ -251,7 +242,6 @@ __global__ void solve_exact_kernel(const float* __restrict__ A, const float* __r
             if (r == c) *piv = acc;
             else L[colstart(c) + r] = acc;
         }
-        if (tid == ythr && c > 0) forward(c - 1);
         __syncthreads();
         const double d = *piv;
         if (!(d > 0.0)) {  // CTA-uniform
@@ -274,11 +264,10 @@ __global__ void solve_exact_kernel(const float* __restrict__ A, const float* __r
         if (tid == 0) work[subst_at(row, f, per)] = 0.0;
         return;
     }
-    if (tid == ythr) forward(f - 1);
     if (tid == 0) column[row] = 0;
     __syncthreads();
     SE_LAP(2)
-    // hand off to backsub_exact_kernel: y, then per row i (descending) the diagonal and
+    // hand off to backsub_exact_kernel: b, then per column i (descending) the diagonal and
     // column i below it -- one contiguous run of the column-major L
     double* wk = work + subst_at(row, 0, per);
     for (int i = tid; i < f; i += nt) wk[32 * i] = y[i];
@@ -293,41 +282,57 @@ __global__ void solve_exact_kernel(const float* __restrict__ A, const float* __r
 #undef SE_LAP
 }
 
-// Back substitution, one thread per system (solver.hpp:254-259): for i = f-1 down to 0,
-// x_i = float((y_i - sum_{j>i} L[j][i] * double(x_j)) / L[i][i]), the sum subtracted in
-// ascending j, each product and difference rounded separately -- the reference's order,
-// inherently one chain per system, so systems run side by side (thousands per SM) instead
-// of on one thread of a CTA. x lives in shared memory, [j][thread] (conflict-free).
-__global__ void __launch_bounds__(128) backsub_exact_kernel(const double* __restrict__ work, int f, int64_t count,
-                                                            float* __restrict__ X) {
-    extern __shared__ float xsh[];
+// Forward and back substitution, one thread per system (solver.hpp:249-259), each a chain
+// the reference's order makes serial: y_i = (b_i - sum_{j<i} l_ij y_j) / l_ii with the
+// subtractions in ascending j (applied column by column: for j ascending, y_j = s_j / l_jj,
+// then s_i -= l_ij y_j for i > j -- the same per-entry order), then for i = f-1 down to 0
+// x_i = float((y_i - sum_{j>i} l_ji double(x_j)) / l_ii), ascending j, each product and
+// difference rounded separately. Systems run side by side (thousands per SM) instead of on
+// one thread of a CTA. s/y/x live in one shared-memory array, [i][thread] (conflict-free):
+// x_j overwrites y_j once y_j is consumed.
+constexpr int BS_THREADS = 64;
+constexpr int BS_G = 8;  // back-substitution products formed per group (16, and grouping the
+                          // forward updates, measured slower)
+__global__ void __launch_bounds__(BS_THREADS) backsub_exact_kernel(const double* __restrict__ work, int f, int64_t count,
+                                                                   float* __restrict__ X) {
+    extern __shared__ double ysh[];
     const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (t >= count) return;
     const int64_t per = subst_stride(f);
-    const double* y = work + subst_at(t, 0, per);  // element e at y[32 * e]
-    const double* u = y + 32 * f;
-    if (!(u[0] > 0.0)) return;  // all-zero or broken system: x already written
-    float* xs = xsh + threadIdx.x;
+    const double* b = work + subst_at(t, 0, per);  // element e at b[32 * e]
+    const double* cols = b + 32 * f;                 // column f-1 first
+    if (!(cols[0] > 0.0)) return;  // all-zero or broken system: x already written
+    double* ys = ysh + threadIdx.x;
     const int bd = blockDim.x;
+    for (int i = 0; i < f; ++i) ys[i * bd] = b[32 * i];
+    // forward: column j starts (f-1-j)(f-j)/2 elements into the column stream
+    for (int j = 0; j < f; ++j) {
+        const double* c = cols + 32 * ((static_cast<int64_t>(f - 1 - j) * (f - j)) / 2);
+        const double yj = __ddiv_rn(ys[j * bd], c[0]);
+        ys[j * bd] = yj;
+        for (int i = j + 1; i < f; ++i) ys[i * bd] = __dsub_rn(ys[i * bd], __dmul_rn(c[32 * (i - j)], yj));
+    }
+    // back substitution over the stream in stored order (column f-1 first)
+    const double* u = cols;
     for (int i = f - 1; i >= 0; --i) {
         const double d = u[0];
-        double acc = y[32 * i];
+        double acc = ys[i * bd];
         const double* c = u + 32;
         const int n = f - 1 - i;
         int k = 0;
-        for (; k + 8 <= n; k += 8) {  // products formed ahead; only the subtractions chain
-            double p[8];
+        for (; k + BS_G <= n; k += BS_G) {  // products formed ahead; only the subtractions chain
+            double p[BS_G];
 #pragma unroll
-            for (int q = 0; q < 8; ++q) p[q] = __dmul_rn(c[32 * (k + q)], static_cast<double>(xs[(i + 1 + k + q) * bd]));
+            for (int q = 0; q < BS_G; ++q) p[q] = __dmul_rn(c[32 * (k + q)], ys[(i + 1 + k + q) * bd]);
 #pragma unroll
-            for (int q = 0; q < 8; ++q) acc = __dsub_rn(acc, p[q]);
+            for (int q = 0; q < BS_G; ++q) acc = __dsub_rn(acc, p[q]);
         }
-        for (; k < n; ++k) acc = __dsub_rn(acc, __dmul_rn(c[32 * k], static_cast<double>(xs[(i + 1 + k) * bd])));
-        xs[i * bd] = static_cast<float>(__ddiv_rn(acc, d));
+        for (; k < n; ++k) acc = __dsub_rn(acc, __dmul_rn(c[32 * k], ys[(i + 1 + k) * bd]));
+        ys[i * bd] = static_cast<double>(static_cast<float>(__ddiv_rn(acc, d)));
         u += 32 * (n + 1);
     }
     float* x = X + t * f;
-    for (int i = 0; i < f; ++i) x[i] = xs[i * bd];
+    for (int i = 0; i < f; ++i) x[i] = static_cast<float>(ys[i * bd]);
 }
 
 }  // namespace
@@ -422,8 +427,8 @@ void solve_exact(const float* A, const float* B, int64_t count, int f, bool /*ze
     const int64_t per = subst_stride(f);
     const int64_t chunk = std::max<int64_t>(32, std::min<int64_t>(1LL << 30, (int64_t{4} << 30) / (per * 8)) & ~int64_t{31});
     DevBuf work(sizeof(double) * per * ((std::min(count, chunk) + 31) & ~int64_t{31}), s);
-    constexpr int BT = 128;
-    const size_t bsmem = static_cast<size_t>(BT) * f * sizeof(float);
+    constexpr int BT = BS_THREADS;
+    const size_t bsmem = static_cast<size_t>(BT) * f * sizeof(double);
     ALSK_CUDA(cudaFuncSetAttribute(backsub_exact_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsmem));
     for (int64_t b0 = 0; b0 < count; b0 += chunk) {
         const int64_t n = std::min<int64_t>(count - b0, chunk);
@@ -445,7 +450,7 @@ void solve_exact(const float* A, const float* B, int64_t count, int f, bool /*ze
             unsigned long long h[4];
             d2h(h, pb.as<unsigned long long>(), 4, s);
             ALSK_CUDA(cudaStreamSynchronize(s));
-            std::fprintf(stderr, "[se-prof f=%d systems=%lld threads=%d] kcyc per system: load %.1f factor+forward %.1f last row %.1f hand-off %.1f\n",
+            std::fprintf(stderr, "[se-prof f=%d systems=%lld threads=%d] kcyc per system: load %.1f factor %.1f - %.1f hand-off %.1f\n",
                          f, static_cast<long long>(n), threads, h[0] / 1e3 / n, h[1] / 1e3 / n, h[2] / 1e3 / n,
                          h[3] / 1e3 / n);
         }
