@@ -439,10 +439,21 @@ alsk_status alsk_update_x(const alsk_csr* r, const float* theta, int64_t theta_r
         // the last range's download are exposed, and both are small.
         static constexpr double kPipeCuts[] = {0.0, 1.0 / 64, 3.0 / 64, 6.0 / 64, 11.0 / 64, 19.0 / 64, 31.0 / 64,
                                                43.0 / 64, 53.0 / 64, 59.0 / 64, 62.0 / 64, 1.0};
-        constexpr int kPipeRanges = sizeof(kPipeCuts) / sizeof(kPipeCuts[0]) - 1;
+        std::vector<double> fr(std::begin(kPipeCuts), std::end(kPipeCuts));
+        if (const char* e = measure_env("ALSK_PIPE_CUTS")) {  // A/B: "n1,n2,...,64" in 64ths
+            fr.assign(1, 0.0);
+            for (const char* q = e; *q;) {
+                char* end = nullptr;
+                const double v = std::strtod(q, &end);
+                if (end == q) break;
+                fr.push_back(v / 64.0);
+                q = *end ? end + 1 : end;
+            }
+        }
+        const int kPipeRanges = static_cast<int>(fr.size()) - 1;
         std::vector<int64_t> cut{0};
         for (int k = 1; k < kPipeRanges; ++k) {
-            const int64_t want = static_cast<int64_t>(kPipeCuts[k] * static_cast<double>(nnz));
+            const int64_t want = static_cast<int64_t>(fr[k] * static_cast<double>(nnz));
             const int64_t row = std::lower_bound(r->row_ptr, r->row_ptr + m + 1, want) - r->row_ptr;
             if (row > cut.back() && row < m) cut.push_back(row);
         }

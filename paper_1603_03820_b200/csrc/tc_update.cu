@@ -121,9 +121,10 @@ __device__ __forceinline__ void tma_gather4(uint32_t dst, const CUtensorMap* map
         : "memory");
 }
 
-// spin (ns == 0) or nanosleep back-off
+// spin (ns == 0), park in try_wait with a suspend-time hint (ns == 1) or nanosleep back-off
 __device__ __forceinline__ void tc_wait(uint64_t* bar, uint32_t parity, uint32_t ns) {
     if (ns == 0) mbar_wait(bar, parity);
+    else if (ns == 1) mbar_wait_park(bar, parity);
     else mbar_wait_sleep(bar, parity, ns);
 }
 
@@ -348,7 +349,7 @@ tc_update_kernel(const __grid_constant__ CUtensorMap theta_map, int ldt, const i
                 const uint32_t ph = ring_ph;
                 {
                     TP(t0);
-                    mbar_wait_sleep(&raw_empty[s], ph ^ 1u, load_sleep);
+                    tc_wait(&raw_empty[s], ph ^ 1u, load_sleep);
                     TA(t0, 0);
                 }
                 if (ldr == 0) {
@@ -538,7 +539,7 @@ tc_update_kernel(const __grid_constant__ CUtensorMap theta_map, int ldt, const i
                 TP(t0);
                 // long, latency-tolerant wait (the group has the other group's row as slack):
                 // back off so the spinning does not take issue slots from the split warps
-                mbar_wait_sleep(&tfull[2 * g + b], use[b] & 1u, epi_sleep);
+                tc_wait(&tfull[2 * g + b], use[b] & 1u, epi_sleep);
                 TA(t0, 4);
                 ++use[b];
                 tc_fence_after();
