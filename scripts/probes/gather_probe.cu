@@ -1,4 +1,8 @@
 // Bring-up probe (not part of the library): gathered-row copy rate into shared memory.
+// NOTE (round 2): its ~46-50 cycles per row for every mechanism was an artifact of this
+// harness (one CTA per SM, one mbarrier and a CTA barrier per chunk); l2bw_probe.cu
+// measures the same copies with many warps: 17 B/clk per SM for lane = rating cp.async,
+// 38-45 for lane = piece cp.async, 67 for TMA tile::gather4.
 // Each CTA (one per SM) repeatedly stages 32 random rows of 400 B (f=100 floats) from a
 // table of `rows` rows into a 4-deep ring, with W issuing warps, by one of:
 //  0: cp.async 16 B, lane = rating (25 instructions per chunk)
