@@ -509,6 +509,23 @@ __device__ __forceinline__ void small_chol_solve(float* a, float* b, bool writer
 }
 
 
+// Factor-row loads of the small-rank kernel (read-only path) with a 64-byte L2 prefetch
+// size (`.L2::64B`): a 40-byte row at a 40-byte stride otherwise pulls whole 128-byte lines
+// from DRAM (SparkALS Theta half: 528 -> 328 GB read per launch; time unchanged, the kernel
+// is latency-bound).
+#ifndef SMALL_L2_64B
+#define SMALL_L2_64B 1
+#endif
+__device__ __forceinline__ float2 ld_row2(const float2* p) {
+#if SMALL_L2_64B
+    float2 v;
+    asm volatile("ld.global.nc.L2::64B.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "l"(p));
+    return v;
+#else
+    return __ldg(p);
+#endif
+}
+
 template <int F, bool WARP, bool PARTIAL>
 __global__ void __launch_bounds__(128)
 small_update_kernel(const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col_idx,
@@ -535,14 +552,28 @@ small_update_kernel(const int64_t* __restrict__ row_ptr, const int32_t* __restri
     // sums keep the one-rating-at-a-time order.
     constexpr int SU = F <= 12 ? 4 : 2;
     constexpr int64_t step = WARP ? 32 : 1;
+    // The next round's indices and ratings are loaded while this round's rows arrive and
+    // multiply, so a round waits for one load latency instead of two.
+    int nv[SU];
+    float nr[SU];
+#pragma unroll
+    for (int j = 0; j < SU; ++j) {
+        const int64_t kj = k0 + lane + j * step;
+        const bool ok = kj < k1;
+        nv[j] = ok ? __ldg(col_idx + kj) - static_cast<int>(col_lo) : 0;
+        nr[j] = ok ? __ldg(values + kj) : 0.f;
+    }
     for (int64_t k = k0 + lane; k < k1; k += SU * step) {
         int vv[SU];
         float rr[SU];
 #pragma unroll
         for (int j = 0; j < SU; ++j) {
-            const bool ok = k + j * step < k1;
-            vv[j] = ok ? __ldg(col_idx + k + j * step) - static_cast<int>(col_lo) : 0;
-            rr[j] = ok ? __ldg(values + k + j * step) : 0.f;
+            vv[j] = nv[j];
+            rr[j] = nr[j];
+            const int64_t kj = k + (SU + j) * step;
+            const bool ok = kj < k1;
+            nv[j] = ok ? __ldg(col_idx + kj) - static_cast<int>(col_lo) : 0;
+            nr[j] = ok ? __ldg(values + kj) : 0.f;
         }
         // the caller's rows in place (no padded copy): 16-, 8- or 4-byte loads by F's alignment
         float th[SU][4 * NQ];
@@ -559,7 +590,8 @@ small_update_kernel(const int64_t* __restrict__ row_ptr, const int32_t* __restri
             } else if constexpr (F % 2 == 0) {
 #pragma unroll
                 for (int q = 0; q < F / 2; ++q) {
-                    const float2 w = ok ? __ldg(reinterpret_cast<const float2*>(src) + q) : make_float2(0.f, 0.f);
+                    float2 w = make_float2(0.f, 0.f);
+                    if (ok) w = ld_row2(reinterpret_cast<const float2*>(src) + q);
                     th[j][2 * q] = w.x, th[j][2 * q + 1] = w.y;
                 }
             } else {
