@@ -651,8 +651,18 @@ CUtensorMap factor_rows_map(const float* theta, int64_t theta_rows, int ldt) {
     const cuuint64_t dims[2] = {static_cast<cuuint64_t>(ldt), static_cast<cuuint64_t>(rows)};
     const cuuint64_t strides[1] = {static_cast<cuuint64_t>(ldt) * 4};
     const cuuint32_t box[2] = {static_cast<cuuint32_t>(ldt), 1}, es[2] = {1, 1};
+    // L2 promotion of the gathered rows: 64 B reads the fewest DRAM bytes (Netflix Theta half,
+    // X gathered from HBM: 24.5 GB at 256 B, 23.0 at none or 128, 21.8 at 64; same time).
+    // A/B: ALSK_TC_L2PROMO = 0 (none), 64, 128, 256
+    static const CUtensorMapL2promotion promo = [] {
+        const char* e = measure_env("ALSK_TC_L2PROMO");
+        const int v = e ? std::atoi(e) : 64;
+        return v == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE
+                      : v == 64 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+                                : v == 128 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+    }();
     const CUresult rc = encode(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), dims, strides, box, es,
-                               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, promo,
                                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (rc != CUDA_SUCCESS) throw Failure(ALSK_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string(static_cast<int>(rc)) + ")");
     return m;
