@@ -268,3 +268,28 @@ def test_tc_error_order_matches_reference(A, ref, gpu, batch_rows):
     else:
         assert "cholesky breakdown at batch index 1" in msg and isinstance(e.value, A.NumericalError)
         assert str(e.value).startswith("cholesky breakdown at batch index 1")
+
+
+@pytest.mark.parametrize("f", [16, 100])
+def test_tc_update_x_factor_without_rows(A, orc, gpu, f):
+    """A matrix of zero columns (every row empty) with a 0-row factor: the TMA row map then
+    points at a zeroed dummy row and every row solves to zero, as in the reference."""
+    m = 300
+    r = A.CsrMatrix(m, 0, 0, np.zeros(m + 1, np.int64), np.zeros(0, np.int32), np.zeros(0, np.float32))
+    th = A.random_factor(0, f, 3)
+    x = tc_update(A, r, th, f, 0.05)
+    assert x.entries.size == m * f
+    assert not np.any(x.entries)
+
+
+def test_tc_update_x_partial_groups(A, orc, gpu):
+    """Row lengths 1..40: every remainder of the 4-row TMA gather groups and of the 8-rating
+    k-groups (padding rows gathered past the map arrive as zeros)."""
+    f, n = 100, 300
+    lengths = [1 + (u % 40) for u in range(600)]
+    r = rows_with_lengths(A, lengths, n, 11)
+    th = A.random_factor(n, f, 12)
+    st, xo = orc.update_x(ocsr(r), th.entries, n, f, 0.05, acc_double=1)
+    assert st == 0
+    x = tc_update(A, r, th, f, 0.05)
+    assert normwise_gap(x.entries, xo) <= FP32_TOL
