@@ -4,9 +4,10 @@
 // bit: every A/B entry is one thread's sequential double sum over the row's nonzeros in
 // ascending order (a float*float product is exact in double, so FMA vs mul+add cannot
 // differ), lambda*n_u is added last on the diagonal and the result rounded once to float
-// (solver.hpp:99-157). The Cholesky is right-looking, but each entry still receives its
-// updates in ascending column order with separately rounded multiply and subtract, which
-// is exactly the left-looking order of batch_solve_into (solver.hpp:223-246).
+// (solver.hpp:99-157). The Cholesky is left-looking like batch_solve_into (solver.hpp:
+// 223-246): each entry's sum in ascending column order with separately rounded multiply and
+// subtract; the forward and back substitutions (solver.hpp:249-259) run one thread per
+// system in the same order.
 #include <cuda_runtime.h>
 
 #include <cstdint>
