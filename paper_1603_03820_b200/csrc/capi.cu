@@ -1432,6 +1432,11 @@ __global__ void ooc_add_rows_kernel(float* __restrict__ acc, const float* __rest
         reinterpret_cast<float4*>(acc)[k] = a;
     }
 }
+// flag[0] = first out-of-slab entry of a block (~0 if none); copies that entry's column into
+// flag[1] while the block is still resident, so the error can be raised after it is released
+__global__ void ooc_bad_column_kernel(const int32_t* __restrict__ col_idx, unsigned long long* flag) {
+    if (flag[0] != ~0ull) flag[1] = static_cast<unsigned long long>(static_cast<int64_t>(col_idx[flag[0]]));
+}
 }  // namespace alsk
 
 // One half-sweep over a persisted p x q grid (persist_grid, dataio.hpp:381-400) whose blocks
@@ -1471,7 +1476,12 @@ alsk_status alsk_ooc_update(const char* grid_dir, const float* factor, int64_t f
             part.alloc(sizeof(float) * pkn * lr_max, s);
         }
         DeviceBlockStream bs(grid_dir, order);
+        // per block of a partition: first out-of-slab entry and its column, checked on the
+        // device; read back once per partition (no host round trip per block)
+        DevBuf flags(sizeof(unsigned long long) * 2 * static_cast<size_t>(p), s);
+        std::vector<unsigned long long> hflags(2 * static_cast<size_t>(p));
         for (int j = 0; j < q; ++j) {
+            ALSK_CUDA(cudaMemsetAsync(flags.as<void>(), 0xff, sizeof(unsigned long long) * 2 * p, s));
             const int64_t r0 = g.row_cuts[j], lr = g.row_cuts[j + 1] - r0;
             const auto cuts = slice_cuts(lr, p);
             std::vector<DevBuf> pa, pb;
@@ -1489,11 +1499,16 @@ alsk_status alsk_ooc_update(const char* grid_dir, const float* factor, int64_t f
                 const DevCsr v{o.rows, o.cols, o.col_offset, o.nnz, o.row_ptr, o.col_idx, o.values};
                 const int64_t lo = g.col_cuts[i], width = g.col_cuts[i + 1] - lo;
                 if (lr == 0) continue;
-                // the block's columns against its slab, with the reference's message (blocks are
-                // large here, so the round trip is cheap next to their Hermitians)
-                check_columns(v, 0, lr, lo, lo + width, s);
+                // the block's columns against its slab, resolved with the partition's statuses
+                unsigned long long* fl = flags.as<unsigned long long>() + 2 * i;
+                check_columns_async(v, 0, o.nnz, lo, lo + width, fl, s);
+                ooc_bad_column_kernel<<<1, 1, 0, s>>>(v.col_idx, fl);
+                ALSK_LAUNCHED();
                 const float* slab = factor + lo * f;
                 if (tc) {
+                    // block i's packed partial rows, added into the partition's running rows by a
+                    // streaming kernel (FP32, the blocks in order; adding in the Hermitian's
+                    // epilogue instead measured 1.5x slower: a dependent load per packed block)
                     hermitian_packed_tc(v, slab, width, f, static_cast<float>(cfg->lambda), 0, lr,
                                         i == 0 ? acc.as<float>() : part.as<float>(), s);
                     if (i > 0) {
@@ -1510,6 +1525,15 @@ alsk_status alsk_ooc_update(const char* grid_dir, const float* factor, int64_t f
                 }
             }
             if (lr == 0) continue;
+            // the partition's column errors in block order, before anything of it is solved
+            // (the reference's worker assembles partition j block by block, then solves it)
+            d2h(hflags.data(), flags.as<unsigned long long>(), 2 * static_cast<size_t>(p), s);
+            ALSK_CUDA(cudaStreamSynchronize(s));
+            for (int i = 0; i < p; ++i)
+                if (hflags[2 * i] != ~0ull)
+                    fail_input("column " + std::to_string(static_cast<int64_t>(hflags[2 * i + 1])) +
+                               " outside partition [" + std::to_string(g.col_cuts[i]) + ", " +
+                               std::to_string(g.col_cuts[i + 1]) + ")");
             std::vector<StatusBufs> status;
             status.reserve(p);
             if (tc) {
